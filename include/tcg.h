@@ -1,0 +1,140 @@
+/*
+ * tcg.h — C ABI of the B200-native TC-GNN hot path (libtcg_b200.so).
+ *
+ * Every entry point takes plain device pointers, int64 sizes and a
+ * cudaStream_t (passed as void* so this header needs no CUDA include); it is
+ * stream-ordered, never allocates or frees caller memory, never throws across
+ * the ABI and returns 0 on success or a negative TCG_E* code; tcg_last_error()
+ * gives the thread-local message of the last failure. Outputs are written
+ * only; callers allocate them (the torch caching allocator in the Python
+ * host layer). Nothing here falls back to the CPU.
+ *
+ * Each entry point replaces one function of the reference package `tcgraph`
+ * (/root/reference/pkg/src/tcgraph, numpy emulation, no native code); the
+ * reference interface it stands in for is cited per function. INTEGRATION.md
+ * shows the ctypes binding the reference would add for each symbol.
+ */
+#ifndef TCG_B200_H
+#define TCG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TCG_OK 0
+#define TCG_E_INVALID (-1)   /* bad argument (shape, null pointer, mode)   */
+#define TCG_E_CUDA (-2)      /* CUDA launch / runtime error                */
+#define TCG_E_WORKSPACE (-3) /* workspace too small                        */
+#define TCG_E_UNSUPPORTED (-4)
+
+#define TCG_PREC_F32 0  /* exact f32: CSR-order fold, bitwise = reference f32 */
+#define TCG_PREC_TF32 1 /* tensor cores: RNE-to-tf32 operands, f32 accumulate */
+
+/* SDDMM epilogues (fused per row window; rows never straddle windows). */
+#define TCG_EPI_NONE 0        /* out[e] = <xa[row e], xb[col e]>                 */
+#define TCG_EPI_SOFTMAX 1     /* out[e] = row softmax of the scores               */
+#define TCG_EPI_SOFTMAX_BWD 2 /* out[e] = P_e (s_e - sum_row P s), P = aux        */
+
+/* Device-resident SGT result (reference TiledGraph, sgt.py:43-98) plus the
+ * CSR it was built from. All pointers are device pointers. */
+typedef struct tcg_tiling {
+  int64_t num_nodes;            /* N                                         */
+  int64_t num_edges;            /* M                                         */
+  int64_t num_windows;          /* W = ceil(N / blk_h)                        */
+  int64_t num_unique;           /* U = col_offsets[W]                         */
+  int32_t blk_h, blk_w;         /* BlockConfig (sgt.py:21-40)                 */
+  const int64_t* node_ptr;      /* i64[N+1]  CsrGraph.node_pointer            */
+  const uint32_t* edge_list;    /* u32[M]    CsrGraph.edge_list               */
+  const uint32_t* edge_to_col;  /* u32[M]    TiledGraph.edge_to_col           */
+  const int64_t* col_offsets;   /* i64[W+1]  TiledGraph.col_offsets           */
+  const uint32_t* col_to_node;  /* u32[U]    TiledGraph.col_to_node           */
+  const uint32_t* win_partition;/* u32[W]    TiledGraph.win_partition         */
+} tcg_tiling;
+
+/* ---- library ---------------------------------------------------------- */
+const char* tcg_last_error(void);
+const char* tcg_version(void);
+/* Number of kernels this library has launched in this process (all entry
+ * points; a CUDA-graph replay of captured launches is not re-counted). */
+int64_t tcg_launch_count(void);
+/* Multiprocessor count / L2 bytes of the current device (0 if unavailable). */
+int tcg_device_info(int64_t* num_sms, int64_t* l2_bytes);
+
+/* ---- SGT: reference sgt.translate (sgt.py:101-137) ---------------------- */
+/* Workspace bytes tcg_sgt needs for this graph size. */
+size_t tcg_sgt_workspace_bytes(int64_t num_nodes, int64_t num_edges, int32_t blk_h);
+/* One stream-ordered call: per-window sort/dedup/rank on the GPU.
+ * Writes win_partition[W], edge_to_col[M], col_offsets[W+1] and
+ * col_to_node[0..U) where U = col_offsets[W] (col_to_node capacity must be
+ * >= M). Bit-exact with the reference for any blk_h, blk_w >= 1. */
+int tcg_sgt(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_nodes,
+            int64_t num_edges, int32_t blk_h, int32_t blk_w, uint32_t* win_partition,
+            uint32_t* edge_to_col, int64_t* col_offsets, uint32_t* col_to_node,
+            void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- CSR transpose (backward support; no reference counterpart — the
+ * reference has no backward. SURVEY.md Appendix B restates it as
+ * CsrGraph.from_edges(dst, src), graph.py:55-89) ------------------------ */
+size_t tcg_csr_transpose_workspace_bytes(int64_t num_nodes, int64_t num_edges);
+/* ptr_t[N+1], cols_t[M] = A^T in CSR; perm[k] = edge of A that is edge k of
+ * A^T (stable by row => equals np.lexsort((rows, cols))). */
+int tcg_csr_transpose(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_nodes,
+                      int64_t num_edges, int64_t* ptr_t, uint32_t* cols_t, uint32_t* perm,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- SpMM: reference kernels.spmm (kernels.py:213-374, Alg. 2) ----------- */
+/* Y[r - y_row0, :] (+)= sum_e w_e * X[col e, :] for rows r of windows
+ * [win_begin, win_end), D columns, bias added if non-null.
+ *  weights   : nullable f32[M] edge weights (null => 1.0);
+ *  weight_idx: nullable u32[M] indirection (w_e = weights[weight_idx[e]]),
+ *              used to read A's edge weights in A^T edge order;
+ *  x2/weights2/weight_idx2: optional second term accumulated into the same
+ *              tile (Y = A_w X + A_w2 X2), used by the AGNN backward;
+ *  accumulate: 0 => overwrite Y rows, 1 => Y += result.
+ * precision TCG_PREC_F32 is bitwise equal to the reference f32 path
+ * (oracle.ref_spmm fold order); TCG_PREC_TF32 uses mma.sync m16n8k8 tf32. */
+int tcg_spmm(const tcg_tiling* t, const float* x, int64_t ldx, int64_t dim,
+             const float* weights, const uint32_t* weight_idx, const float* x2, int64_t ldx2,
+             const float* weights2, const uint32_t* weight_idx2, const float* bias,
+             float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
+             int32_t precision, int32_t accumulate, void* stream);
+
+/* ---- SDDMM: reference kernels.sddmm (kernels.py:377-538, Alg. 3) --------- */
+/* out[e] = <xa[row e], xb[col e]> for the edges e of windows
+ * [win_begin, win_end); xb may equal xa (or be null => xa). Edge-indexed
+ * arrays (out, aux, spmm weights) are addressed by absolute edge id: a shard
+ * holding only edges [eb, ee) passes base - eb.
+ * epilogue TCG_EPI_SOFTMAX fuses kernels.segment_softmax (kernels.py:541-556);
+ * TCG_EPI_SOFTMAX_BWD reads aux = P (same indexing) and writes
+ * P*(s - sum_row P*s). */
+int tcg_sddmm(const tcg_tiling* t, const float* xa, int64_t lda, const float* xb, int64_t ldb,
+              int64_t dim, const float* aux, float* out, int64_t win_begin, int64_t win_end,
+              int32_t precision, int32_t epilogue, void* stream);
+
+/* ---- segment softmax: reference kernels.segment_softmax (541-556) ------- */
+int tcg_segment_softmax(const int64_t* node_ptr, int64_t num_rows, const float* values,
+                        float* out, void* stream);
+/* dS = P * (dP - rowsum(P * dP)) (backward; no reference counterpart). */
+int tcg_segment_softmax_backward(const int64_t* node_ptr, int64_t num_rows, const float* p,
+                                 const float* dp, float* ds, void* stream);
+
+/* ---- fused AGNN layer: reference kernels.agnn_layer (586-601) ----------- */
+/* One CTA per window: gather the window's neighbour rows of Z once into
+ * shared memory, SDDMM -> row softmax -> weighted SpMM from the same tile.
+ * Writes P[M] (edge order, needed by the backward) and Y rows.
+ * Falls back to the unfused sequence for windows too large for shared
+ * memory (same kernels, same results). TF32 only. */
+int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim, float* p,
+                     float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
+                     void* stream);
+
+/* ---- TF32 operand rounding: reference tiles.quantize_tf32 (67-82) ------- */
+int tcg_quantize_tf32(const float* in, float* out, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCG_B200_H */

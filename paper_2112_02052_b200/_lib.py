@@ -1,0 +1,108 @@
+"""ctypes binding of the C ABI in include/tcg.h (libtcg_b200.so).
+
+The library is the only compute path: if it is missing or cannot be loaded,
+every entry point raises — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("TCG_B200_LIB", _PKG / "libtcg_b200.so"))
+
+TCG_OK = 0
+PREC_F32 = 0
+PREC_TF32 = 1
+EPI_NONE = 0
+EPI_SOFTMAX = 1
+EPI_SOFTMAX_BWD = 2
+
+
+class TcgTiling(C.Structure):
+    """Mirror of `tcg_tiling` (include/tcg.h)."""
+
+    _fields_ = [
+        ("num_nodes", C.c_int64),
+        ("num_edges", C.c_int64),
+        ("num_windows", C.c_int64),
+        ("num_unique", C.c_int64),
+        ("blk_h", C.c_int32),
+        ("blk_w", C.c_int32),
+        ("node_ptr", C.c_void_p),
+        ("edge_list", C.c_void_p),
+        ("edge_to_col", C.c_void_p),
+        ("col_offsets", C.c_void_p),
+        ("col_to_node", C.c_void_p),
+        ("win_partition", C.c_void_p),
+    ]
+
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_I32 = C.c_int32
+_SZ = C.c_size_t
+
+# symbol -> (restype, argtypes); the exact set include/tcg.h declares
+SIGNATURES = {
+    "tcg_last_error": (C.c_char_p, []),
+    "tcg_version": (C.c_char_p, []),
+    "tcg_launch_count": (_I64, []),
+    "tcg_device_info": (C.c_int, [C.POINTER(_I64), C.POINTER(_I64)]),
+    "tcg_sgt_workspace_bytes": (_SZ, [_I64, _I64, _I32]),
+    "tcg_sgt": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
+    "tcg_csr_transpose_workspace_bytes": (_SZ, [_I64, _I64]),
+    "tcg_csr_transpose": (C.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P, _SZ, _P]),
+    "tcg_spmm": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P,
+                           _P, _I64, _I64, _I64, _I64, _I32, _I32, _P]),
+    "tcg_sddmm": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _P, _I64, _I64, _P, _P, _I64, _I64,
+                            _I32, _I32, _P]),
+    "tcg_segment_softmax": (C.c_int, [_P, _I64, _P, _P, _P]),
+    "tcg_segment_softmax_backward": (C.c_int, [_P, _I64, _P, _P, _P, _P]),
+    "tcg_agnn_forward": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _I64, _P, _P, _I64, _I64,
+                                   _I64, _I64, _P]),
+    "tcg_quantize_tf32": (C.c_int, [_P, _P, _I64, _P]),
+}
+
+_lib = None
+_load_error: str | None = None
+
+
+def load() -> C.CDLL:
+    """Load (once) and type the library; raise loudly if it is unavailable."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        _load_error = (f"{LIB_PATH} not found: build it with "
+                       "`python -m paper_2112_02052_b200._build` (no CPU fallback exists)")
+        raise RuntimeError(_load_error)
+    lib = C.CDLL(str(LIB_PATH))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class TcgError(RuntimeError):
+    pass
+
+
+def check(rc: int, what: str) -> None:
+    if rc != TCG_OK:
+        msg = load().tcg_last_error().decode(errors="replace")
+        if rc == -1:
+            raise ValueError(msg)
+        raise TcgError(f"{what} failed ({rc}): {msg}")
+
+
+def launch_count() -> int:
+    return int(load().tcg_launch_count())
+
+
+def version() -> str:
+    return load().tcg_version().decode()

@@ -1,0 +1,183 @@
+"""torch.autograd layers over the B200 kernels: GCNConv / AGNNConv and the
+two models of the paper's evaluation.
+
+The reference has forward functions only (gcn_layer, agnn_layer,
+kernels.py:559-601; backprop is a non-goal there). The layers
+here keep those forward semantics and add the backward passes:
+
+  GCNConv(X)  = A (X W) + b            (update-first reordering of
+                                         gcn_layer's (A X) W + b: same maths,
+                                         fp32 reassociation only)
+      dH = A^T G (SpMM on SGT(A^T), weights through the edge permutation)
+  AGNNConv(X) = agnn_layer(t, X W):  S_e = <Z_i, Z_j>, P = rowsoftmax(S),
+                Y_i = sum_e P_e Z_j
+      dS = P * (<G_i, Z_j> - rowsum(P <G_i, Z_j>))   (SDDMM2 + fused softmax bwd)
+      dZ = A_dS Z + A^T_{P} G + A^T_{dS} Z            (one SpMM on A, one dual
+                                                       SpMM on A^T)
+
+Every sparse op is a libtcg_b200.so kernel; the dense GEMMs are torch fp32
+(TF32 disabled). With a ShardPlan (dist.py) each rank
+computes its window range and the results are all-gathered.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+from . import _lib
+from .dist import ShardPlan, allgather_edges, allgather_rows
+from .kernels import sddmm_device, spmm_device
+from .sgt import TiledGraph
+
+
+def _edge_weights(t: TiledGraph):
+    g = t._require_graph()
+    return None if g.edge_values is None else g.device_arrays(t.device)[2]
+
+
+def _rows_out(t: TiledGraph, d: int, like: torch.Tensor, shard: ShardPlan | None):
+    if shard is None:
+        return torch.empty((t.num_nodes, d), dtype=torch.float32, device=like.device), 0, None
+    r0, _ = shard.my_rows
+    slab = torch.empty((shard.rows_max, d), dtype=torch.float32, device=like.device)
+    return slab, r0, shard.my_windows
+
+
+def _finish_rows(slab, shard):
+    return slab if shard is None else allgather_rows(slab, shard)
+
+
+class GcnAggregate(torch.autograd.Function):
+    """Y = A_w H + b, w = stored edge values (or 1)."""
+
+    @staticmethod
+    def forward(ctx, h, bias, t: TiledGraph, mode: str, shard: ShardPlan | None):
+        h = h.contiguous()
+        out, r0, wr = _rows_out(t, h.shape[1], h, shard)
+        spmm_device(t, h, _edge_weights(t), mode=mode, out=out, bias=bias, win_range=wr,
+                    y_row0=r0)
+        ctx.t, ctx.mode, ctx.shard = t, mode, shard
+        ctx.has_bias = bias is not None
+        return _finish_rows(out, shard)
+
+    @staticmethod
+    def backward(ctx, g):
+        t, shard = ctx.t, ctx.shard
+        g = g.contiguous()
+        tt = t.transpose()
+        out, r0, wr = _rows_out(t, g.shape[1], g, shard)
+        spmm_device(tt.tiled, g, _edge_weights(t), weight_idx=tt.perm if t.num_edges else None,
+                    mode=ctx.mode, out=out, win_range=wr, y_row0=r0)
+        dh = _finish_rows(out, shard)
+        db = g.sum(0) if ctx.has_bias else None
+        return dh, db, None, None, None
+
+
+class AgnnAggregate(torch.autograd.Function):
+    """Y = spmm(A, P; Z), P = rowsoftmax(sddmm(Z, Z))."""
+
+    @staticmethod
+    def forward(ctx, z, t: TiledGraph, mode: str, shard: ShardPlan | None):
+        z = z.contiguous()
+        m = t.num_edges
+        p = torch.empty(max(m, 1), dtype=torch.float32, device=z.device)
+        out, r0, wr = _rows_out(t, z.shape[1], z, shard)
+        if m:
+            sddmm_device(t, z, mode=mode, epilogue=_lib.EPI_SOFTMAX, out=p, win_range=wr)
+        spmm_device(t, z, p if m else None, mode=mode, out=out, win_range=wr, y_row0=r0)
+        if shard is not None and m:
+            e0, e1 = shard.my_edges
+            loc = torch.zeros(shard.edges_max, dtype=torch.float32, device=z.device)
+            loc[: e1 - e0] = p[e0:e1]
+            p = allgather_edges(loc, shard)
+        ctx.save_for_backward(z, p)
+        ctx.t, ctx.mode, ctx.shard = t, mode, shard
+        return _finish_rows(out, shard)
+
+    @staticmethod
+    def backward(ctx, g):
+        z, p = ctx.saved_tensors
+        t, mode, shard = ctx.t, ctx.mode, ctx.shard
+        g = g.contiguous()
+        m = t.num_edges
+        out, r0, wr = _rows_out(t, z.shape[1], z, shard)
+        if m == 0:
+            out.zero_()
+            return _finish_rows(out, shard), None, None, None
+        ds = torch.empty(m, dtype=torch.float32, device=z.device)
+        sddmm_device(t, g, z, mode=mode, epilogue=_lib.EPI_SOFTMAX_BWD, aux=p, out=ds,
+                     win_range=wr)
+        if shard is not None:
+            e0, e1 = shard.my_edges
+            loc = torch.zeros(shard.edges_max, dtype=torch.float32, device=z.device)
+            loc[: e1 - e0] = ds[e0:e1]
+            ds = allgather_edges(loc, shard)
+        spmm_device(t, z, ds, mode=mode, out=out, win_range=wr, y_row0=r0)
+        tt = t.transpose()
+        spmm_device(tt.tiled, g, p, weight_idx=tt.perm, x2=z, weights2=ds, weight_idx2=tt.perm,
+                    mode=mode, out=out, accumulate=True, win_range=wr, y_row0=r0)
+        return _finish_rows(out, shard), None, None, None
+
+
+def _glorot(fan_in, fan_out, gen=None):
+    return torch.randn(fan_in, fan_out, generator=gen) / math.sqrt(fan_in)
+
+
+class GCNConv(nn.Module):
+    """TC-GNN GCNConv: Y = A (X W) + b."""
+
+    def __init__(self, in_dim: int, out_dim: int, mode: str = "tf32", gen=None):
+        super().__init__()
+        self.weight = nn.Parameter(_glorot(in_dim, out_dim, gen))
+        self.bias = nn.Parameter(torch.zeros(out_dim))
+        self.mode = mode
+
+    def forward(self, x, t: TiledGraph, shard: ShardPlan | None = None):
+        return GcnAggregate.apply(x @ self.weight, self.bias, t, self.mode, shard)
+
+
+class AGNNConv(nn.Module):
+    """TC-GNN AGNNConv: agnn_layer(t, X W) (kernels.py:586-601 + a linear map)."""
+
+    def __init__(self, in_dim: int, out_dim: int, mode: str = "tf32", gen=None):
+        super().__init__()
+        self.weight = nn.Parameter(_glorot(in_dim, out_dim, gen))
+        self.mode = mode
+
+    def forward(self, x, t: TiledGraph, shard: ShardPlan | None = None):
+        return AgnnAggregate.apply(x @ self.weight, t, self.mode, shard)
+
+
+class GCN(nn.Module):
+    """X -> GCNConv(F,h) -> ReLU -> GCNConv(h,C) -> log_softmax."""
+
+    def __init__(self, f_in, hidden, classes, mode="tf32", seed=3):
+        super().__init__()
+        gen = torch.Generator().manual_seed(seed)
+        self.c1 = GCNConv(f_in, hidden, mode, gen)
+        self.c2 = GCNConv(hidden, classes, mode, gen)
+
+    def forward(self, x, t, shard=None):
+        return F.log_softmax(self.c2(F.relu(self.c1(x, t, shard)), t, shard), dim=1)
+
+
+class AGNN(nn.Module):
+    """X -> Linear(F,h) -> ReLU -> L x AGNNConv(h,h) -> Linear(h,C) ->
+    log_softmax."""
+
+    def __init__(self, f_in, hidden, classes, layers=4, mode="tf32", seed=3):
+        super().__init__()
+        gen = torch.Generator().manual_seed(seed)
+        self.lin_in = nn.Linear(f_in, hidden)
+        self.convs = nn.ModuleList([AGNNConv(hidden, hidden, mode, gen) for _ in range(layers)])
+        self.lin_out = nn.Linear(hidden, classes)
+
+    def forward(self, x, t, shard=None):
+        h = F.relu(self.lin_in(x))
+        for c in self.convs:
+            h = c(h, t, shard)
+        return F.log_softmax(self.lin_out(h), dim=1)

@@ -1,0 +1,296 @@
+"""Sparse Graph Translation on the GPU and the tiled-graph container.
+
+`translate` keeps the reference signature (`tcgraph.sgt.translate(g, cfg)`,
+/root/reference/pkg/src/tcgraph/sgt.py:101-137) but runs on the B200 through
+`tcg_sgt` (csrc/sgt.cu). The TiledGraph keeps its four SGT arrays resident in
+HBM (the per-epoch kernels read them there) and materialises the numpy views
+the reference exposes (`win_partition`, `edge_to_col`, `col_offsets`,
+`col_to_node`) lazily, on first host access.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .graph import CsrGraph
+
+PRECISION_MODES = ("f32", "tf32")
+
+
+@dataclass(frozen=True)
+class BlockConfig:
+    """Tile shape and numeric mode (sgt.py:21-40)."""
+
+    blk_h: int = 16
+    blk_w: int = 8
+    precision_mode: str = "f32"
+
+    def __post_init__(self):
+        if self.blk_h < 1 or self.blk_w < 1:
+            raise ValueError(f"tile shape must be >= 1, got {self.blk_h}x{self.blk_w}")
+        if self.precision_mode not in PRECISION_MODES:
+            raise ValueError(
+                f"precision_mode must be one of {PRECISION_MODES}, got {self.precision_mode!r}"
+            )
+
+
+def _to_np_u32(t) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint32)
+
+
+@dataclass
+class TiledGraph:
+    """SGT result (sgt.py:43-98). Device tensors live in `dev`:
+    node_ptr i64[N+1], edge_list/edge_to_col/col_to_node/win_partition as
+    int32 tensors holding u32 bits, col_offsets i64[W+1]."""
+
+    graph: CsrGraph | None
+    config: BlockConfig
+    num_nodes: int
+    num_edges: int
+    num_row_windows: int
+    dev: dict = field(default_factory=dict, repr=False)
+    _host: dict = field(default_factory=dict, repr=False, compare=False)
+    _aux: dict = field(default_factory=dict, repr=False, compare=False)
+
+    # ---- host views (reference attribute names) ---------------------------
+    def _host_array(self, name, conv):
+        a = self._host.get(name)
+        if a is None:
+            a = conv(self.dev[name])
+            self._host[name] = a
+        return a
+
+    @property
+    def win_partition(self) -> np.ndarray:
+        return self._host_array("win_partition", _to_np_u32)
+
+    @property
+    def edge_to_col(self) -> np.ndarray:
+        return self._host_array("edge_to_col", _to_np_u32)
+
+    @property
+    def col_offsets(self) -> np.ndarray:
+        return self._host_array("col_offsets", lambda t: t.cpu().numpy())
+
+    @property
+    def col_to_node(self) -> np.ndarray:
+        return self._host_array("col_to_node", _to_np_u32)
+
+    @property
+    def num_unique(self) -> int:
+        return int(self.dev["num_unique"])
+
+    def unique_count(self, window: int) -> int:
+        return int(self.col_offsets[window + 1] - self.col_offsets[window])
+
+    def window_nodes(self, window: int) -> np.ndarray:
+        return self.col_to_node[self.col_offsets[window]:self.col_offsets[window + 1]]
+
+    def window_edge_range(self, window: int) -> tuple[int, int]:
+        g = self._require_graph()
+        bh = self.config.blk_h
+        r0, r1 = min(window * bh, g.num_nodes), min((window + 1) * bh, g.num_nodes)
+        return int(g.node_pointer[r0]), int(g.node_pointer[r1])
+
+    def window_edge_rows(self, window: int) -> np.ndarray:
+        """edgeToRow: row offset within the window of each of its edges."""
+        g = self._require_graph()
+        bh = self.config.blk_h
+        r0, r1 = min(window * bh, g.num_nodes), min((window + 1) * bh, g.num_nodes)
+        return np.repeat(np.arange(r1 - r0, dtype=np.int64), np.diff(g.node_pointer[r0:r1 + 1]))
+
+    def _require_graph(self) -> CsrGraph:
+        if self.graph is None:
+            raise ValueError(
+                "this TiledGraph holds tiling structure only (no source graph); "
+                "reload the original edge list or matrix file to run kernels"
+            )
+        return self.graph
+
+    # ---- device descriptor --------------------------------------------------
+    def abi(self) -> _lib.TcgTiling:
+        """The `tcg_tiling` descriptor handed to every kernel call."""
+        s = self._aux.get("abi")
+        if s is None:
+            self._require_graph()
+            d = self.dev
+            s = _lib.TcgTiling(
+                self.num_nodes, self.num_edges, self.num_row_windows, self.num_unique,
+                self.config.blk_h, self.config.blk_w,
+                d["node_ptr"].data_ptr(), d["edge_list"].data_ptr() if self.num_edges else None,
+                d["edge_to_col"].data_ptr() if self.num_edges else None,
+                d["col_offsets"].data_ptr(),
+                d["col_to_node"].data_ptr() if self.num_unique else None,
+                d["win_partition"].data_ptr() if self.num_row_windows else None,
+            )
+            self._aux["abi"] = s
+        return s
+
+    @property
+    def device(self):
+        return self.dev["node_ptr"].device
+
+    def block_offsets(self) -> np.ndarray:
+        """Per-window TC-block offsets: exclusive cumsum of win_partition
+        (the 'counts and offsets' of north_star; the reference derives the
+        SDDMM analogue tile_base at kernels.py:461-462)."""
+        out = np.zeros(self.num_row_windows + 1, dtype=np.int64)
+        np.cumsum(self.win_partition.astype(np.int64), out=out[1:])
+        return out
+
+    def transpose(self) -> "TransposedTiling":
+        """A^T tiled with the same BlockConfig, plus the edge permutation
+        (backward passes; cached)."""
+        tt = self._aux.get("transpose")
+        if tt is None:
+            tt = _transpose(self)
+            self._aux["transpose"] = tt
+        return tt
+
+
+@dataclass
+class TransposedTiling:
+    tiled: TiledGraph
+    perm: object  # torch int32 tensor (u32 bits): edge k of A^T is edge perm[k] of A
+
+
+def _stream_ptr():
+    import torch
+
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _sgt_device(ptr, cols, n: int, m: int, cfg: BlockConfig, graph) -> TiledGraph:
+    import torch
+
+    lib = _lib.load()
+    dev = ptr.device
+    W = -(-n // cfg.blk_h)
+    wp = torch.empty(max(W, 1), dtype=torch.int32, device=dev)
+    e2c = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+    offs = torch.empty(W + 1, dtype=torch.int64, device=dev)
+    c2n = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+    wsb = int(lib.tcg_sgt_workspace_bytes(n, m, cfg.blk_h))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    _lib.check(lib.tcg_sgt(ptr.data_ptr(), cols.data_ptr() if m else None, n, m, cfg.blk_h,
+                           cfg.blk_w, wp.data_ptr(), e2c.data_ptr(), offs.data_ptr(),
+                           c2n.data_ptr(), ws.data_ptr(), wsb, _stream_ptr()), "tcg_sgt")
+    u = int(offs[-1].item()) if W else 0
+    t = TiledGraph(graph, cfg, n, m, W)
+    t.dev.update(node_ptr=ptr, edge_list=cols, win_partition=wp[:W], edge_to_col=e2c[:m],
+                 col_offsets=offs, col_to_node=c2n[:u], num_unique=u)
+    return t
+
+
+def translate(g: CsrGraph, cfg: BlockConfig, device=None) -> TiledGraph:
+    """GPU Sparse Graph Translation; bit-exact with the reference translate
+    (sgt.py:101-137) for any BlockConfig."""
+    if not isinstance(cfg, BlockConfig):
+        raise TypeError("cfg must be a BlockConfig")
+    ptr, cols, _ = g.device_arrays(device)
+    return _sgt_device(ptr, cols, g.num_nodes, g.num_edges, cfg, g)
+
+
+def _transpose(t: TiledGraph) -> TransposedTiling:
+    import torch
+
+    lib = _lib.load()
+    g = t._require_graph()
+    n, m = t.num_nodes, t.num_edges
+    ptr, cols = t.dev["node_ptr"], t.dev["edge_list"]
+    dev = ptr.device
+    ptr_t = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    cols_t = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+    perm = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+    wsb = int(lib.tcg_csr_transpose_workspace_bytes(n, m))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    _lib.check(lib.tcg_csr_transpose(ptr.data_ptr(), cols.data_ptr() if m else None, n, m,
+                                     ptr_t.data_ptr(), cols_t.data_ptr(), perm.data_ptr(),
+                                     ws.data_ptr(), wsb, _stream_ptr()), "tcg_csr_transpose")
+    cols_t, perm = cols_t[:m], perm[:m]
+    gt = _DeviceCsr(n, ptr_t, cols_t, g)
+    tt = _sgt_device(ptr_t, cols_t, n, m, t.config, gt)
+    return TransposedTiling(tt, perm)
+
+
+class _DeviceCsr(CsrGraph):
+    """A CsrGraph whose arrays were built on the device (A^T); host views are
+    materialised on demand."""
+
+    def __init__(self, n, ptr_d, cols_d, parent):
+        self.num_nodes = int(n)
+        self._dev = {("csr", ptr_d.device.index): (ptr_d, cols_d, None)}
+        self._ptr_d, self._cols_d = ptr_d, cols_d
+        self.edge_values = None
+        self._np = None
+
+    def _host(self):
+        if self._np is None:
+            self._np = (self._ptr_d.cpu().numpy(), self._cols_d.cpu().numpy().view(np.uint32))
+        return self._np
+
+    @property
+    def node_pointer(self):
+        return self._host()[0]
+
+    @node_pointer.setter
+    def node_pointer(self, v):
+        pass
+
+    @property
+    def edge_list(self):
+        return self._host()[1]
+
+    @edge_list.setter
+    def edge_list(self, v):
+        pass
+
+    @property
+    def num_edges(self) -> int:
+        return int(self._cols_d.shape[0])
+
+
+# ---- tile accounting (sgt.py:140-217; reporting, host-side) -----------------
+
+
+def count_blocks_before(g: CsrGraph, cfg: BlockConfig) -> tuple[int, np.ndarray]:
+    """Occupied blk_w-wide original-column buckets per window (sgt.py:140-157)."""
+    n, bh, bw = g.num_nodes, cfg.blk_h, cfg.blk_w
+    W = -(-n // bh)
+    if g.num_edges == 0:
+        return 0, np.zeros(W, dtype=np.int64)
+    win = np.repeat(np.arange(n, dtype=np.int64), g.degrees()) // bh
+    nb = -(-n // bw)
+    uniq = np.unique(win * nb + g.edge_list.astype(np.int64) // bw)
+    return int(uniq.shape[0]), np.bincount(uniq // nb, minlength=W)
+
+
+def count_blocks_after(t: TiledGraph) -> int:
+    return int(t.win_partition.astype(np.int64).sum())
+
+
+def reduction_ratio(before: int, after: int) -> float:
+    return 0.0 if before == 0 else 1.0 - after / before
+
+
+def block_columns(t: TiledGraph, window: int, block: int) -> np.ndarray:
+    if not 0 <= window < t.num_row_windows:
+        raise IndexError(f"window {window} out of range [0, {t.num_row_windows})")
+    if not 0 <= block < int(t.win_partition[window]):
+        raise IndexError(
+            f"block {block} out of range [0, {int(t.win_partition[window])}) in window {window}")
+    bw = t.config.blk_w
+    lo = t.col_offsets[window] + block * bw
+    hi = min(lo + bw, t.col_offsets[window + 1])
+    return t.col_to_node[lo:hi].copy()
+
+
+def paired_block_counts(t: TiledGraph) -> np.ndarray:
+    """ceil(wp * blk_w / blk_h) square output tiles per window (sgt.py:190-198)."""
+    bh, bw = t.config.blk_h, t.config.blk_w
+    return (t.win_partition.astype(np.int64) * bw + bh - 1) // bh
