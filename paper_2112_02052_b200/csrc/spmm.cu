@@ -403,8 +403,8 @@ extern "C" int tcg_spmm(const tcg_tiling* t, const float* x, int64_t ldx, int64_
 
   TCG_REQUIRE(t->blk_h == 16 && t->blk_w == 8,
               "tf32 mode requires the 16x8 tile shape, got %dx%d", t->blk_h, t->blk_w);
-  TCG_REQUIRE(t->edge_to_col && t->col_offsets && t->win_partition &&
-                  (t->col_to_node || t->num_unique == 0),
+  TCG_REQUIRE(t->col_offsets && t->win_partition &&
+                  (t->num_edges == 0 || (t->edge_to_col && t->col_to_node)),
               "tcg_spmm: tiling arrays missing");
   int nt, nchunks;
   if (dim <= 64) {

@@ -1,0 +1,127 @@
+"""GPU autograd layers: forward = reference layer semantics, backward = the
+restated gradients (oracle.agnn_backward / spmm_transpose), CSR transpose =
+the oracle's stable permutation, CUDA-graph replay = eager."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import TF32_REL_L2, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    import paper_2112_02052_b200 as tcg
+    from paper_2112_02052_b200 import layers
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return tcg, layers, torch
+
+
+@pytest.mark.parametrize("n,deg,seed", [(300, 5, 7), (1000, 8, 3), (45, 3, 2), (2708, 4, 1)])
+def test_csr_transpose_matches_oracle(env, oracle, n, deg, seed):
+    tcg, _, _ = env
+    g = tcg.synth.gen_uniform(n, deg, seed)
+    t = tcg.translate(g, tcg.BlockConfig())
+    tt = t.transpose()
+    pt, ct, perm = oracle.csr_transpose(g.node_pointer, g.edge_list, n)
+    assert np.array_equal(tt.tiled.graph.node_pointer, pt)
+    assert np.array_equal(tt.tiled.graph.edge_list, ct)
+    assert np.array_equal(tt.perm.cpu().numpy().view(np.uint32).astype(np.int64), perm)
+    ref = oracle.translate(pt, ct, n, 16, 8)
+    for k, v in zip(("win_partition", "edge_to_col", "col_offsets", "col_to_node"), ref):
+        assert np.array_equal(getattr(tt.tiled, k), v), k
+
+
+@pytest.mark.parametrize("mode,tol", [("f32", 2e-5), ("tf32", TF32_REL_L2)])
+def test_agnn_backward_vs_oracle(env, oracle, mode, tol):
+    tcg, layers, torch = env
+    g = tcg.synth.gen_uniform(3000, 6, 11)
+    t = tcg.translate(g, tcg.BlockConfig())
+    rng = np.random.default_rng(0)
+    z = rng.standard_normal((3000, 32)).astype(np.float32)
+    gy = rng.standard_normal((3000, 32)).astype(np.float32)
+    zt = torch.from_numpy(z).cuda().requires_grad_(True)
+    y = layers.AgnnAggregate.apply(zt, t, mode, None)
+    y.backward(torch.from_numpy(gy).cuda())
+    ptr, cols = g.node_pointer, g.edge_list
+    p = oracle.segment_softmax(oracle.sddmm(ptr, cols, z), ptr)
+    y_ref = oracle.spmm(ptr, cols, z, f=p)
+    dz_ref = oracle.agnn_backward(ptr, cols, z, p, gy)
+    assert rel_l2(y.detach().cpu().numpy(), y_ref) <= tol
+    assert rel_l2(zt.grad.cpu().numpy(), dz_ref) <= tol
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_gcn_backward_vs_oracle(env, oracle, weighted):
+    tcg, layers, torch = env
+    base = tcg.synth.gen_uniform(2000, 5, 4)
+    vals = np.random.default_rng(5).random(base.num_edges).astype(np.float32) if weighted else None
+    g = tcg.CsrGraph(2000, base.node_pointer, base.edge_list, vals)
+    t = tcg.translate(g, tcg.BlockConfig())
+    rng = np.random.default_rng(1)
+    h = rng.standard_normal((2000, 16)).astype(np.float32)
+    b = rng.standard_normal(16).astype(np.float32)
+    gy = rng.standard_normal((2000, 16)).astype(np.float32)
+    ht = torch.from_numpy(h).cuda().requires_grad_(True)
+    bt = torch.from_numpy(b).cuda().requires_grad_(True)
+    y = layers.GcnAggregate.apply(ht, bt, t, "f32", None)
+    y.backward(torch.from_numpy(gy).cuda())
+    ptr, cols = g.node_pointer, g.edge_list
+    assert np.array_equal(y.detach().cpu().numpy(),
+                          (oracle.spmm(ptr, cols, h, f=vals) + b).astype(np.float32))
+    dh = oracle.spmm_transpose(ptr, cols, gy, f=vals)
+    assert np.array_equal(ht.grad.cpu().numpy(), dh)  # exact mode: same fold order
+    np.testing.assert_allclose(bt.grad.cpu().numpy(), gy.sum(0), rtol=1e-4, atol=1e-3)
+
+
+def test_models_train_and_graph_capture(env):
+    tcg, layers, torch = env
+    g = tcg.synth.gen_uniform(5000, 7, 2)
+    t = tcg.translate(g, tcg.BlockConfig())
+    t.transpose()
+    x = torch.randn(5000, 64, device="cuda")
+    labels = torch.randint(0, 10, (5000,), device="cuda")
+    for Model in (lambda: layers.GCN(64, 16, 10), lambda: layers.AGNN(64, 32, 10, layers=2)):
+        torch.manual_seed(0)
+        m = Model().cuda()
+        opt = torch.optim.Adam(m.parameters(), lr=0.01)
+        losses = []
+        for _ in range(20):
+            opt.zero_grad(set_to_none=False)
+            loss = torch.nn.functional.nll_loss(m(x, t), labels)
+            loss.backward()
+            opt.step()
+            losses.append(float(loss))
+        assert losses[-1] < losses[0]
+        # CUDA graph replay of one step equals eager
+        m2 = Model().cuda()
+        m2.load_state_dict(m.state_dict())
+
+        def step(mod):
+            mod.zero_grad(set_to_none=False)
+            out = torch.nn.functional.nll_loss(mod(x, t), labels)
+            out.backward()
+            return out
+
+        eager = step(m2).detach().clone()
+        grads = [p.grad.clone() for p in m2.parameters()]
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                step(m2)
+        torch.cuda.current_stream().wait_stream(s)
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            cap = step(m2)
+        gr.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(cap, eager)
+        for p, q in zip(m2.parameters(), grads):
+            assert torch.equal(p.grad, q)
