@@ -52,6 +52,8 @@ typedef struct tcg_tiling {
   const int64_t* col_offsets;   /* i64[W+1]  TiledGraph.col_offsets           */
   const uint32_t* col_to_node;  /* u32[U]    TiledGraph.col_to_node           */
   const uint32_t* win_partition;/* u32[W]    TiledGraph.win_partition         */
+  int64_t max_window_edges;     /* max edges of one window (0 = unknown)       */
+  int64_t max_window_unique;    /* max condensed columns of one window         */
 } tcg_tiling;
 
 /* ---- library ---------------------------------------------------------- */
@@ -122,14 +124,23 @@ int tcg_segment_softmax_backward(const int64_t* node_ptr, int64_t num_rows, cons
                                  const float* dp, float* ds, void* stream);
 
 /* ---- fused AGNN layer: reference kernels.agnn_layer (586-601) ----------- */
-/* One CTA per window: gather the window's neighbour rows of Z once into
- * shared memory, SDDMM -> row softmax -> weighted SpMM from the same tile.
- * Writes P[M] (edge order, needed by the backward) and Y rows.
- * Falls back to the unfused sequence for windows too large for shared
- * memory (same kernels, same results). TF32 only. */
+/* One warp per window: the window's condensed neighbour rows of Z are
+ * gathered once into shared memory and serve both the SDDMM (scores) and,
+ * after the in-register row softmax, the weighted SpMM. Writes P[e]
+ * (absolute edge ids; kept for the backward) and Y rows. Windows that do
+ * not fit (max_window_edges > 256 or more condensed columns than one staged
+ * round, or dim > 64) run the same two products unfused. TF32, 16x8 only. */
 int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim, float* p,
                      float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
                      void* stream);
+/* AGNN backward, A-side half (no reference counterpart):
+ * dS = P * (dP - rowsum(P dP)) with dP_e = <G_row, Z_col> (written to ds),
+ * and dZ rows = A_dS Z (overwritten). The A^T half (A^T_P G + A^T_dS Z) is
+ * one dual tcg_spmm on the transposed tiling with weight_idx = perm. */
+int tcg_agnn_backward(const tcg_tiling* t, const float* z, int64_t ldz, const float* gy,
+                      int64_t ldg, int64_t dim, const float* p, float* ds, float* dz,
+                      int64_t lddz, int64_t dz_row0, int64_t win_begin, int64_t win_end,
+                      void* stream);
 
 /* ---- TF32 operand rounding: reference tiles.quantize_tf32 (67-82) ------- */
 int tcg_quantize_tf32(const float* in, float* out, int64_t n, void* stream);

@@ -37,6 +37,8 @@ class TcgTiling(C.Structure):
         ("col_offsets", C.c_void_p),
         ("col_to_node", C.c_void_p),
         ("win_partition", C.c_void_p),
+        ("max_window_edges", C.c_int64),
+        ("max_window_unique", C.c_int64),
     ]
 
 
@@ -63,6 +65,8 @@ SIGNATURES = {
     "tcg_segment_softmax_backward": (C.c_int, [_P, _I64, _P, _P, _P, _P]),
     "tcg_agnn_forward": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _I64, _P, _P, _I64, _I64,
                                    _I64, _I64, _P]),
+    "tcg_agnn_backward": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _P, _I64, _I64, _P, _P,
+                                    _P, _I64, _I64, _I64, _I64, _P]),
     "tcg_quantize_tf32": (C.c_int, [_P, _P, _I64, _P]),
 }
 

@@ -4,7 +4,6 @@
 //    kernels.py:541-556) and its backward (no reference counterpart);
 //  * TF32 operand rounding (reference tiles.quantize_tf32, tiles.py:67-82);
 //  * CSR transpose with the edge permutation (backward support);
-//  * the AGNN layer entry point (reference kernels.agnn_layer, 586-601).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -231,14 +230,4 @@ extern "C" int tcg_csr_transpose(const int64_t* node_ptr, const uint32_t* edge_l
            "transpose scan");
   launch_counter().fetch_add(1, std::memory_order_relaxed);
   return TCG_OK;
-}
-
-extern "C" int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim,
-                                float* p, float* y, int64_t ldy, int64_t y_row0,
-                                int64_t win_begin, int64_t win_end, void* stream) {
-  int rc = tcg_sddmm(t, z, ldz, z, ldz, dim, nullptr, p, win_begin, win_end, TCG_PREC_TF32,
-                     TCG_EPI_SOFTMAX, stream);
-  if (rc != TCG_OK) return rc;
-  return tcg_spmm(t, z, ldz, dim, p, nullptr, nullptr, 0, nullptr, nullptr, nullptr, y, ldy,
-                  y_row0, win_begin, win_end, TCG_PREC_TF32, 0, stream);
 }

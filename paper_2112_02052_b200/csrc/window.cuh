@@ -1,0 +1,67 @@
+// Row-window engine interface (see window.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tcg {
+namespace win {
+
+enum Mode { MODE_SPMM = 0, MODE_SPMM_DUAL = 1, MODE_SDDMM = 2, MODE_AGNN_FWD = 3, MODE_AGNN_BWD = 4 };
+
+// edges per window the fused AGNN kernels keep in shared memory
+constexpr int kEdgesPerWindow = 256;
+
+// condensed columns staged per round (rows of X in shared memory)
+__host__ __device__ constexpr int cols_per_round(int nt, int mode) {
+  return (nt <= 4 ? 128 : 64) / (mode == MODE_SPMM_DUAL ? 2 : 1);
+}
+
+struct Params {
+  // tiling (16x8)
+  const int64_t* ptr;
+  const uint32_t* e2c;
+  const int64_t* coff;
+  const uint32_t* c2n;
+  int64_t n;
+  int64_t win_begin, nwin;
+  int nchunks;  // feature chunks of 8*NT (SpMM modes); 1 otherwise
+  int nkc;      // SDDMM k-chunks of 8*NT features
+  int dim;
+  int vec16;    // 16-B staging legal (dim, ld, base aligned)
+  int vec_out;  // 16-B output stores legal
+  // gathered operand(s)
+  const float* x;
+  int64_t ldx;
+  const float* x2;
+  int64_t ldx2;
+  // SpMM weights (nullable; *_idx: indirection, A^T edge order)
+  const float* w;
+  const uint32_t* widx;
+  const float* w2;
+  const uint32_t* widx2;
+  // SpMM output
+  const float* bias;
+  float* y;
+  int64_t ldy;
+  int64_t y_row0;
+  int accumulate;
+  // SDDMM A operand (window rows) and edge outputs
+  const float* xa;
+  int64_t lda;
+  const float* aux;
+  float* eout;
+  int epilogue;
+};
+
+int launch(int mode, int nt, const Params& p, cudaStream_t s);
+
+inline int nt_for(int64_t dim) {
+  if (dim <= 8) return 1;
+  if (dim <= 16) return 2;
+  if (dim <= 32) return 4;
+  return 8;
+}
+
+}  // namespace win
+}  // namespace tcg

@@ -272,6 +272,43 @@ def sddmm_device(t: TiledGraph, xa, xb=None, *, mode="tf32", epilogue=_lib.EPI_N
     return out
 
 
+def agnn_forward_device(t: TiledGraph, z, *, p=None, out=None, win_range=None, y_row0=0):
+    """Fused TF32 AGNN aggregation (tcg_agnn_forward): returns (Y, P)."""
+    import torch
+
+    lib = _lib.load()
+    wb, we = win_range if win_range is not None else (0, t.num_row_windows)
+    if p is None:
+        p = torch.empty(max(t.num_edges, 1), dtype=torch.float32, device=z.device)
+    if out is None:
+        out = torch.empty((t.num_nodes, z.shape[1]), dtype=torch.float32, device=z.device)
+        y_row0 = 0
+    _lib.check(lib.tcg_agnn_forward(C.byref(t.abi()), z.data_ptr(), z.stride(0), z.shape[1],
+                                    p.data_ptr(), out.data_ptr(), out.stride(0), y_row0, wb, we,
+                                    _stream()), "tcg_agnn_forward")
+    return out, p
+
+
+def agnn_backward_device(t: TiledGraph, z, gy, p, *, ds=None, out=None, win_range=None,
+                         y_row0=0):
+    """A-side half of the AGNN backward (tcg_agnn_backward): returns (dZ_A, dS)
+    with dS = P (dP - rowsum(P dP)), dP = <G_i, Z_j>, dZ_A = A_dS Z."""
+    import torch
+
+    lib = _lib.load()
+    wb, we = win_range if win_range is not None else (0, t.num_row_windows)
+    if ds is None:
+        ds = torch.empty(max(t.num_edges, 1), dtype=torch.float32, device=z.device)
+    if out is None:
+        out = torch.empty((t.num_nodes, z.shape[1]), dtype=torch.float32, device=z.device)
+        y_row0 = 0
+    _lib.check(lib.tcg_agnn_backward(C.byref(t.abi()), z.data_ptr(), z.stride(0), gy.data_ptr(),
+                                     gy.stride(0), z.shape[1], p.data_ptr(), ds.data_ptr(),
+                                     out.data_ptr(), out.stride(0), y_row0, wb, we, _stream()),
+               "tcg_agnn_backward")
+    return out, ds
+
+
 # ---------------------------------------------------------------------------
 # reference-compatible API
 # ---------------------------------------------------------------------------
@@ -376,11 +413,11 @@ def agnn_layer(t: TiledGraph, x, mode: str | None = None, workers: int = 1,
     xd, host = _embeddings(t, x)
     mode = _resolve_mode(t, mode)
     _check_engine(engine)
-    if t.num_edges:
-        p = sddmm_device(t, xd, mode=mode, epilogue=_lib.EPI_SOFTMAX)
+    if mode == "tf32":
+        out, _ = agnn_forward_device(t, xd)  # one gather serves SDDMM and SpMM
     else:
-        p = None
-    out = spmm_device(t, xd, p, mode=mode)
+        p = sddmm_device(t, xd, mode=mode, epilogue=_lib.EPI_SOFTMAX) if t.num_edges else None
+        out = spmm_device(t, xd, p, mode=mode)
     if counters is not None:
         counters.add(_sddmm_counters(t, xd.shape[1]))
         counters.add(_spmm_counters(t, make_plan(t, xd.shape[1])))

@@ -30,7 +30,7 @@ import torch.nn.functional as F
 
 from . import _lib
 from .dist import ShardPlan, allgather_edges, allgather_rows
-from .kernels import sddmm_device, spmm_device
+from .kernels import agnn_backward_device, agnn_forward_device, sddmm_device, spmm_device
 from .sgt import TiledGraph
 
 
@@ -86,9 +86,12 @@ class AgnnAggregate(torch.autograd.Function):
         m = t.num_edges
         p = torch.empty(max(m, 1), dtype=torch.float32, device=z.device)
         out, r0, wr = _rows_out(t, z.shape[1], z, shard)
-        if m:
-            sddmm_device(t, z, mode=mode, epilogue=_lib.EPI_SOFTMAX, out=p, win_range=wr)
-        spmm_device(t, z, p if m else None, mode=mode, out=out, win_range=wr, y_row0=r0)
+        if mode == "tf32":
+            agnn_forward_device(t, z, p=p, out=out, win_range=wr, y_row0=r0)
+        else:
+            if m:
+                sddmm_device(t, z, mode=mode, epilogue=_lib.EPI_SOFTMAX, out=p, win_range=wr)
+            spmm_device(t, z, p if m else None, mode=mode, out=out, win_range=wr, y_row0=r0)
         if shard is not None and m:
             e0, e1 = shard.my_edges
             loc = torch.zeros(shard.edges_max, dtype=torch.float32, device=z.device)
@@ -109,14 +112,19 @@ class AgnnAggregate(torch.autograd.Function):
             out.zero_()
             return _finish_rows(out, shard), None, None, None
         ds = torch.empty(m, dtype=torch.float32, device=z.device)
-        sddmm_device(t, g, z, mode=mode, epilogue=_lib.EPI_SOFTMAX_BWD, aux=p, out=ds,
-                     win_range=wr)
+        if mode == "tf32":
+            # dS and A_dS Z from one gather of Z's neighbour rows
+            agnn_backward_device(t, z, g, p, ds=ds, out=out, win_range=wr, y_row0=r0)
+        else:
+            sddmm_device(t, g, z, mode=mode, epilogue=_lib.EPI_SOFTMAX_BWD, aux=p, out=ds,
+                         win_range=wr)
         if shard is not None:
             e0, e1 = shard.my_edges
             loc = torch.zeros(shard.edges_max, dtype=torch.float32, device=z.device)
             loc[: e1 - e0] = ds[e0:e1]
             ds = allgather_edges(loc, shard)
-        spmm_device(t, z, ds, mode=mode, out=out, win_range=wr, y_row0=r0)
+        if mode != "tf32":
+            spmm_device(t, z, ds, mode=mode, out=out, win_range=wr, y_row0=r0)
         tt = t.transpose()
         spmm_device(tt.tiled, g, p, weight_idx=tt.perm, x2=z, weights2=ds, weight_idx2=tt.perm,
                     mode=mode, out=out, accumulate=True, win_range=wr, y_row0=r0)

@@ -127,9 +127,31 @@ class TiledGraph:
                 d["col_offsets"].data_ptr(),
                 d["col_to_node"].data_ptr() if self.num_unique else None,
                 d["win_partition"].data_ptr() if self.num_row_windows else None,
+                *self.window_maxima(),
             )
             self._aux["abi"] = s
         return s
+
+    def window_maxima(self) -> tuple[int, int]:
+        """(max edges, max condensed columns) over the windows: decides
+        whether the fused AGNN kernels can keep a whole window on chip."""
+        mx = self._aux.get("maxima")
+        if mx is None:
+            if self.num_row_windows == 0:
+                mx = (0, 0)
+            else:
+                ptr = self.dev["node_ptr"]
+                bh = self.config.blk_h
+                idx = np.minimum(np.arange(self.num_row_windows + 1) * bh, self.num_nodes)
+                import torch
+
+                eb = ptr[torch.from_numpy(idx).to(ptr.device)]
+                me = int((eb[1:] - eb[:-1]).max().item())
+                co = self.dev["col_offsets"]
+                mu = int((co[1:] - co[:-1]).max().item())
+                mx = (me, mu)
+            self._aux["maxima"] = mx
+        return mx
 
     @property
     def device(self):
