@@ -52,6 +52,8 @@ typedef struct tcg_tiling {
   const int64_t* col_offsets;   /* i64[W+1]  TiledGraph.col_offsets           */
   const uint32_t* col_to_node;  /* u32[U]    TiledGraph.col_to_node           */
   const uint32_t* win_partition;/* u32[W]    TiledGraph.win_partition         */
+  const uint32_t* edge_frag;    /* u32[M]    mma fragment slot of each edge in
+                                   its 16x8 A tile (tcg_edge_frag; TF32 only) */
   int64_t max_window_edges;     /* max edges of one window (0 = unknown)       */
   int64_t max_window_unique;    /* max condensed columns of one window         */
 } tcg_tiling;
@@ -76,6 +78,13 @@ int tcg_sgt(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_node
             int64_t num_edges, int32_t blk_h, int32_t blk_w, uint32_t* win_partition,
             uint32_t* edge_to_col, int64_t* col_offsets, uint32_t* col_to_node,
             void* workspace, size_t workspace_bytes, void* stream);
+
+/* Per-edge fragment slot for the TF32 kernels (16x8 tilings): edge e of row
+ * r with condensed column c lands at (c/8)*128 + lane*4 + slot of its
+ * window's A tiles, lane = (r%8)*4 + c%4, slot = r%16/8 + 2*(c%8/4). Derived
+ * once per tiling, like the reference's per-edge _spmm_aux cache
+ * (kernels.py:173-188: r_local, b_of_edge, c_local). */
+int tcg_edge_frag(const tcg_tiling* t, uint32_t* edge_frag, void* stream);
 
 /* ---- CSR transpose (backward support; no reference counterpart — the
  * reference has no backward. SURVEY.md Appendix B restates it as

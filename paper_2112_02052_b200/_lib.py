@@ -37,6 +37,7 @@ class TcgTiling(C.Structure):
         ("col_offsets", C.c_void_p),
         ("col_to_node", C.c_void_p),
         ("win_partition", C.c_void_p),
+        ("edge_frag", C.c_void_p),
         ("max_window_edges", C.c_int64),
         ("max_window_unique", C.c_int64),
     ]
@@ -55,6 +56,7 @@ SIGNATURES = {
     "tcg_device_info": (C.c_int, [C.POINTER(_I64), C.POINTER(_I64)]),
     "tcg_sgt_workspace_bytes": (_SZ, [_I64, _I64, _I32]),
     "tcg_sgt": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
+    "tcg_edge_frag": (C.c_int, [C.POINTER(TcgTiling), _P, _P]),
     "tcg_csr_transpose_workspace_bytes": (_SZ, [_I64, _I64]),
     "tcg_csr_transpose": (C.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P, _SZ, _P]),
     "tcg_spmm": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P,

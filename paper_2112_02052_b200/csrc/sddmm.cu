@@ -100,6 +100,7 @@ win::Params base_params(const tcg_tiling* t, int64_t win_begin, int64_t win_end)
   win::Params q{};
   q.ptr = t->node_ptr;
   q.e2c = t->edge_to_col;
+  q.efrag = t->edge_frag;
   q.coff = t->col_offsets;
   q.c2n = t->col_to_node;
   q.n = t->num_nodes;
@@ -154,6 +155,7 @@ extern "C" int tcg_sddmm(const tcg_tiling* t, const float* xa, int64_t lda, cons
   }
   TCG_REQUIRE(t->blk_h == 16 && t->blk_w == 8,
               "tf32 mode requires the 16x8 tile shape, got %dx%d", t->blk_h, t->blk_w);
+  TCG_REQUIRE(t->edge_frag, "tcg_sddmm: tf32 needs edge_frag (tcg_edge_frag)");
   win::Params q = base_params(t, win_begin, win_end);
   const int nt = win::nt_for(dim);
   q.nkc = (int)((dim + 8 * nt - 1) / (8 * nt));
@@ -224,4 +226,13 @@ extern "C" int tcg_agnn_backward(const tcg_tiling* t, const float* z, int64_t ld
   q.x = z, q.ldx = ldz, q.xa = gy, q.lda = ldg;
   q.aux = p, q.eout = ds, q.y = dz, q.ldy = lddz, q.y_row0 = dz_row0;
   return win::launch(win::MODE_AGNN_BWD, nt, q, as_stream(stream));
+}
+
+extern "C" int tcg_edge_frag(const tcg_tiling* t, uint32_t* edge_frag, void* stream) {
+  TCG_REQUIRE(t != nullptr, "tcg_edge_frag: null tiling");
+  TCG_REQUIRE(t->blk_h == 16 && t->blk_w == 8,
+              "tf32 mode requires the 16x8 tile shape, got %dx%d", t->blk_h, t->blk_w);
+  if (t->num_edges == 0) return TCG_OK;
+  TCG_REQUIRE(t->node_ptr && t->edge_to_col && edge_frag, "tcg_edge_frag: null pointer");
+  return win::edge_frag(t->node_ptr, t->edge_to_col, t->num_nodes, edge_frag, as_stream(stream));
 }

@@ -187,9 +187,11 @@ extern "C" int tcg_spmm(const tcg_tiling* t, const float* x, int64_t ldx, int64_
   TCG_REQUIRE(t->col_offsets && t->win_partition &&
                   (t->num_edges == 0 || (t->edge_to_col && t->col_to_node)),
               "tcg_spmm: tiling arrays missing");
+  TCG_REQUIRE(t->num_edges == 0 || t->edge_frag, "tcg_spmm: tf32 needs edge_frag (tcg_edge_frag)");
   win::Params q{};
   q.ptr = t->node_ptr;
   q.e2c = t->edge_to_col;
+  q.efrag = t->edge_frag;
   q.coff = t->col_offsets;
   q.c2n = t->col_to_node;
   q.n = t->num_nodes;

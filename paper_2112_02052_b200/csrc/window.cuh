@@ -21,6 +21,7 @@ struct Params {
   // tiling (16x8)
   const int64_t* ptr;
   const uint32_t* e2c;
+  const uint32_t* efrag;  // per-edge mma fragment slot: (c>>3)*128 + lane*4 + slot
   const int64_t* coff;
   const uint32_t* c2n;
   int64_t n;
@@ -55,6 +56,10 @@ struct Params {
 };
 
 int launch(int mode, int nt, const Params& p, cudaStream_t s);
+
+// per-edge fragment slots of a 16x8 tiling (InitSparse addresses)
+int edge_frag(const int64_t* ptr, const uint32_t* e2c, int64_t n, uint32_t* efrag,
+              cudaStream_t s);
 
 inline int nt_for(int64_t dim) {
   if (dim <= 8) return 1;

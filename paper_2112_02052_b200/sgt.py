@@ -127,8 +127,17 @@ class TiledGraph:
                 d["col_offsets"].data_ptr(),
                 d["col_to_node"].data_ptr() if self.num_unique else None,
                 d["win_partition"].data_ptr() if self.num_row_windows else None,
+                None,
                 *self.window_maxima(),
             )
+            if (self.config.blk_h, self.config.blk_w) == (16, 8) and self.num_edges:
+                import torch
+
+                ef = torch.empty(self.num_edges, dtype=torch.int32, device=self.device)
+                _lib.check(_lib.load().tcg_edge_frag(C.byref(s), ef.data_ptr(), _stream_ptr()),
+                           "tcg_edge_frag")
+                d["edge_frag"] = ef
+                s.edge_frag = ef.data_ptr()
             self._aux["abi"] = s
         return s
 
