@@ -6,15 +6,18 @@
 // memory:
 //
 //   1. FetchDense  — the window's condensed neighbour rows X[col_to_node[c]]
-//      are gathered into shared memory with cp.async (16-B chunks, 8 lanes
-//      per 128-B row so every warp instruction moves whole L2 sectors), all
-//      rows of the window in flight at once. Row c of the window is stored at
-//      smem row srow(c) = (c & ~7) | bitrev3(c & 7) with its 16-B chunks
-//      XOR-swizzled by (srow & 7): with that placement both fragment read
-//      patterns (SpMM: rows t / chunks g; SDDMM: rows g / chunks t) hit 32
-//      distinct banks per phase. While the gather is in flight the warp
-//      prefetches the NEXT window's metadata and col_to_node slice (cross-
-//      window software pipeline) and loads this window's edge data.
+//      are gathered into shared memory by TMA (cp.async.bulk.tensor
+//      tile::gather4: one instruction moves 4 rows; each lane of the warp
+//      issues one, so a whole window is in flight after a single warp
+//      instruction) completing on an mbarrier. The tensor map's 128B/64B/32B
+//      swizzle places row s's 16-B chunk k at k ^ f(s); condensed column c is
+//      written to smem row srow(c) = (c & ~7) | bitrev3(c & 7), so both
+//      fragment read patterns (SpMM: rows t / chunks g; SDDMM: rows g /
+//      chunks t) are bank-conflict free for 128-B rows. Padding columns of
+//      the last 16-column group use an out-of-range row index: TMA fills
+//      them with zeros. (Fallback when TMA is not legal: cp.async 16-B/4-B.)
+//      While the gather is in flight the warp prefetches the NEXT window's
+//      metadata and col_to_node slice and loads this window's edge data.
 //   2. InitSparse  — edge weights are scattered into the 16x8 A tiles in
 //      mma.m16n8k8 fragment order through the per-edge fragment slot
 //      `efrag` (computed once per tiling, the analogue of the reference's
@@ -22,8 +25,8 @@
 //   3. mma.sync.m16n8k8 TF32 (operands RNE-rounded by cvt.rn.tf32.f32, fp32
 //      accumulate) for SpMM (B = staged rows, features permuted so each
 //      lane's slice is contiguous) and for SDDMM (A = the window's own 16
-//      rows, B = staged rows, k = features). All fragment addresses are
-//      per-lane constants plus a block stride.
+//      rows, B = staged rows, k = features). Fragment addresses are per-lane
+//      constants plus a block stride.
 //   4. Epilogues: StoreDense (bias / accumulate, vectorised row stores),
 //      StoreSparse (score tile -> edge order), row softmax and its backward
 //      (rows never straddle windows, 2 lanes per row).
@@ -35,6 +38,11 @@
 //   AGNN_FWD   P = softmax(<Z_i,Z_j>), Y = A_P Z     reference agnn_layer,
 //              one gather of Z's neighbour rows serves both products
 //   AGNN_BWD   dS = P (dP - rowsum(P dP)), dP = <G_i,Z_j>; Y = A_dS Z
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 #include "window.cuh"
 
@@ -46,29 +54,65 @@ constexpr int kWarps = 4;
 __host__ __device__ constexpr int brev3(int x) { return ((x & 1) << 2) | (x & 2) | ((x >> 2) & 1); }
 __device__ __forceinline__ int srow(int c) { return (c & ~7) | brev3(c & 7); }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
 __device__ __forceinline__ void cp_async16(void* s, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(s)),
-               "l"(g));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g));
 }
 __device__ __forceinline__ void cp_async4(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(s)),
-               "l"(g));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait_all() {
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, int col, int r0,
+                                            int r1, int r2, int r3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+      "r"(smem_u32(bar))
+      : "memory");
+}
 
+// Staged-row geometry. Rows are stored exactly as the TMA swizzle writes
+// them (region bases 1024-B aligned): 16-B chunk k of row s goes to
+// k ^ ((s * rowbytes >> 7) & mask). NT=8 rows are split into two 128-B
+// halves stored in two regions.
 template <int NT>
 struct Geo {
-  static constexpr int DS = 8 * NT;                  // staged row stride (floats)
-  static constexpr int CH = DS / 4;                  // 16-B chunks per row
-  static constexpr int CHM = (CH < 8 ? CH : 8) - 1;  // swizzle mask
+  static constexpr int BW = NT >= 4 ? 32 : 8 * NT;  // floats per TMA box row
+  static constexpr int HALVES = NT == 8 ? 2 : 1;
+  static constexpr int DS = 8 * NT;                  // features per staged row
   static constexpr int V = NT < 4 ? NT : 4;          // fragment read vector width
+  __host__ __device__ static constexpr int swz(int s) {
+    return BW == 32 ? (s & 7) : BW == 16 ? ((s >> 1) & 3) : ((s >> 2) & 1);
+  }
+  template <int CPR>
   __host__ __device__ static constexpr int off(int s, int f) {
-    return s * DS + ((((f >> 2) ^ (s & CHM)) << 2) | (f & 3));
+    return (f / BW) * CPR * BW + s * BW + ((((f % BW) >> 2) ^ swz(s)) << 2) + (f & 3);
   }
 };
 
@@ -78,15 +122,17 @@ struct Carve {
   static constexpr bool kFused = MODE == MODE_AGNN_FWD || MODE == MODE_AGNN_BWD;
   static constexpr int CPR = cols_per_round(NT, MODE);
   static constexpr int tile_stride = CPR + 4;
-  static constexpr int rps = 0;  // 2 x 17 int64
-  static constexpr int xs = 288;
+  static constexpr int xs = 0;  // 1024-B aligned
   static constexpr int xs_bytes = CPR * 8 * NT * 4;
   static constexpr int frag = xs + xs_bytes * (kDual ? 2 : 1);
   static constexpr int frag_a = (CPR / 8) * 512 * (kDual ? 2 : 1);
   static constexpr int frag_t = (kFused || MODE == MODE_SDDMM) ? 16 * tile_stride * 4 : 0;
   static constexpr int frag_bytes = frag_a > frag_t ? frag_a : frag_t;
   static constexpr int edges = frag + frag_bytes;
-  static constexpr int total = (edges + (kFused ? kEdgesPerWindow * 4 : 0) + 127) & ~127;
+  static constexpr int rps = edges + (kFused ? kEdgesPerWindow * 4 : 0);  // 2 x 17 int64
+  static constexpr int nodes = rps + 288;                                  // CPR int
+  static constexpr int bar = nodes + CPR * 4;                              // mbarrier
+  static constexpr int total = (bar + 8 + 1023) & ~1023;
 };
 
 template <int VW>
@@ -110,46 +156,52 @@ __device__ __forceinline__ void decode_slot(int fi, int& row, int& col) {
 }
 
 template <int NT, int MODE>
-__global__ void __launch_bounds__(kWarps * 32) window_kernel(Params p) {
+__global__ void __launch_bounds__(kWarps * 32)
+    window_kernel(const Params p, const __grid_constant__ CUtensorMap tmx,
+                  const __grid_constant__ CUtensorMap tmx2) {
   using G = Geo<NT>;
   using CV = Carve<NT, MODE>;
   constexpr int CPR = CV::CPR;
   constexpr int DS = G::DS;
   constexpr int V = G::V;
   constexpr int NQ = NT / V;
-  constexpr int NPF = CPR / 32;    // prefetched col_to_node registers per lane
-  constexpr int RPI = 32 / G::CH;  // staged rows per warp instruction
-  constexpr int IPK = 32 / RPI;    // instructions per 32 rows
+  constexpr int NPF = CPR / 32;  // prefetched col_to_node registers per lane
   constexpr bool kDual = CV::kDual;
   constexpr bool kFused = CV::kFused;
   constexpr bool kSpmmPhase = MODE != MODE_SDDMM;
   constexpr bool kSddmmPhase = MODE == MODE_SDDMM || kFused;
   constexpr int TS = CV::tile_stride;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int XS2 = CPR * DS;  // floats between the two operands' regions (dual)
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   unsigned char* sm = smem_raw + warp * CV::total;
-  int64_t* rps2 = reinterpret_cast<int64_t*>(sm + CV::rps);  // [2][17]
+  if ((smem_u32(sm) & 1023) != 0) __trap();  // TMA swizzle needs 1024-B aligned rows
   float* xs = reinterpret_cast<float*>(sm + CV::xs);
   uint32_t* afrag = reinterpret_cast<uint32_t*>(sm + CV::frag);
   uint32_t* afrag2 = afrag + (CPR / 8) * 128;
   float* tile = reinterpret_cast<float*>(sm + CV::frag);
   float* escore = reinterpret_cast<float*>(sm + CV::edges);
+  int64_t* rps2 = reinterpret_cast<int64_t*>(sm + CV::rps);  // [2][17]
+  int* nodes = reinterpret_cast<int*>(sm + CV::nodes);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + CV::bar);
 
   // zero the staged rows once: feature padding [dim, DS) is never written
   for (int i = lane; i < CPR * DS * (kDual ? 2 : 1); i += 32) xs[i] = 0.f;
+  if (lane == 0) mbar_init(bar);
+  uint32_t phase = 0;
+  __syncwarp();
 
   // per-lane fragment offsets (floats) within an 8-row (SpMM) / 16-row
   // (SDDMM) block of staged rows; blocks add a constant stride
   int spo0[NQ], spo1[NQ], sdo0[NQ], sdo1[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
-    spo0[q] = G::off(brev3(t), g * NT + q * V);
-    spo1[q] = G::off(brev3(t + 4), g * NT + q * V);
-    sdo0[q] = G::off(brev3(g), t * NT + q * V);
-    sdo1[q] = G::off(brev3(g), (t + 4) * NT + q * V);
+    spo0[q] = G::template off<CPR>(brev3(t), g * NT + q * V);
+    spo1[q] = G::template off<CPR>(brev3(t + 4), g * NT + q * V);
+    sdo0[q] = G::template off<CPR>(brev3(g), t * NT + q * V);
+    sdo1[q] = G::template off<CPR>(brev3(g), (t + 4) * NT + q * V);
   }
-  const int ch = lane % G::CH, rsub = lane / G::CH;  // staging: chunk, row-in-group
 
   const int64_t nwarps = (int64_t)gridDim.x * kWarps;
   const int64_t tasks = p.nwin * p.nchunks;
@@ -185,9 +237,8 @@ __global__ void __launch_bounds__(kWarps * 32) window_kernel(Params p) {
     if (lane <= 16) rps[lane] = pf_rp;
     const int64_t c0 = pf_c0;
     const int u = (int)(pf_cend - pf_c0);
-    int cur_node[NPF];
 #pragma unroll
-    for (int k = 0; k < NPF; ++k) cur_node[k] = pf_node[k];
+    for (int k = 0; k < NPF; ++k) nodes[lane + 32 * k] = pf_node[k];
     __syncwarp();
     const int64_t e0 = rps[0], e1 = rps[16];
     const int E = (int)(e1 - e0);
@@ -204,60 +255,57 @@ __global__ void __launch_bounds__(kWarps * 32) window_kernel(Params p) {
       const int pad = min(CPR, (max(ncols, 0) + 15) & ~15);
       if (rd > 0) {
         __syncwarp();
-#pragma unroll
-        for (int k = 0; k < NPF; ++k) {
-          const int c = cb + lane + 32 * k;
-          cur_node[k] = c < u ? (int)__ldg(p.c2n + c0 + c) : 0;
-        }
+        for (int c = lane; c < ncols; c += 32) nodes[c] = (int)__ldg(p.c2n + c0 + cb + c);
+        __syncwarp();
       }
       for (int kc = 0; kc < nkc; ++kc) {
         // SDDMM folds D in k-chunks of 8*NT features; SpMM modes use one chunk
         const int dk = MODE == MODE_SDDMM ? kc * 8 * NT : d0;
         const int dv = min(8 * NT, p.dim - dk);
         if (kc > 0) __syncwarp();
-        // ---- 1. FetchDense: stage rows [0, ncols), zero rows [ncols, pad) ----
-        if (p.vec16) {
-          const bool chv = ch * 4 < dv;
-          const float* xl = p.x + dk + ch * 4;
-          const float* xl2 = kDual ? p.x2 + dk + ch * 4 : nullptr;
+        // ---- 1. FetchDense: stage rows [0, ncols) ----
+        const bool staged_tma = p.use_tma && pad > 0;
+        if (staged_tma) {
+          constexpr uint32_t kGroupBytes = 4u * G::BW * 4u * G::HALVES * (kDual ? 2 : 1);
+          fence_proxy_async();  // previous generic reads of xs before async writes
+          __syncwarp();
+          if (lane == 0) mbar_expect(bar, (uint32_t)(pad / 4) * kGroupBytes);
+          __syncwarp();
+          if (lane < pad / 4) {
+            int rr[4];
 #pragma unroll
-          for (int k = 0; k < NPF; ++k) {
-            if (32 * k >= pad) break;
+            for (int r = 0; r < 4; ++r) {
+              const int srw = 4 * lane + r;
+              const int c = (srw & ~7) | brev3(srw & 7);
+              rr[r] = c < ncols ? nodes[c] : (int)p.n;  // out of range -> zero fill
+            }
+            float* dst = xs + 4 * lane * G::BW;
 #pragma unroll
-            for (int i = 0; i < IPK; ++i) {
-              const int cl = RPI * i + rsub;  // column within this 32-group
-              const int c = 32 * k + cl;
-              const int node = __shfl_sync(0xffffffffu, cur_node[k], cl);
-              float* dst = xs + G::off(srow(c), ch * 4);
-              if (c < ncols) {
-                if (chv) {
-                  cp_async16(dst, xl + (int64_t)node * p.ldx);
-                  if (kDual) cp_async16(dst + CPR * DS, xl2 + (int64_t)node * p.ldx2);
-                }
-              } else if (c < pad) {
-                *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (kDual)
-                  *reinterpret_cast<float4*>(dst + CPR * DS) = make_float4(0.f, 0.f, 0.f, 0.f);
-              }
+            for (int hv = 0; hv < G::HALVES; ++hv) {
+              tma_gather4(dst + hv * CPR * G::BW, &tmx, dk + hv * 32, rr[0], rr[1], rr[2], rr[3],
+                          bar);
+              if (kDual)
+                tma_gather4(dst + XS2 + hv * CPR * G::BW, &tmx2, dk + hv * 32, rr[0], rr[1],
+                            rr[2], rr[3], bar);
             }
           }
-        } else {
+        } else if (pad > 0) {
           for (int q = lane; q < pad * DS; q += 32) {
             const int c = q / DS, f = q % DS;
-            float* dst = xs + G::off(srow(c), f);
+            float* dst = xs + G::template off<CPR>(srow(c), f);
             if (c < ncols) {
               if (f < dv) {
-                const int64_t node = (int64_t)__ldg(p.c2n + c0 + cb + c);
+                const int64_t node = nodes[c];
                 cp_async4(dst, p.x + node * p.ldx + dk + f);
-                if (kDual) cp_async4(dst + CPR * DS, p.x2 + node * p.ldx2 + dk + f);
+                if (kDual) cp_async4(dst + XS2, p.x2 + node * p.ldx2 + dk + f);
               }
             } else {
               *dst = 0.f;
-              if (kDual) dst[CPR * DS] = 0.f;
+              if (kDual) dst[XS2] = 0.f;
             }
           }
+          cp_commit();
         }
-        cp_commit();
         // ---- prefetch the next task (overlaps the gather) ----
         if ((rd == nrounds - 1 || nrounds == 0) && kc == nkc - 1) prefetch(task + nwarps);
 
@@ -325,7 +373,12 @@ __global__ void __launch_bounds__(kWarps * 32) window_kernel(Params p) {
             }
           }
         }
-        cp_wait_all();
+        if (staged_tma) {
+          mbar_wait(bar, phase);
+          phase ^= 1;
+        } else {
+          cp_wait_all();
+        }
         __syncwarp();
 
         // ---- 3a. SDDMM phase: scores for 16-column paired blocks ----
@@ -342,7 +395,7 @@ __global__ void __launch_bounds__(kWarps * 32) window_kernel(Params p) {
             float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-              const float* blk = xs + (sb * 16 + hh * 8) * DS;
+              const float* blk = xs + (sb * 16 + hh * 8) * G::BW;
               float b0[NT], b1[NT];
 #pragma unroll
               for (int q = 0; q < NQ; ++q) {
@@ -436,7 +489,7 @@ __global__ void __launch_bounds__(kWarps * 32) window_kernel(Params p) {
 #pragma unroll 2
         for (int b = 0; b < nb; ++b) {
           const uint4 af = reinterpret_cast<const uint4*>(afrag)[b * 32 + lane];
-          const float* blk = xs + b * 8 * DS;
+          const float* blk = xs + b * 8 * G::BW;
           float x0[NT], x1[NT];
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
@@ -448,7 +501,7 @@ __global__ void __launch_bounds__(kWarps * 32) window_kernel(Params p) {
             mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
           if constexpr (kDual) {
             const uint4 af2 = reinterpret_cast<const uint4*>(afrag2)[b * 32 + lane];
-            const float* blk2 = blk + CPR * DS;
+            const float* blk2 = blk + XS2;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
               lds_vec<V>(x0 + q * V, blk2 + spo0[q]);
@@ -555,6 +608,68 @@ __global__ void edge_frag_kernel(const int64_t* __restrict__ ptr, const uint32_t
   }
 }
 
+// ---- host: tensor maps for the gathered operands ----------------------------
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+struct TmKey {
+  const void* x;
+  int64_t n, dim, ld;
+  int bw;
+  bool operator==(const TmKey& o) const {
+    return x == o.x && n == o.n && dim == o.dim && ld == o.ld && bw == o.bw;
+  }
+};
+struct TmHash {
+  size_t operator()(const TmKey& k) const {
+    return std::hash<const void*>()(k.x) ^ (size_t)(k.n * 1315423911u) ^ (size_t)(k.ld << 7) ^
+           (size_t)k.bw;
+  }
+};
+
+// fp32 [n rows, dim cols] with row stride ld; box = (bw cols, 1 row) for gather4
+bool make_tmap(const float* x, int64_t n, int64_t dim, int64_t ld, int bw, CUtensorMap* out) {
+  static std::mutex mu;
+  static std::unordered_map<TmKey, CUtensorMap, TmHash> cache;
+  const TmKey key{x, n, dim, ld, bw};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)dim, (cuuint64_t)n};
+  cuuint64_t gstride[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)bw, 1};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle swz = bw == 32   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : bw == 16 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                            : CU_TENSOR_MAP_SWIZZLE_32B;
+  CUtensorMap tm;
+  if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x), gdim, gstride, box, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, tm);
+  *out = tm;
+  return true;
+}
+
 int edge_frag(const int64_t* ptr, const uint32_t* e2c, int64_t n, uint32_t* efrag,
               cudaStream_t s) {
   if (n == 0) return TCG_OK;
@@ -564,8 +679,9 @@ int edge_frag(const int64_t* ptr, const uint32_t* e2c, int64_t n, uint32_t* efra
 }
 
 template <int NT, int MODE>
-int launch_nt(const Params& p, cudaStream_t s) {
+int launch_nt(Params& p, cudaStream_t s) {
   using CV = Carve<NT, MODE>;
+  using G = Geo<NT>;
   const size_t smem = (size_t)CV::total * kWarps;
   auto kern = window_kernel<NT, MODE>;
   static int configured_dev = -1;
@@ -580,18 +696,28 @@ int launch_nt(const Params& p, cudaStream_t s) {
     if (per_sm < 1) per_sm = 1;
     configured_dev = dev;
   }
+  // TMA gather legality: 16-B aligned base and row stride, int32 row ids
+  CUtensorMap tm1{}, tm2{};
+  const bool dual = MODE == MODE_SPMM_DUAL;
+  const int64_t tcols = p.dim;
+  bool tma = p.n < (1LL << 31) - 1 && p.ldx % 4 == 0 &&
+             (reinterpret_cast<uintptr_t>(p.x) & 15) == 0 &&
+             (!dual || (p.ldx2 % 4 == 0 && (reinterpret_cast<uintptr_t>(p.x2) & 15) == 0));
+  if (tma) tma = make_tmap(p.x, p.n, tcols, p.ldx, G::BW, &tm1);
+  if (tma && dual) tma = make_tmap(p.x2, p.n, tcols, p.ldx2, G::BW, &tm2);
+  p.use_tma = tma ? 1 : 0;
   const int64_t tasks = p.nwin * p.nchunks;
   int64_t blocks = (tasks + kWarps - 1) / kWarps;
   const int64_t cap = (int64_t)num_sms() * per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) return TCG_OK;
-  kern<<<(unsigned)blocks, kWarps * 32, smem, s>>>(p);
+  kern<<<(unsigned)blocks, kWarps * 32, smem, s>>>(p, tm1, tm2);
   TCG_LAUNCHED("window_kernel");
   return TCG_OK;
 }
 
 template <int MODE>
-int launch_mode(int nt, const Params& p, cudaStream_t s) {
+int launch_mode(int nt, Params& p, cudaStream_t s) {
   switch (nt) {
     case 1: return launch_nt<1, MODE>(p, s);
     case 2: return launch_nt<2, MODE>(p, s);
@@ -600,7 +726,7 @@ int launch_mode(int nt, const Params& p, cudaStream_t s) {
   }
 }
 
-int launch(int mode, int nt, const Params& p, cudaStream_t s) {
+int launch(int mode, int nt, Params& p, cudaStream_t s) {
   switch (mode) {
     case MODE_SPMM: return launch_mode<MODE_SPMM>(nt, p, s);
     case MODE_SPMM_DUAL: return launch_mode<MODE_SPMM_DUAL>(nt, p, s);

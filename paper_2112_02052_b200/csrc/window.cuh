@@ -1,6 +1,7 @@
 // Row-window engine interface (see window.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -31,6 +32,7 @@ struct Params {
   int dim;
   int vec16;    // 16-B staging legal (dim, ld, base aligned)
   int vec_out;  // 16-B output stores legal
+  int use_tma;  // stage rows with TMA gather4 (tensor maps valid)
   // gathered operand(s)
   const float* x;
   int64_t ldx;
@@ -55,7 +57,7 @@ struct Params {
   int epilogue;
 };
 
-int launch(int mode, int nt, const Params& p, cudaStream_t s);
+int launch(int mode, int nt, Params& p, cudaStream_t s);
 
 // per-edge fragment slots of a 16x8 tiling (InitSparse addresses)
 int edge_frag(const int64_t* ptr, const uint32_t* e2c, int64_t n, uint32_t* efrag,
