@@ -122,17 +122,17 @@ struct Carve {
   static constexpr bool kFused = MODE == MODE_AGNN_FWD || MODE == MODE_AGNN_BWD;
   static constexpr int CPR = cols_per_round(NT, MODE);
   static constexpr int tile_stride = CPR + 4;
-  static constexpr int xs = 0;  // 1024-B aligned
-  static constexpr int xs_bytes = CPR * 8 * NT * 4;
-  static constexpr int frag = xs + xs_bytes * (kDual ? 2 : 1);
+  static constexpr int xs_bytes = CPR * 8 * NT * 4 * (kDual ? 2 : 1);  // one stage
+  static constexpr int xs = 0;                                          // 2 stages, 1024-B aligned
+  static constexpr int frag = xs + 2 * xs_bytes;
   static constexpr int frag_a = (CPR / 8) * 512 * (kDual ? 2 : 1);
   static constexpr int frag_t = (kFused || MODE == MODE_SDDMM) ? 16 * tile_stride * 4 : 0;
   static constexpr int frag_bytes = frag_a > frag_t ? frag_a : frag_t;
   static constexpr int edges = frag + frag_bytes;
-  static constexpr int rps = edges + (kFused ? kEdgesPerWindow * 4 : 0);  // 2 x 17 int64
-  static constexpr int nodes = rps + 288;                                  // CPR int
-  static constexpr int bar = nodes + CPR * 4;                              // mbarrier
-  static constexpr int total = (bar + 8 + 1023) & ~1023;
+  static constexpr int rps = edges + (kFused ? kEdgesPerWindow * 4 : 0);  // 17 int64
+  static constexpr int nodes = rps + 136;                                  // CPR int
+  static constexpr int bar = (nodes + CPR * 4 + 7) & ~7;                   // 2 mbarriers
+  static constexpr int total = (bar + 16 + 1023) & ~1023;
 };
 
 template <int VW>
@@ -155,6 +155,14 @@ __device__ __forceinline__ void decode_slot(int fi, int& row, int& col) {
   col = (fi >> 7) * 8 + (ln & 3) + 4 * (sl >> 1);
 }
 
+// Per-window metadata carried in registers through the software pipeline.
+struct Meta {
+  int64_t w;     // window id (-1: no task)
+  int chunk;     // feature chunk (SpMM modes)
+  int64_t rp;    // lane <= 16: node_ptr[min(16*w + lane, n)]
+  int64_t c0, cend;
+};
+
 template <int NT, int MODE>
 __global__ void __launch_bounds__(kWarps * 32)
     window_kernel(const Params p, const __grid_constant__ CUtensorMap tmx,
@@ -165,31 +173,36 @@ __global__ void __launch_bounds__(kWarps * 32)
   constexpr int DS = G::DS;
   constexpr int V = G::V;
   constexpr int NQ = NT / V;
-  constexpr int NPF = CPR / 32;  // prefetched col_to_node registers per lane
+  constexpr int NPF = CPR / 32;  // col_to_node registers per lane
   constexpr bool kDual = CV::kDual;
   constexpr bool kFused = CV::kFused;
   constexpr bool kSpmmPhase = MODE != MODE_SDDMM;
   constexpr bool kSddmmPhase = MODE == MODE_SDDMM || kFused;
   constexpr int TS = CV::tile_stride;
-  constexpr int XS2 = CPR * DS;  // floats between the two operands' regions (dual)
+  constexpr int XS2 = CPR * DS;                 // floats to the second operand (dual)
+  constexpr int XSTAGE = CV::xs_bytes / 4;      // floats per pipeline stage
+  constexpr int EV = kFused ? kEdgesPerWindow / 32 : 4;  // prefetched edges / 32
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   unsigned char* sm = smem_raw + warp * CV::total;
   if ((smem_u32(sm) & 1023) != 0) __trap();  // TMA swizzle needs 1024-B aligned rows
-  float* xs = reinterpret_cast<float*>(sm + CV::xs);
+  float* xs_base = reinterpret_cast<float*>(sm + CV::xs);
   uint32_t* afrag = reinterpret_cast<uint32_t*>(sm + CV::frag);
   uint32_t* afrag2 = afrag + (CPR / 8) * 128;
   float* tile = reinterpret_cast<float*>(sm + CV::frag);
   float* escore = reinterpret_cast<float*>(sm + CV::edges);
-  int64_t* rps2 = reinterpret_cast<int64_t*>(sm + CV::rps);  // [2][17]
-  int* nodes = reinterpret_cast<int*>(sm + CV::nodes);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + CV::bar);
+  int64_t* rps = reinterpret_cast<int64_t*>(sm + CV::rps);
+  int* nodes_s = reinterpret_cast<int*>(sm + CV::nodes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + CV::bar);
 
-  // zero the staged rows once: feature padding [dim, DS) is never written
-  for (int i = lane; i < CPR * DS * (kDual ? 2 : 1); i += 32) xs[i] = 0.f;
-  if (lane == 0) mbar_init(bar);
-  uint32_t phase = 0;
+  // zero both stages once: feature padding [dim, DS) is never written
+  for (int i = lane; i < 2 * XSTAGE; i += 32) xs_base[i] = 0.f;
+  if (lane == 0) {
+    mbar_init(bars);
+    mbar_init(bars + 1);
+  }
+  uint32_t ph0 = 0, ph1 = 0;
   __syncwarp();
 
   // per-lane fragment offsets (floats) within an 8-row (SpMM) / 16-row
@@ -205,111 +218,208 @@ __global__ void __launch_bounds__(kWarps * 32)
 
   const int64_t nwarps = (int64_t)gridDim.x * kWarps;
   const int64_t tasks = p.nwin * p.nchunks;
-  int64_t task = (int64_t)blockIdx.x * kWarps + warp;
+  const int nkc = MODE == MODE_SDDMM ? p.nkc : 1;
 
-  // ---- prefetch registers for the next task ----
-  int64_t pf_rp = 0, pf_c0 = 0, pf_cend = 0;
-  int pf_node[NPF];
-  auto prefetch = [&](int64_t tk) {
-    if (tk >= tasks) return;
-    const int64_t w = p.win_begin + tk / p.nchunks;
-    const int64_t r0 = w * 16;
-    pf_rp = lane <= 16 ? __ldg(p.ptr + min(r0 + lane, p.n)) : 0;
-    pf_c0 = __ldg(p.coff + w);
-    pf_cend = __ldg(p.coff + w + 1);
-    const int64_t u = pf_cend - pf_c0;
+  // ------------------------------------------------------------------ //
+  // pipeline helpers
+  // ------------------------------------------------------------------ //
+  auto load_meta = [&](int64_t tk) {
+    Meta m;
+    if (tk >= tasks) {
+      m.w = -1, m.chunk = 0, m.rp = 0, m.c0 = 0, m.cend = 0;
+      return m;
+    }
+    m.w = p.win_begin + tk / p.nchunks;
+    m.chunk = (int)(tk % p.nchunks);
+    m.rp = lane <= 16 ? __ldg(p.ptr + min(m.w * 16 + lane, p.n)) : 0;
+    m.c0 = __ldg(p.coff + m.w);
+    m.cend = __ldg(p.coff + m.w + 1);
+    return m;
+  };
+  // col_to_node of the first CPR columns (out-of-range row id beyond u)
+  auto load_nodes = [&](const Meta& m, int cb, int (&nd)[NPF]) {
+    const int u = m.w < 0 ? 0 : (int)(m.cend - m.c0);
 #pragma unroll
     for (int k = 0; k < NPF; ++k) {
-      const int c = lane + 32 * k;
-      pf_node[k] = c < u ? (int)__ldg(p.c2n + pf_c0 + c) : 0;
+      const int c = cb + lane + 32 * k;
+      nd[k] = c < u ? (int)__ldg(p.c2n + m.c0 + c) : (int)p.n;
     }
   };
-  prefetch(task);
-  int buf = 0;
-
-  for (; task < tasks; task += nwarps, buf ^= 1) {
-    const int64_t w = p.win_begin + task / p.nchunks;
-    const int chunk = (int)(task % p.nchunks);
-    const int d0 = chunk * 8 * NT;
-    const int64_t r0 = w * 16;
-    const int64_t r1 = min(r0 + 16, p.n);
-    int64_t* rps = rps2 + buf * 17;
-    if (lane <= 16) rps[lane] = pf_rp;
-    const int64_t c0 = pf_c0;
-    const int u = (int)(pf_cend - pf_c0);
+  // edge data of the first 32*EV edges: fragment slot (+ weights / P)
+  auto load_edges = [&](const Meta& m, uint32_t (&ef)[EV], float (&wa)[EV], float (&wb)[EV]) {
+    const int64_t e0 = __shfl_sync(0xffffffffu, m.rp, 0);
+    const int64_t e1 = __shfl_sync(0xffffffffu, m.rp, 16);
 #pragma unroll
-    for (int k = 0; k < NPF; ++k) nodes[lane + 32 * k] = pf_node[k];
+    for (int v = 0; v < EV; ++v) {
+      const int64_t e = e0 + lane + 32 * v;
+      const bool ok = m.w >= 0 && e < e1;
+      ef[v] = ok ? __ldg(p.efrag + e) : 0xffffffffu;
+      wa[v] = 1.f;
+      wb[v] = 1.f;
+      if constexpr (MODE == MODE_SPMM || kDual) {
+        if (ok && p.w) wa[v] = p.widx ? __ldg(p.w + __ldg(p.widx + e)) : __ldg(p.w + e);
+      }
+      if constexpr (kDual) {
+        if (ok && p.w2) wb[v] = p.widx2 ? __ldg(p.w2 + __ldg(p.widx2 + e)) : __ldg(p.w2 + e);
+      }
+      if constexpr (MODE == MODE_AGNN_BWD) {
+        if (ok) wa[v] = __ldg(p.aux + e);
+      }
+    }
+  };
+  // the window's own 16 rows (SDDMM A operand), feature chunk at dk
+  auto load_arows = [&](const Meta& m, int dk, float (&ar)[4][NT]) {
+    const int64_t r0 = m.w * 16, r1 = min(r0 + 16, p.n);
+    const int dv = min(8 * NT, p.dim - dk);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int64_t r = r0 + g + ((h & 1) ? 8 : 0);
+      const int f0 = ((h & 2) ? (t + 4) : t) * NT;
+      const bool rok = m.w >= 0 && r < r1;
+      const float* src = p.xa + r * p.lda + dk + f0;
+      bool done = false;
+      if constexpr (NT % 4 == 0) {
+        if (p.vec16 && rok && f0 + NT <= dv) {
+#pragma unroll
+          for (int j = 0; j < NT; j += 4) {
+            const float4 q4 = __ldg(reinterpret_cast<const float4*>(src + j));
+            ar[h][j] = q4.x, ar[h][j + 1] = q4.y, ar[h][j + 2] = q4.z, ar[h][j + 3] = q4.w;
+          }
+          done = true;
+        }
+      }
+      if (!done) {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) ar[h][j] = (rok && f0 + j < dv) ? __ldg(src + j) : 0.f;
+      }
+    }
+  };
+  // FetchDense into stage `st`: returns true if a TMA transaction was issued
+  auto stage_rows = [&](const Meta& m, const int (&nd)[NPF], int cb, int dk, int st) -> bool {
+    const int u = m.w < 0 ? 0 : (int)(m.cend - m.c0);
+    const int ncols = min(CPR, u - cb);
+    if (ncols <= 0) return false;
+    const int pad = min(CPR, (ncols + 15) & ~15);
+    float* xs = xs_base + st * XSTAGE;
+    fence_proxy_async();  // earlier generic reads of this stage before async writes
+#pragma unroll
+    for (int k = 0; k < NPF; ++k) nodes_s[lane + 32 * k] = nd[k];
+    __syncwarp();
+    if (p.use_tma) {
+      constexpr uint32_t kGroupBytes = 4u * G::BW * 4u * G::HALVES * (kDual ? 2 : 1);
+      if (lane == 0) mbar_expect(bars + st, (uint32_t)(pad / 4) * kGroupBytes);
+      __syncwarp();
+      if (lane < pad / 4) {
+        int rr[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int srw = 4 * lane + r;
+          rr[r] = nodes_s[(srw & ~7) | brev3(srw & 7)];
+        }
+        float* dst = xs + 4 * lane * G::BW;
+#pragma unroll
+        for (int hv = 0; hv < G::HALVES; ++hv) {
+          tma_gather4(dst + hv * CPR * G::BW, &tmx, dk + hv * 32, rr[0], rr[1], rr[2], rr[3],
+                      bars + st);
+          if (kDual)
+            tma_gather4(dst + XS2 + hv * CPR * G::BW, &tmx2, dk + hv * 32, rr[0], rr[1], rr[2],
+                        rr[3], bars + st);
+        }
+      }
+      return true;
+    }
+    const int dv = min(8 * NT, p.dim - dk);
+    for (int q = lane; q < pad * DS; q += 32) {
+      const int c = q / DS, f = q % DS;
+      float* dst = xs + G::template off<CPR>(srow(c), f);
+      if (c < ncols) {
+        if (f < dv) {
+          const int64_t node = nodes_s[c];
+          cp_async4(dst, p.x + node * p.ldx + dk + f);
+          if (kDual) cp_async4(dst + XS2, p.x2 + node * p.ldx2 + dk + f);
+        }
+      } else {
+        *dst = 0.f;
+        if (kDual) dst[XS2] = 0.f;
+      }
+    }
+    cp_commit();
+    return false;
+  };
+  auto wait_stage = [&](bool tma, int st) {
+    if (tma) {
+      if (st == 0) {
+        mbar_wait(bars, ph0);
+        ph0 ^= 1;
+      } else {
+        mbar_wait(bars + 1, ph1);
+        ph1 ^= 1;
+      }
+    } else {
+      cp_wait_all();
+    }
+    __syncwarp();
+  };
+
+  // ------------------------------------------------------------------ //
+  // prologue: metadata 3 tasks ahead, nodes 2 ahead, rows + edges 1 ahead
+  // ------------------------------------------------------------------ //
+  int64_t task = (int64_t)blockIdx.x * kWarps + warp;
+  Meta m0 = load_meta(task), m1 = load_meta(task + nwarps), m2 = load_meta(task + 2 * nwarps);
+  int n0[NPF], n1[NPF];
+  load_nodes(m0, 0, n0);
+  load_nodes(m1, 0, n1);
+  uint32_t ef0[EV];
+  float wa0[EV], wb0[EV];
+  load_edges(m0, ef0, wa0, wb0);
+  float ar0[kSddmmPhase ? 4 : 1][kSddmmPhase ? NT : 1];
+  if constexpr (kSddmmPhase) load_arows(m0, m0.chunk * 0, ar0);
+  bool tma0 = stage_rows(m0, n0, 0, MODE == MODE_SDDMM ? 0 : m0.chunk * 8 * NT, 0);
+  int st = 0;
+
+  for (; task < tasks; task += nwarps) {
+    // ---- 1. issue the next window's gather, prefetch further ahead ----
+    const bool tma1 = stage_rows(m1, n1, 0, MODE == MODE_SDDMM ? 0 : m1.chunk * 8 * NT, st ^ 1);
+    uint32_t ef1[EV];
+    float wa1[EV], wb1[EV];
+    load_edges(m1, ef1, wa1, wb1);
+    float ar1[kSddmmPhase ? 4 : 1][kSddmmPhase ? NT : 1];
+    if constexpr (kSddmmPhase) load_arows(m1, 0, ar1);
+    int n2[NPF];
+    load_nodes(m2, 0, n2);
+    const Meta m3 = load_meta(task + 3 * nwarps);
+
+    // ---- 2. compute the current window ----
+    const int64_t w = m0.w;
+    const int d0 = m0.chunk * 8 * NT;
+    const int64_t r0 = w * 16, r1 = min(r0 + 16, p.n);
+    if (lane <= 16) rps[lane] = m0.rp;
     __syncwarp();
     const int64_t e0 = rps[0], e1 = rps[16];
     const int E = (int)(e1 - e0);
+    const int u = (int)(m0.cend - m0.c0);
     const int nrounds = kFused ? 1 : (u + CPR - 1) / CPR;
-    const int nkc = MODE == MODE_SDDMM ? p.nkc : 1;
 
     float acc[NT][4];
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
 
     for (int rd = 0; rd < max(nrounds, 1); ++rd) {
-      const int cb = rd * CPR;             // first column of this round
-      const int ncols = min(CPR, u - cb);  // <= 0 for empty windows
+      const int cb = rd * CPR;
+      const int ncols = min(CPR, u - cb);
       const int pad = min(CPR, (max(ncols, 0) + 15) & ~15);
-      if (rd > 0) {
-        __syncwarp();
-        for (int c = lane; c < ncols; c += 32) nodes[c] = (int)__ldg(p.c2n + c0 + cb + c);
-        __syncwarp();
-      }
+      const float* xs = xs_base + st * XSTAGE;
+      const int fbase = cb * 16, flim = ((max(ncols, 0) + 7) >> 3) * 128;  // whole blocks
       for (int kc = 0; kc < nkc; ++kc) {
-        // SDDMM folds D in k-chunks of 8*NT features; SpMM modes use one chunk
         const int dk = MODE == MODE_SDDMM ? kc * 8 * NT : d0;
-        const int dv = min(8 * NT, p.dim - dk);
-        if (kc > 0) __syncwarp();
-        // ---- 1. FetchDense: stage rows [0, ncols) ----
-        const bool staged_tma = p.use_tma && pad > 0;
-        if (staged_tma) {
-          constexpr uint32_t kGroupBytes = 4u * G::BW * 4u * G::HALVES * (kDual ? 2 : 1);
-          fence_proxy_async();  // previous generic reads of xs before async writes
-          __syncwarp();
-          if (lane == 0) mbar_expect(bar, (uint32_t)(pad / 4) * kGroupBytes);
-          __syncwarp();
-          if (lane < pad / 4) {
-            int rr[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              const int srw = 4 * lane + r;
-              const int c = (srw & ~7) | brev3(srw & 7);
-              rr[r] = c < ncols ? nodes[c] : (int)p.n;  // out of range -> zero fill
-            }
-            float* dst = xs + 4 * lane * G::BW;
-#pragma unroll
-            for (int hv = 0; hv < G::HALVES; ++hv) {
-              tma_gather4(dst + hv * CPR * G::BW, &tmx, dk + hv * 32, rr[0], rr[1], rr[2], rr[3],
-                          bar);
-              if (kDual)
-                tma_gather4(dst + XS2 + hv * CPR * G::BW, &tmx2, dk + hv * 32, rr[0], rr[1],
-                            rr[2], rr[3], bar);
-            }
-          }
-        } else if (pad > 0) {
-          for (int q = lane; q < pad * DS; q += 32) {
-            const int c = q / DS, f = q % DS;
-            float* dst = xs + G::template off<CPR>(srow(c), f);
-            if (c < ncols) {
-              if (f < dv) {
-                const int64_t node = nodes[c];
-                cp_async4(dst, p.x + node * p.ldx + dk + f);
-                if (kDual) cp_async4(dst + XS2, p.x2 + node * p.ldx2 + dk + f);
-              }
-            } else {
-              *dst = 0.f;
-              if (kDual) dst[XS2] = 0.f;
-            }
-          }
-          cp_commit();
+        bool tma_cur = tma0;
+        if (rd > 0 || kc > 0) {  // rare: rounds / k-chunks beyond the pipelined one
+          int nd[NPF];
+          load_nodes(m0, cb, nd);
+          tma_cur = stage_rows(m0, nd, cb, dk, st);
+          if constexpr (kSddmmPhase) load_arows(m0, dk, ar0);
         }
-        // ---- prefetch the next task (overlaps the gather) ----
-        if ((rd == nrounds - 1 || nrounds == 0) && kc == nkc - 1) prefetch(task + nwarps);
-
-        // ---- 2. per-edge work while rows land ----
+        // ---- InitSparse (non-fused SpMM modes) while rows land ----
         if constexpr (kSpmmPhase && !kFused) {
           const int nb = (pad + 7) >> 3;
           for (int i = lane; i < nb * 32; i += 32) {
@@ -317,78 +427,39 @@ __global__ void __launch_bounds__(kWarps * 32)
             if (kDual) reinterpret_cast<uint4*>(afrag2)[i] = make_uint4(0, 0, 0, 0);
           }
           __syncwarp();
-          const int fbase = cb * 16, flim = ((max(ncols, 0) + 7) >> 3) * 128;  // whole blocks
-          for (int64_t eb = e0; eb < e1; eb += 128) {
-            int fi[4];
-            float wv[4], wv2[4];
+          if (rd == 0) {
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const int64_t e = eb + lane + 32 * v;
-              fi[v] = e < e1 ? (int)__ldg(p.efrag + e) - fbase : -1;
-              wv[v] = 1.f;
-              wv2[v] = 1.f;
-              if (e < e1 && p.w) wv[v] = p.widx ? __ldg(p.w + __ldg(p.widx + e)) : __ldg(p.w + e);
-              if (kDual && e < e1 && p.w2)
-                wv2[v] = p.widx2 ? __ldg(p.w2 + __ldg(p.widx2 + e)) : __ldg(p.w2 + e);
-            }
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              if (fi[v] >= 0 && fi[v] < flim) {
-                afrag[fi[v]] = tf32_rn(wv[v]);
-                if (kDual) afrag2[fi[v]] = tf32_rn(wv2[v]);
+            for (int v = 0; v < EV; ++v) {
+              const int fi = (int)ef0[v];
+              if (ef0[v] != 0xffffffffu && fi < flim) {
+                afrag[fi] = tf32_rn(wa0[v]);
+                if (kDual) afrag2[fi] = tf32_rn(wb0[v]);
               }
             }
           }
-        }
-        uint32_t efr[kFused ? kEdgesPerWindow / 32 : 1];
-        if constexpr (kFused) {
-#pragma unroll
-          for (int v = 0; v < kEdgesPerWindow / 32; ++v) {
-            const int i = lane + 32 * v;
-            efr[v] = i < E ? __ldg(p.efrag + e0 + i) : 0u;
-          }
-        }
-        // A operand of the SDDMM phase: the window's own rows, to registers
-        float ar[4][NT];
-        if constexpr (kSddmmPhase) {
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const int64_t r = r0 + g + ((h & 1) ? 8 : 0);
-            const int f0 = ((h & 2) ? (t + 4) : t) * NT;
-            const float* src = p.xa + r * p.lda + dk + f0;
-            bool done = false;
-            if constexpr (NT % 4 == 0) {
-              if (p.vec16 && r < r1 && f0 + NT <= dv) {
-#pragma unroll
-                for (int j = 0; j < NT; j += 4) {
-                  const float4 q4 = __ldg(reinterpret_cast<const float4*>(src + j));
-                  ar[h][j] = q4.x, ar[h][j + 1] = q4.y, ar[h][j + 2] = q4.z, ar[h][j + 3] = q4.w;
-                }
-                done = true;
-              }
-            }
-            if (!done) {
-#pragma unroll
-              for (int j = 0; j < NT; ++j) ar[h][j] = (r < r1 && f0 + j < dv) ? __ldg(src + j) : 0.f;
+          for (int64_t e = e0 + (rd == 0 ? 32 * EV : 0) + lane; e < e1; e += 32) {
+            const int fi = (int)__ldg(p.efrag + e) - fbase;
+            if (fi < 0 || fi >= flim) continue;
+            float wv = 1.f;
+            if (p.w) wv = p.widx ? __ldg(p.w + __ldg(p.widx + e)) : __ldg(p.w + e);
+            afrag[fi] = tf32_rn(wv);
+            if constexpr (kDual) {
+              float wv2 = 1.f;
+              if (p.w2) wv2 = p.widx2 ? __ldg(p.w2 + __ldg(p.widx2 + e)) : __ldg(p.w2 + e);
+              afrag2[fi] = tf32_rn(wv2);
             }
           }
         }
-        if (staged_tma) {
-          mbar_wait(bar, phase);
-          phase ^= 1;
-        } else {
-          cp_wait_all();
-        }
-        __syncwarp();
+        wait_stage(tma_cur, st);
 
-        // ---- 3a. SDDMM phase: scores for 16-column paired blocks ----
+        // ---- SDDMM phase: scores for 16-column paired blocks ----
         if constexpr (kSddmmPhase) {
           const int npb = pad >> 4;
           uint32_t a[4][NT];
 #pragma unroll
           for (int h = 0; h < 4; ++h)
 #pragma unroll
-            for (int j = 0; j < NT; ++j) a[h][j] = tf32_rn(ar[h][j]);
+            for (int j = 0; j < NT; ++j) a[h][j] = tf32_rn(ar0[h][j]);
           float* trow0 = tile + g * TS + 2 * t;
           float* trow1 = tile + (g + 8) * TS + 2 * t;
           for (int sb = 0; sb < npb; ++sb) {
@@ -409,81 +480,113 @@ __global__ void __launch_bounds__(kWarps * 32)
             }
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-              float2* p0 = reinterpret_cast<float2*>(trow0 + sb * 16 + hh * 8);
-              float2* p1 = reinterpret_cast<float2*>(trow1 + sb * 16 + hh * 8);
+              float2* q0 = reinterpret_cast<float2*>(trow0 + sb * 16 + hh * 8);
+              float2* q1 = reinterpret_cast<float2*>(trow1 + sb * 16 + hh * 8);
               if (kc == 0) {
-                *p0 = make_float2(sc[hh][0], sc[hh][1]);
-                *p1 = make_float2(sc[hh][2], sc[hh][3]);
+                *q0 = make_float2(sc[hh][0], sc[hh][1]);
+                *q1 = make_float2(sc[hh][2], sc[hh][3]);
               } else {
-                const float2 o0 = *p0, o1 = *p1;
-                *p0 = make_float2(o0.x + sc[hh][0], o0.y + sc[hh][1]);
-                *p1 = make_float2(o1.x + sc[hh][2], o1.y + sc[hh][3]);
+                const float2 o0 = *q0, o1 = *q1;
+                *q0 = make_float2(o0.x + sc[hh][0], o0.y + sc[hh][1]);
+                *q1 = make_float2(o1.x + sc[hh][2], o1.y + sc[hh][3]);
               }
             }
           }
-        }
-        if constexpr (kFused) {
-          // edge scores out of the tile
           __syncwarp();
-#pragma unroll
-          for (int v = 0; v < kEdgesPerWindow / 32; ++v) {
-            const int i = lane + 32 * v;
-            if (i < E) {
-              int row, col;
-              decode_slot((int)efr[v], row, col);
-              escore[i] = tile[row * TS + col];
-            }
-          }
-          __syncwarp();
-          // row softmax (fwd) / softmax backward (bwd): 2 lanes per row
-          const int row = lane >> 1, sub = lane & 1;
-          const int rb = (int)(rps[row] - e0), re = (int)(rps[row + 1] - e0);
-          if constexpr (MODE == MODE_AGNN_FWD) {
-            float m = -INFINITY;
-            for (int i = rb + sub; i < re; i += 2) m = fmaxf(m, escore[i]);
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-            float s = 0.f;
-            for (int i = rb + sub; i < re; i += 2) s += expf(escore[i] - m);
-            s += __shfl_xor_sync(0xffffffffu, s, 1);
-            for (int i = rb + sub; i < re; i += 2) escore[i] = expf(escore[i] - m) / s;
-          } else {
-            float s = 0.f;
-            for (int i = rb + sub; i < re; i += 2) s += __ldg(p.aux + e0 + i) * escore[i];
-            s += __shfl_xor_sync(0xffffffffu, s, 1);
-            for (int i = rb + sub; i < re; i += 2)
-              escore[i] = __ldg(p.aux + e0 + i) * (escore[i] - s);
-          }
-          // weights -> edge order (P or dS) and -> fragment-ordered A tiles
-          const int nb = (pad + 7) >> 3;
-          for (int i = lane; i < nb * 32; i += 32)
-            reinterpret_cast<uint4*>(afrag)[i] = make_uint4(0, 0, 0, 0);
-          __syncwarp();
-#pragma unroll
-          for (int v = 0; v < kEdgesPerWindow / 32; ++v) {
-            const int i = lane + 32 * v;
-            if (i < E) {
-              const float wgt = escore[i];
-              p.eout[e0 + i] = wgt;
-              afrag[efr[v]] = tf32_rn(wgt);
-            }
-          }
         }
       }  // k-chunks
+
       if constexpr (MODE == MODE_SDDMM) {
         // StoreSparse: raw scores of this round's columns to edge order
-        __syncwarp();
-        const int fbase = cb * 16, flim = ((max(ncols, 0) + 7) >> 3) * 128;  // whole blocks
-        for (int64_t e = e0 + lane; e < e1; e += 32) {
+        if (rd == 0) {
+#pragma unroll
+          for (int v = 0; v < EV; ++v) {
+            const int fi = (int)ef0[v];
+            if (ef0[v] != 0xffffffffu && fi < flim) {
+              int row, col;
+              decode_slot(fi, row, col);
+              p.eout[e0 + lane + 32 * v] = tile[row * TS + col];
+            }
+          }
+        }
+        for (int64_t e = e0 + (rd == 0 ? 32 * EV : 0) + lane; e < e1; e += 32) {
           const int fi = (int)__ldg(p.efrag + e) - fbase;
           if (fi < 0 || fi >= flim) continue;
           int row, col;
           decode_slot(fi, row, col);
           p.eout[e] = tile[row * TS + col];
         }
+        __syncwarp();
       }
-      __syncwarp();
+      if constexpr (kFused) {
+        // edge scores out of the tile
+#pragma unroll
+        for (int v = 0; v < EV; ++v) {
+          const int i = lane + 32 * v;
+          if (i < E) {
+            int row, col;
+            decode_slot((int)ef0[v], row, col);
+            escore[i] = tile[row * TS + col];
+          }
+        }
+        __syncwarp();
+        // row softmax (fwd) / softmax backward (bwd): 2 lanes per row
+        const int row = lane >> 1, sub = lane & 1;
+        const int rb = (int)(rps[row] - e0), re = (int)(rps[row + 1] - e0);
+        if constexpr (MODE == MODE_AGNN_FWD) {
+          float mx = -INFINITY;
+          for (int i = rb + sub; i < re; i += 2) mx = fmaxf(mx, escore[i]);
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+          float s = 0.f;
+          for (int i = rb + sub; i < re; i += 2) s += expf(escore[i] - mx);
+          s += __shfl_xor_sync(0xffffffffu, s, 1);
+          for (int i = rb + sub; i < re; i += 2) escore[i] = expf(escore[i] - mx) / s;
+          __syncwarp();
+        } else {
+          // P_e * dP_e per edge (P prefetched in wa0), then the row sums
+#pragma unroll
+          for (int v = 0; v < EV; ++v) {
+            const int i = lane + 32 * v;
+            if (i < E) escore[i] = wa0[v] * escore[i];
+          }
+          __syncwarp();
+          float s = 0.f;
+          for (int i = rb + sub; i < re; i += 2) s += escore[i];
+          s += __shfl_xor_sync(0xffffffffu, s, 1);
+          __syncwarp();
+          // dS = P dP - P * rowsum  (= P (dP - rowsum))
+          for (int i = rb + sub; i < re; i += 2) escore[i] = s;  // broadcast row sum
+          __syncwarp();
+#pragma unroll
+          for (int v = 0; v < EV; ++v) {
+            const int i = lane + 32 * v;
+            if (i < E) {
+              int rw, cl;
+              decode_slot((int)ef0[v], rw, cl);
+              const float dp = tile[rw * TS + cl];
+              escore[i] = wa0[v] * (dp - escore[i]);
+            }
+          }
+          __syncwarp();
+        }
+        // weights -> edge order (P or dS) and -> fragment-ordered A tiles
+        const int nb = (pad + 7) >> 3;
+        for (int i = lane; i < nb * 32; i += 32)
+          reinterpret_cast<uint4*>(afrag)[i] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+#pragma unroll
+        for (int v = 0; v < EV; ++v) {
+          const int i = lane + 32 * v;
+          if (i < E) {
+            const float wgt = escore[i];
+            p.eout[e0 + i] = wgt;
+            afrag[ef0[v]] = tf32_rn(wgt);
+          }
+        }
+        __syncwarp();
+      }
 
-      // ---- 3c. SpMM phase over the 16x8 blocks of this round ----
+      // ---- SpMM phase over the 16x8 blocks of this round ----
       if constexpr (kSpmmPhase) {
         const int nb = (max(ncols, 0) + 7) >> 3;
 #pragma unroll 2
@@ -512,24 +615,23 @@ __global__ void __launch_bounds__(kWarps * 32)
               mma_tf32(acc[j], af2.x, af2.y, af2.z, af2.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
           }
         }
-        __syncwarp();
       }
+      __syncwarp();
     }  // rounds
 
-    // ---- 4. epilogues after all rounds ----
+    // ---- epilogues ----
     if constexpr (MODE == MODE_SDDMM) {
-      if (p.epilogue != 0) {
-        __syncwarp();
+      if (p.epilogue != 0 && w >= 0) {
         const int row = lane >> 1, sub = lane & 1;
         const int64_t rb = rps[row], re = rps[row + 1];
         if (p.epilogue == 1) {
-          float m = -INFINITY;
-          for (int64_t i = rb + sub; i < re; i += 2) m = fmaxf(m, p.eout[i]);
-          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+          float mx = -INFINITY;
+          for (int64_t i = rb + sub; i < re; i += 2) mx = fmaxf(mx, p.eout[i]);
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
           float s = 0.f;
-          for (int64_t i = rb + sub; i < re; i += 2) s += expf(p.eout[i] - m);
+          for (int64_t i = rb + sub; i < re; i += 2) s += expf(p.eout[i] - mx);
           s += __shfl_xor_sync(0xffffffffu, s, 1);
-          for (int64_t i = rb + sub; i < re; i += 2) p.eout[i] = expf(p.eout[i] - m) / s;
+          for (int64_t i = rb + sub; i < re; i += 2) p.eout[i] = expf(p.eout[i] - mx) / s;
         } else {
           float s = 0.f;
           for (int64_t i = rb + sub; i < re; i += 2) s += __ldg(p.aux + i) * p.eout[i];
@@ -591,7 +693,26 @@ __global__ void __launch_bounds__(kWarps * 32)
       }
     }
     __syncwarp();
+
+    // ---- 3. rotate the pipeline ----
+    m0 = m1;
+    m1 = m2;
+    m2 = m3;
+#pragma unroll
+    for (int k = 0; k < NPF; ++k) n1[k] = n2[k];
+#pragma unroll
+    for (int v = 0; v < EV; ++v) ef0[v] = ef1[v], wa0[v] = wa1[v], wb0[v] = wb1[v];
+    if constexpr (kSddmmPhase) {
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) ar0[h][j] = ar1[h][j];
+    }
+    tma0 = tma1;
+    st ^= 1;
   }
+  // drain: nothing in flight is consumed after the last window (the extra
+  // stage issued for a non-existent task never starts: stage_rows skips w < 0)
 }
 
 // Per-edge fragment slot of the 16x8 tiling: one thread per row.
