@@ -64,37 +64,36 @@ __device__ __forceinline__ void decode_slot(int fi, int& row, int& col) {
 }
 
 // NT consecutive floats of row `node` starting at feature f0 (0 if node < 0
-// or past dim), vectorised when legal.
-template <int NT>
+// or past dim). FULL: dim is a multiple of the chunk width and rows are
+// 16-B aligned, so the loads are unconditional vectors (no per-load
+// branches); an absent node reads row 0 and is zeroed by a select.
+template <int NT, bool FULL>
 __device__ __forceinline__ void load_slice(float (&v)[NT], const float* __restrict__ x, int node,
-                                           int64_t ld, int f0, int dim, bool vec) {
-  if (node < 0) {
+                                           int64_t ld, int f0, int dim) {
+  const bool ok = node >= 0;
+  const float* src = x + (int64_t)(ok ? node : 0) * ld + f0;
+  if constexpr (FULL && NT % 4 == 0) {
 #pragma unroll
-    for (int j = 0; j < NT; ++j) v[j] = 0.f;
-    return;
-  }
-  const float* src = x + (int64_t)node * ld + f0;
-  if constexpr (NT % 4 == 0) {
-    if (vec && f0 + NT <= dim) {
-#pragma unroll
-      for (int j = 0; j < NT; j += 4) {
-        const float4 q = __ldg(reinterpret_cast<const float4*>(src + j));
-        v[j] = q.x, v[j + 1] = q.y, v[j + 2] = q.z, v[j + 3] = q.w;
-      }
-      return;
+    for (int j = 0; j < NT; j += 4) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(src + j));
+      v[j] = q.x, v[j + 1] = q.y, v[j + 2] = q.z, v[j + 3] = q.w;
     }
-  } else if constexpr (NT == 2) {
-    if (vec && f0 + 2 <= dim) {
-      const float2 q = __ldg(reinterpret_cast<const float2*>(src));
-      v[0] = q.x, v[1] = q.y;
-      return;
-    }
-  }
+  } else if constexpr (FULL && NT == 2) {
+    const float2 q = __ldg(reinterpret_cast<const float2*>(src));
+    v[0] = q.x, v[1] = q.y;
+  } else if constexpr (FULL) {
+    v[0] = __ldg(src);
+  } else {
 #pragma unroll
-  for (int j = 0; j < NT; ++j) v[j] = (f0 + j < dim) ? __ldg(src + j) : 0.f;
+    for (int j = 0; j < NT; ++j) v[j] = (ok && f0 + j < dim) ? __ldg(src + j) : 0.f;
+  }
+  if constexpr (FULL) {
+#pragma unroll
+    for (int j = 0; j < NT; ++j) v[j] = ok ? v[j] : 0.f;
+  }
 }
 
-template <int NT, int MODE>
+template <int NT, int MODE, bool FULL>
 __global__ void __launch_bounds__(kWarps * 32, NT >= 8 ? 2
                                                 : (NT == 4 && MODE != MODE_SPMM &&
                                                    MODE != MODE_SDDMM) ? 3 : 4)
@@ -123,7 +122,6 @@ __global__ void __launch_bounds__(kWarps * 32, NT >= 8 ? 2
 
   const int64_t nwarps = (int64_t)gridDim.x * kWarps;
   const int64_t tasks = p.nwin * p.nchunks;
-  const bool vec = p.vec16 != 0;
 
   // next-window prefetch (metadata, then its col_to_node slice)
   auto meta_of = [&](int64_t tk, int64_t& rp, int64_t& c0, int64_t& ce) {
@@ -205,7 +203,7 @@ __global__ void __launch_bounds__(kWarps * 32, NT >= 8 ? 2
             for (int h = 0; h < 4; ++h) {
               const int64_t r = r0 + g + ((h & 1) ? 8 : 0);
               const int f0 = dk + ((h & 2) ? (t + 4) : t) * NT;
-              load_slice<NT>(ar[h], p.xa, r < r1 ? (int)r : -1, p.lda, f0, p.dim, vec);
+              load_slice<NT, FULL>(ar[h], p.xa, r < r1 ? (int)r : -1, p.lda, f0, p.dim);
             }
 #pragma unroll
             for (int h = 0; h < 4; ++h)
@@ -221,9 +219,9 @@ __global__ void __launch_bounds__(kWarps * 32, NT >= 8 ? 2
             for (int hh = 0; hh < 2; ++hh) {
               const int col = sb * 16 + hh * 8 + g;
               const int node = __shfl_sync(0xffffffffu, nd[(sb * 16) >> 5], col & 31);
-              load_slice<NT>(bq[slot][2 * hh], p.x, node, p.ldx, dk + t * NT, p.dim, vec);
-              load_slice<NT>(bq[slot][2 * hh + 1], p.x, node, p.ldx, dk + (t + 4) * NT, p.dim,
-                             vec);
+              load_slice<NT, FULL>(bq[slot][2 * hh], p.x, node, p.ldx, dk + t * NT, p.dim);
+              load_slice<NT, FULL>(bq[slot][2 * hh + 1], p.x, node, p.ldx, dk + (t + 4) * NT,
+                                   p.dim);
             }
           };
 #pragma unroll
@@ -336,11 +334,11 @@ __global__ void __launch_bounds__(kWarps * 32, NT >= 8 ? 2
           const int k = (b * 8) >> 5;
           const int n0 = __shfl_sync(0xffffffffu, nd[k], (b * 8 + t) & 31);
           const int n1 = __shfl_sync(0xffffffffu, nd[k], (b * 8 + t + 4) & 31);
-          load_slice<NT>(xq[slot][0], p.x, n0, p.ldx, d0 + g * NT, p.dim, vec);
-          load_slice<NT>(xq[slot][1], p.x, n1, p.ldx, d0 + g * NT, p.dim, vec);
+          load_slice<NT, FULL>(xq[slot][0], p.x, n0, p.ldx, d0 + g * NT, p.dim);
+          load_slice<NT, FULL>(xq[slot][1], p.x, n1, p.ldx, d0 + g * NT, p.dim);
           if constexpr (kDual) {
-            load_slice<NT>(xq[slot][2], p.x2, n0, p.ldx2, d0 + g * NT, p.dim, vec);
-            load_slice<NT>(xq[slot][3], p.x2, n1, p.ldx2, d0 + g * NT, p.dim, vec);
+            load_slice<NT, FULL>(xq[slot][2], p.x2, n0, p.ldx2, d0 + g * NT, p.dim);
+            load_slice<NT, FULL>(xq[slot][3], p.x2, n1, p.ldx2, d0 + g * NT, p.dim);
           }
         };
 #pragma unroll
@@ -500,11 +498,11 @@ int edge_frag(const int64_t* ptr, const uint32_t* e2c, int64_t n, uint32_t* efra
   return TCG_OK;
 }
 
-template <int NT, int MODE>
-int launch_nt(Params& p, cudaStream_t s) {
+template <int NT, int MODE, bool FULL>
+int launch_full(Params& p, cudaStream_t s) {
   using CV = Carve<NT, MODE>;
   const size_t smem = (size_t)CV::total * kWarps;
-  auto kern = window_kernel<NT, MODE>;
+  auto kern = window_kernel<NT, MODE, FULL>;
   static int configured_dev = -1;
   static int per_sm = 1;
   int dev = 0;
@@ -526,6 +524,14 @@ int launch_nt(Params& p, cudaStream_t s) {
   kern<<<(unsigned)blocks, kWarps * 32, smem, s>>>(p);
   TCG_LAUNCHED("window_kernel");
   return TCG_OK;
+}
+
+template <int NT, int MODE>
+int launch_nt(Params& p, cudaStream_t s) {
+  // FULL: every feature chunk is complete and rows are 16-B aligned (the
+  // caller's vec16 covers x, x2 and xa) -> branch-free vector loads
+  const bool full = p.vec16 && p.dim % (8 * NT) == 0;
+  return full ? launch_full<NT, MODE, true>(p, s) : launch_full<NT, MODE, false>(p, s);
 }
 
 template <int MODE>
