@@ -158,12 +158,30 @@ extern "C" int tcg_sddmm(const tcg_tiling* t, const float* xa, int64_t lda, cons
   TCG_REQUIRE(t->edge_frag, "tcg_sddmm: tf32 needs edge_frag (tcg_edge_frag)");
   win::Params q = base_params(t, win_begin, win_end);
   const int nt = win::nt_for(dim);
-  q.nkc = (int)((dim + 8 * nt - 1) / (8 * nt));
+  const int kw = 8 * nt;  // features per launch (<= 64)
+  const int nkc = (int)((dim + kw - 1) / kw);
   q.dim = (int)dim;
   q.vec16 = vec;
   q.x = xb, q.ldx = ldb, q.xa = xa, q.lda = lda;
-  q.aux = aux, q.eout = out, q.epilogue = epilogue;
-  return win::launch(win::MODE_SDDMM, nt, q, s);
+  q.aux = aux, q.eout = out;
+  // D > 64: partial dot products per 64-feature chunk, accumulated into out;
+  // the row softmax (if any) then runs as its own pass
+  q.epilogue = nkc == 1 ? epilogue : TCG_EPI_NONE;
+  for (int kc = 0; kc < nkc; ++kc) {
+    q.koff = kc * kw;
+    q.accumulate = kc > 0;
+    const int rc = win::launch(win::MODE_SDDMM, nt, q, s);
+    if (rc != TCG_OK) return rc;
+  }
+  if (nkc > 1 && epilogue != TCG_EPI_NONE) {
+    const int64_t rb = win_begin * 16;
+    const int64_t re = win_end * 16 < t->num_nodes ? win_end * 16 : t->num_nodes;
+    // rows [rb, re): the softmax kernels index node_ptr from the first row
+    if (epilogue == TCG_EPI_SOFTMAX)
+      return tcg_segment_softmax(t->node_ptr + rb, re - rb, out, out, stream);
+    return tcg_segment_softmax_backward(t->node_ptr + rb, re - rb, aux, out, out, stream);
+  }
+  return TCG_OK;
 }
 
 extern "C" int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim,

@@ -29,6 +29,7 @@ struct Params {
   int64_t win_begin, nwin;
   int nchunks;  // feature chunks of 8*NT (SpMM modes); 1 otherwise
   int nkc;      // SDDMM k-chunks of 8*NT features
+  int koff;     // SDDMM: first feature of this launch's k-chunk
   int dim;
   int vec16;    // 16-B staging legal (dim, ld, base aligned)
   int vec_out;  // 16-B output stores legal
