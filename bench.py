@@ -298,7 +298,7 @@ def run_ours(args):
 
     def train_step():
         opt.zero_grad(set_to_none=False)
-        loss = F.nll_loss(net(x_dev, t, shard), y_dev)
+        loss = layers.cross_entropy(net(x_dev, t, shard), y_dev)
         loss.backward()
         opt.step()
         return loss.detach()
@@ -452,7 +452,7 @@ def run_ours(args):
 
             def gstep():
                 gopt.zero_grad(set_to_none=False)
-                lo = F.nll_loss(gnet(x_dev, t), y_dev)
+                lo = layers.cross_entropy(gnet(x_dev, t), y_dev)
                 lo.backward()
                 gopt.step()
                 return lo.detach()

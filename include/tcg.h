@@ -86,6 +86,10 @@ int tcg_sgt(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_node
  * (kernels.py:173-188: r_local, b_of_edge, c_local). */
 int tcg_edge_frag(const tcg_tiling* t, uint32_t* edge_frag, void* stream);
 
+/* dst[k] = src[idx[k]] — carries A's edge weights (P, dS, edge values) into
+ * A^T edge order once per backward, so the A^T SpMM reads them coalesced. */
+int tcg_permute_f32(const float* src, const uint32_t* idx, float* dst, int64_t n, void* stream);
+
 /* ---- CSR transpose (backward support; no reference counterpart — the
  * reference has no backward. SURVEY.md Appendix B restates it as
  * CsrGraph.from_edges(dst, src), graph.py:55-89) ------------------------ */
@@ -150,6 +154,25 @@ int tcg_agnn_backward(const tcg_tiling* t, const float* z, int64_t ldz, const fl
                       int64_t ldg, int64_t dim, const float* p, float* ds, float* dz,
                       int64_t lddz, int64_t dz_row0, int64_t win_begin, int64_t win_end,
                       void* stream);
+
+/* ---- dense companions of the layers (fp32; no reference counterpart beyond
+ * gcn_layer's `agg @ w + b`, kernels.py:577-582) ---------------------------- */
+/* y[n x co] = act((x .* [mask > 0]) . M + bias) (mask: [n x ci]); M is [ci x co]
+ * (m_transposed = 0) or [co x ci] (m_transposed = 1). co <= 128. */
+int tcg_dense(const float* x, int64_t ldx, int64_t n, int64_t ci, const float* m, int64_t co,
+              int32_t m_transposed, const float* bias, int32_t relu, const float* mask,
+              int64_t ldm, float* y, int64_t ldy, void* stream);
+size_t tcg_gemm_tn_workspace_bytes(int64_t n, int64_t k, int64_t c);
+/* out[k x c] = a^T b (b .* [mask > 0] when mask != null), colsum[c] = column
+ * sums of the (masked) b; deterministic fixed-order reduction. */
+int tcg_gemm_tn(const float* a, int64_t lda, const float* b, int64_t ldb, const float* mask,
+                int64_t ldm, int64_t n, int64_t k, int64_t c, float* out, float* colsum,
+                void* workspace, size_t workspace_bytes, void* stream);
+size_t tcg_softmax_xent_workspace_bytes(int64_t n);
+/* loss = mean_i -log_softmax(logits_i)[labels_i]; dlogits = (softmax - onehot)/n */
+int tcg_softmax_xent(const float* logits, int64_t ld, const int64_t* labels, int64_t n, int64_t c,
+                     float* loss, float* dlogits, void* workspace, size_t workspace_bytes,
+                     void* stream);
 
 /* ---- TF32 operand rounding: reference tiles.quantize_tf32 (67-82) ------- */
 int tcg_quantize_tf32(const float* in, float* out, int64_t n, void* stream);

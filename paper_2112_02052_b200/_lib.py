@@ -57,6 +57,7 @@ SIGNATURES = {
     "tcg_sgt_workspace_bytes": (_SZ, [_I64, _I64, _I32]),
     "tcg_sgt": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
     "tcg_edge_frag": (C.c_int, [C.POINTER(TcgTiling), _P, _P]),
+    "tcg_permute_f32": (C.c_int, [_P, _P, _I64, _P, _P]),
     "tcg_csr_transpose_workspace_bytes": (_SZ, [_I64, _I64]),
     "tcg_csr_transpose": (C.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P, _SZ, _P]),
     "tcg_spmm": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P,
@@ -70,6 +71,13 @@ SIGNATURES = {
     "tcg_agnn_backward": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _P, _I64, _I64, _P, _P,
                                     _P, _I64, _I64, _I64, _I64, _P]),
     "tcg_quantize_tf32": (C.c_int, [_P, _P, _I64, _P]),
+    "tcg_dense": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _I32, _P, _I32, _P, _I64, _P, _I64,
+                            _P]),
+    "tcg_gemm_tn_workspace_bytes": (_SZ, [_I64, _I64, _I64]),
+    "tcg_gemm_tn": (C.c_int, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _SZ,
+                              _P]),
+    "tcg_softmax_xent_workspace_bytes": (_SZ, [_I64]),
+    "tcg_softmax_xent": (C.c_int, [_P, _I64, _P, _I64, _I64, _P, _P, _P, _SZ, _P]),
 }
 
 _lib = None

@@ -1,0 +1,317 @@
+// Dense companions of the sparse layers: the tall-skinny fp32 GEMMs of
+// GCNConv / AGNNConv / Linear (N up to millions of rows, feature widths
+// <= a few hundred) and the fused softmax cross-entropy of the models'
+// output layer. cuBLAS picks
+// split-K "largek" kernels for A^T B with K = N (ncu: ~0.5 ms per weight
+// gradient on the arxiv shape); these kernels are HBM-bound instead:
+//
+//  * rows_x_small: Y[n x co] = act((X .* [mask > 0]) . M + b), M given
+//    as [ci x co] or transposed [co x ci]; 64-row CTA tiles, X and M staged
+//    through shared memory in 32-wide k-chunks, 4 x CT outputs per thread.
+//  * gemm_tn: Out[k x c] = A^T B (B optionally masked by mask > 0) and
+//    colsum(B) — per-slab partial tiles, then a fixed-order sum over slabs
+//    (deterministic, no atomics).
+//  * softmax_xent: per row log-softmax, NLL of the label, and
+//    dlogits = (softmax - onehot) / n; the mean loss by a fixed-order
+//    two-level reduction.
+// All fp32 FMA (no TF32) so the GEMMs keep full fp32 accuracy (SURVEY.md
+// fact 8: TF32 GEMMs would push the 4-layer AGNN past the 5e-3 budget).
+#include "common.cuh"
+
+namespace tcg {
+namespace {
+
+constexpr int kRowsTile = 64;
+constexpr int kKChunk = 32;
+
+// CT = output columns per thread (16 column groups x CT = co padded)
+template <int CT, bool TRANS>
+__global__ void __launch_bounds__(256)
+    rows_x_small(const float* __restrict__ x, int64_t ldx, int64_t n, int ci,
+                 const float* __restrict__ m, int co, const float* __restrict__ bias, int relu,
+                 const float* __restrict__ mask, int64_t ldm, float* __restrict__ y, int64_t ldy) {
+  __shared__ float xs[kRowsTile][kKChunk + 1];
+  __shared__ float ms[kKChunk][16 * CT];
+  const int tid = threadIdx.x;
+  const int cg = tid & 15, rg = tid >> 4;  // column group, row group (16 x 16)
+  const int64_t row0 = (int64_t)blockIdx.x * kRowsTile;
+  const int cbase = blockIdx.y * 16 * CT;  // output column tile
+  float acc[4][CT];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < CT; ++c) acc[r][c] = 0.f;
+  for (int k0 = 0; k0 < ci; k0 += kKChunk) {
+    // stage X[row0 .. +64][k0 .. +32]
+    for (int i = tid; i < kRowsTile * kKChunk; i += 256) {
+      const int r = i / kKChunk, k = i % kKChunk;
+      const int64_t gr = row0 + r;
+      float v = (gr < n && k0 + k < ci) ? __ldg(x + gr * ldx + k0 + k) : 0.f;
+      if (mask && gr < n && k0 + k < ci && !(__ldg(mask + gr * ldm + k0 + k) > 0.f)) v = 0.f;
+      xs[r][k] = v;
+    }
+    // stage M[k0 .. +32][0 .. 16*CT)
+    for (int i = tid; i < kKChunk * 16 * CT; i += 256) {
+      const int k = i / (16 * CT), cl = i % (16 * CT), c = cbase + cl;
+      float v = 0.f;
+      if (k0 + k < ci && c < co)
+        v = TRANS ? __ldg(m + (int64_t)c * ci + k0 + k) : __ldg(m + (int64_t)(k0 + k) * co + c);
+      ms[k][cl] = v;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < kKChunk; ++k) {
+      float a[4], b[CT];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = xs[rg + 16 * r][k];
+#pragma unroll
+      for (int c = 0; c < CT; ++c) b[c] = ms[k][cg + 16 * c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < CT; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t gr = row0 + rg + 16 * r;
+    if (gr >= n) continue;
+#pragma unroll
+    for (int c = 0; c < CT; ++c) {
+      const int col = cbase + cg + 16 * c;
+      if (col >= co) continue;
+      float v = acc[r][c];
+      if (bias) v += __ldg(bias + col);
+      if (relu) v = fmaxf(v, 0.f);
+      y[gr * ldy + col] = v;
+    }
+  }
+}
+
+// Partial A^T B over a slab of rows: grid (slabs, k-tiles of 32, c-tiles of 32)
+__global__ void __launch_bounds__(256)
+    gemm_tn_partial(const float* __restrict__ a, int64_t lda, const float* __restrict__ b,
+                    int64_t ldb, const float* __restrict__ mask, int64_t ldm, int64_t n, int k,
+                    int c, int64_t rows_per_slab, float* __restrict__ part,
+                    float* __restrict__ colpart) {
+  __shared__ float as[32][33];
+  __shared__ float bs[32][33];
+  const int tid = threadIdx.x;
+  const int ti = tid >> 3, tj = tid & 7;  // 32 x 8 threads: i = ti, j = tj + 8*q
+  const int k0 = blockIdx.y * 32, c0 = blockIdx.z * 32;
+  const int64_t r_begin = (int64_t)blockIdx.x * rows_per_slab;
+  const int64_t r_end = min(n, r_begin + rows_per_slab);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float cs[4] = {0.f, 0.f, 0.f, 0.f};  // column sums of (masked) B, k-tile 0 only
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += 32) {
+    for (int i = tid; i < 32 * 32; i += 256) {
+      const int rr = i >> 5, cc = i & 31;
+      const int64_t gr = r0 + rr;
+      const bool rok = gr < r_end;
+      as[rr][cc] = (rok && k0 + cc < k) ? __ldg(a + gr * lda + k0 + cc) : 0.f;
+      float bv = (rok && c0 + cc < c) ? __ldg(b + gr * ldb + c0 + cc) : 0.f;
+      if (mask && rok && c0 + cc < c && !(__ldg(mask + gr * ldm + c0 + cc) > 0.f)) bv = 0.f;
+      bs[rr][cc] = bv;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      const float av = as[rr][ti];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float bv = bs[rr][tj + 8 * q];
+        acc[q] = fmaf(av, bv, acc[q]);
+        if (ti == 0) cs[q] += bv;
+      }
+    }
+    __syncthreads();
+  }
+  float* out = part + (int64_t)blockIdx.x * k * c;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = k0 + ti, j = c0 + tj + 8 * q;
+    if (i < k && j < c) out[(int64_t)i * c + j] = acc[q];
+    if (colpart && blockIdx.y == 0 && ti == 0 && j < c) colpart[(int64_t)blockIdx.x * c + j] = cs[q];
+  }
+}
+
+// Fixed-order sum of the slab partials.
+// 32 outputs per CTA x 8 summers: summer j adds slabs j, j+8, ... in order,
+// then the 8 partial sums are combined in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) sum_slabs(const float* __restrict__ part, int slabs,
+                                                 int64_t len, float* __restrict__ out) {
+  __shared__ float sh[8][33];
+  const int o = threadIdx.x & 31, j = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 32 + o;
+  float s = 0.f;
+  if (i < len)
+    for (int q = j; q < slabs; q += 8) s += part[(int64_t)q * len + i];
+  sh[j][o] = s;
+  __syncthreads();
+  if (j == 0 && i < len) {
+    float tot = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tot += sh[q][o];
+    out[i] = tot;
+  }
+}
+
+// One warp per row: log-softmax, NLL, dlogits; per-CTA loss partials.
+__global__ void __launch_bounds__(256)
+    softmax_xent(const float* __restrict__ logits, int64_t ld, const int64_t* __restrict__ labels,
+                 int64_t n, int c, float* __restrict__ dlogits, float* __restrict__ lpart) {
+  __shared__ float wsum[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + warp;
+  float contrib = 0.f;
+  if (row < n) {
+    const float* lr = logits + row * ld;
+    float mx = -INFINITY;
+    for (int j = lane; j < c; j += 32) mx = fmaxf(mx, lr[j]);
+    mx = warp_max(mx);
+    float s = 0.f;
+    for (int j = lane; j < c; j += 32) s += expf(lr[j] - mx);
+    s = warp_sum(s);
+    const float lse = mx + logf(s);
+    const int64_t lab = labels[row];
+    const float inv_n = 1.f / (float)n;
+    for (int j = lane; j < c; j += 32) {
+      const float pj = expf(lr[j] - lse);
+      dlogits[row * c + j] = (pj - (j == lab ? 1.f : 0.f)) * inv_n;
+    }
+    if (lane == 0) contrib = lse - lr[lab];
+  }
+  if (lane == 0) wsum[warp] = contrib;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < 8; ++w) s += wsum[w];
+    lpart[blockIdx.x] = s;
+  }
+}
+
+__global__ void final_loss(const float* __restrict__ lpart, int64_t parts, int64_t n,
+                           float* __restrict__ loss) {
+  __shared__ float sh[256];
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < parts; i += 256) s += lpart[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = sh[0] / (float)n;
+}
+
+template <bool TRANS>
+int launch_rows(const float* x, int64_t ldx, int64_t n, int ci, const float* m, int co,
+                const float* bias, int relu, const float* mask, int64_t ldm, float* y, int64_t ldy,
+                cudaStream_t s) {
+  // output columns in tiles of up to 128 (16 column groups x CT)
+  const int ct = co > 128 ? 8 : (co + 15) / 16;
+  const dim3 grid((unsigned)((n + kRowsTile - 1) / kRowsTile), (unsigned)((co + 16 * ct - 1) / (16 * ct)));
+#define TCG_ROWS(CTV)                                                                    \
+  case CTV:                                                                              \
+    rows_x_small<CTV, TRANS><<<grid, 256, 0, s>>>(x, ldx, n, ci, m, co, bias, relu, mask, \
+                                                  ldm, y, ldy);                          \
+    break;
+  switch (ct) {
+    TCG_ROWS(1)
+    TCG_ROWS(2)
+    TCG_ROWS(3)
+    TCG_ROWS(4)
+    TCG_ROWS(5)
+    TCG_ROWS(6)
+    TCG_ROWS(7)
+    default:
+      TCG_ROWS(8)
+  }
+#undef TCG_ROWS
+  TCG_LAUNCHED("rows_x_small");
+  return TCG_OK;
+}
+
+int64_t slabs_for(int64_t n) {
+  int64_t s = (n + 63) / 64;  // >= 64 rows per slab; ~4 CTAs per SM per output tile
+  const int64_t cap = 4LL * num_sms();
+  return s < 1 ? 1 : (s > cap ? cap : s);
+}
+
+}  // namespace
+}  // namespace tcg
+
+using namespace tcg;
+
+extern "C" int tcg_dense(const float* x, int64_t ldx, int64_t n, int64_t ci, const float* m,
+                         int64_t co, int32_t m_transposed, const float* bias, int32_t relu,
+                         const float* mask, int64_t ldm, float* y, int64_t ldy, void* stream) {
+  TCG_REQUIRE(n >= 0 && ci >= 1 && co >= 1, "tcg_dense: bad shape");
+  TCG_REQUIRE(ldx >= ci && ldy >= co && (mask == nullptr || ldm >= ci), "tcg_dense: bad ld");
+  if (n == 0) return TCG_OK;
+  TCG_REQUIRE(x && m && y, "tcg_dense: null pointer");
+  cudaStream_t s = as_stream(stream);
+  return m_transposed ? launch_rows<true>(x, ldx, n, (int)ci, m, (int)co, bias, relu, mask, ldm, y,
+                                          ldy, s)
+                      : launch_rows<false>(x, ldx, n, (int)ci, m, (int)co, bias, relu, mask, ldm,
+                                           y, ldy, s);
+}
+
+extern "C" size_t tcg_gemm_tn_workspace_bytes(int64_t n, int64_t k, int64_t c) {
+  const int64_t slabs = slabs_for(n);
+  return (size_t)(slabs * k * c + slabs * c) * sizeof(float);
+}
+
+extern "C" int tcg_gemm_tn(const float* a, int64_t lda, const float* b, int64_t ldb,
+                           const float* mask, int64_t ldm, int64_t n, int64_t k, int64_t c,
+                           float* out, float* colsum, void* workspace, size_t workspace_bytes,
+                           void* stream) {
+  TCG_REQUIRE(n >= 0 && k >= 1 && c >= 1, "tcg_gemm_tn: bad shape");
+  TCG_REQUIRE(lda >= k && ldb >= c && (mask == nullptr || ldm >= c), "tcg_gemm_tn: bad ld");
+  TCG_REQUIRE(workspace_bytes >= tcg_gemm_tn_workspace_bytes(n, k, c),
+              "tcg_gemm_tn: workspace too small");
+  TCG_REQUIRE(out && workspace, "tcg_gemm_tn: null pointer");
+  cudaStream_t s = as_stream(stream);
+  const int64_t slabs = slabs_for(n);
+  const int64_t rows = (n + slabs - 1) / slabs;
+  float* part = static_cast<float*>(workspace);
+  float* colpart = part + slabs * k * c;
+  if (n == 0) {
+    TCG_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * k * c, s), "tcg_gemm_tn memset");
+    if (colsum) TCG_CUDA(cudaMemsetAsync(colsum, 0, sizeof(float) * c, s), "tcg_gemm_tn memset");
+    return TCG_OK;
+  }
+  dim3 grid((unsigned)slabs, (unsigned)((k + 31) / 32), (unsigned)((c + 31) / 32));
+  gemm_tn_partial<<<grid, 256, 0, s>>>(a, lda, b, ldb, mask, ldm, n, (int)k, (int)c, rows, part,
+                                       colsum ? colpart : nullptr);
+  TCG_LAUNCHED("gemm_tn_partial");
+  sum_slabs<<<(unsigned)((k * c + 31) / 32), 256, 0, s>>>(part, (int)slabs, k * c, out);
+  TCG_LAUNCHED("sum_slabs");
+  if (colsum) {
+    sum_slabs<<<(unsigned)((c + 31) / 32), 256, 0, s>>>(colpart, (int)slabs, c, colsum);
+    TCG_LAUNCHED("sum_slabs");
+  }
+  return TCG_OK;
+}
+
+extern "C" size_t tcg_softmax_xent_workspace_bytes(int64_t n) {
+  return (size_t)((n + 7) / 8 + 1) * sizeof(float);
+}
+
+extern "C" int tcg_softmax_xent(const float* logits, int64_t ld, const int64_t* labels, int64_t n,
+                                int64_t c, float* loss, float* dlogits, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  TCG_REQUIRE(n >= 1 && c >= 1 && ld >= c, "tcg_softmax_xent: bad shape");
+  TCG_REQUIRE(workspace_bytes >= tcg_softmax_xent_workspace_bytes(n),
+              "tcg_softmax_xent: workspace too small");
+  TCG_REQUIRE(logits && labels && loss && dlogits, "tcg_softmax_xent: null pointer");
+  cudaStream_t s = as_stream(stream);
+  const int64_t parts = (n + 7) / 8;
+  float* lpart = static_cast<float*>(workspace);
+  softmax_xent<<<(unsigned)parts, 256, 0, s>>>(logits, ld, labels, n, (int)c, dlogits, lpart);
+  TCG_LAUNCHED("softmax_xent");
+  final_loss<<<1, 256, 0, s>>>(lpart, parts, n, loss);
+  TCG_LAUNCHED("final_loss");
+  return TCG_OK;
+}

@@ -44,8 +44,7 @@ namespace tcg {
 namespace win {
 
 constexpr int kCons = 4;  // consumer warps per CTA
-constexpr int kProd = 8;  // producer warps per CTA (one stage each)
-constexpr int kThreads = (kCons + kProd) * 32;
+// producer warps per CTA = stages per CTA (one stage each, as many as fit)
 
 __host__ __device__ constexpr int brev3(int x) { return ((x & 1) << 2) | (x & 2) | ((x >> 2) & 1); }
 __device__ __forceinline__ int srow(int c) { return (c & ~7) | brev3(c & 7); }
@@ -116,8 +115,10 @@ struct Layout {
   // ---- stages that fit next to the consumers (<= 8, >= 2) ----
   static constexpr int budget = 220 * 1024;
   static constexpr int fit = (budget - kCons * cons - 256) / stage;
-  static constexpr int kStages = kProd;  // producer w fills stage w
-  static_assert(fit >= kProd, "stages do not fit in shared memory");
+  static constexpr int kStages = fit > 8 ? 8 : fit;  // producer warp w fills stage w
+  static_assert(fit >= 2, "stages do not fit in shared memory");
+  static constexpr int kProd = kStages;
+  static constexpr int kThreads = (kCons + kProd) * 32;
   static constexpr int bars = kStages * stage + kCons * cons;
   static constexpr int total = bars + 2 * kStages * 8;
 };
@@ -151,7 +152,7 @@ __device__ __forceinline__ void load_slice(float (&v)[NT], const float* __restri
 }
 
 template <int NT, int MODE, bool FULL>
-__global__ void __launch_bounds__(kThreads, 1) window_kernel(const Params p) {
+__global__ void __launch_bounds__(Layout<NT, MODE>::kThreads, 1) window_kernel(const Params p) {
   using G = Geo<NT>;
   using L = Layout<NT, MODE>;
   constexpr int CPR = L::CPR;
@@ -167,6 +168,8 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(const Params p) {
   constexpr bool kSpmmPhase = MODE != MODE_SDDMM;
   constexpr int TS = L::tile_stride;
   constexpr int XS2 = CPR * DS;
+  constexpr int kProd = L::kProd;
+  constexpr int kThreads = L::kThreads;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::bars);
   uint64_t* empty = full + S;
@@ -695,6 +698,7 @@ int edge_frag(const int64_t* ptr, const uint32_t* e2c, int64_t n, uint32_t* efra
 template <int NT, int MODE, bool FULL>
 int launch_full(Params& p, cudaStream_t s) {
   using L = Layout<NT, MODE>;
+  constexpr int kThreads = L::kThreads;
   const size_t smem = (size_t)L::total;
   auto kern = window_kernel<NT, MODE, FULL>;
   static int configured_dev = -1;

@@ -14,8 +14,11 @@ enum Mode { MODE_SPMM = 0, MODE_SPMM_DUAL = 1, MODE_SDDMM = 2, MODE_AGNN_FWD = 3
 constexpr int kEdgesPerWindow = 256;
 
 // condensed columns staged per round (rows of X in shared memory)
+// (the fused AGNN kernels need a whole window resident: 192 columns covers
+//  the BASELINE shapes' largest windows — arxiv 153, amazon0601 ~190)
 __host__ __device__ constexpr int cols_per_round(int nt, int mode) {
-  return (nt <= 4 ? 128 : 64) / (mode == MODE_SPMM_DUAL ? 2 : 1);
+  return (mode == MODE_AGNN_FWD || mode == MODE_AGNN_BWD) ? (nt <= 4 ? 192 : 96)
+         : (nt <= 4 ? 128 : 64) / (mode == MODE_SPMM_DUAL ? 2 : 1);
 }
 
 struct Params {

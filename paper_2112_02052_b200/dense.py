@@ -1,0 +1,126 @@
+"""Dense companions of the GNN layers on the B200 (csrc/dense.cu via the C ABI).
+
+The models' tall-skinny fp32 GEMMs (N x F times F x C with F, C <= a few
+hundred) and the softmax cross-entropy loss, as torch.autograd Functions:
+
+  DenseFn       y = act(x W + b);  dx = (g .* [y > 0]) W^T,
+                dW = x^T (g .* [y > 0]), db = colsum(g .* [y > 0])
+  SoftmaxXentFn loss = mean -log_softmax(logits)[label];
+                dlogits = (softmax - onehot) / n  (computed in the forward)
+
+All reductions are fixed-order (deterministic); no TF32.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+import torch.nn as nn
+
+from . import _lib
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def dense(x, w, bias=None, relu=False, mask=None, transposed=False, out=None):
+    """y = act((x .* [mask>0]) M + bias), M = w ([ci x co]) or w^T when
+    `transposed` (w then [co x ci])."""
+    lib = _lib.load()
+    n, ci = x.shape
+    co = w.shape[0] if transposed else w.shape[1]
+    if out is None:
+        out = torch.empty((n, co), dtype=torch.float32, device=x.device)
+    _lib.check(lib.tcg_dense(x.data_ptr(), x.stride(0), n, ci, w.data_ptr(), co, int(transposed),
+                             _p(bias), int(relu), _p(mask), mask.stride(0) if mask is not None else 0,
+                             out.data_ptr(), out.stride(0), _stream()), "tcg_dense")
+    return out
+
+
+def gemm_tn(a, b, mask=None, colsum=False):
+    """(a^T (b .* [mask>0]), colsum(b .* [mask>0]) or None)."""
+    lib = _lib.load()
+    n, k = a.shape
+    c = b.shape[1]
+    out = torch.empty((k, c), dtype=torch.float32, device=a.device)
+    cs = torch.empty(c, dtype=torch.float32, device=a.device) if colsum else None
+    wsb = int(lib.tcg_gemm_tn_workspace_bytes(n, k, c))
+    ws = torch.empty(max(wsb // 4, 1), dtype=torch.float32, device=a.device)
+    _lib.check(lib.tcg_gemm_tn(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), _p(mask),
+                               mask.stride(0) if mask is not None else 0, n, k, c, out.data_ptr(),
+                               _p(cs), ws.data_ptr(), wsb, _stream()), "tcg_gemm_tn")
+    return out, cs
+
+
+def softmax_xent(logits, labels):
+    """(mean NLL of log_softmax, dlogits)."""
+    lib = _lib.load()
+    n, c = logits.shape
+    loss = torch.empty((), dtype=torch.float32, device=logits.device)
+    dl = torch.empty((n, c), dtype=torch.float32, device=logits.device)
+    wsb = int(lib.tcg_softmax_xent_workspace_bytes(n))
+    ws = torch.empty(max(wsb // 4, 1), dtype=torch.float32, device=logits.device)
+    _lib.check(lib.tcg_softmax_xent(logits.data_ptr(), logits.stride(0), labels.data_ptr(), n, c,
+                                    loss.data_ptr(), dl.data_ptr(), ws.data_ptr(), wsb, _stream()),
+               "tcg_softmax_xent")
+    return loss, dl
+
+
+class DenseFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, b, relu: bool):
+        x = x.contiguous()
+        y = dense(x, w.contiguous(), bias=b, relu=relu)
+        ctx.relu = relu
+        ctx.has_b = b is not None
+        ctx.save_for_backward(x, w, y if relu else None)
+        return y
+
+    @staticmethod
+    def backward(ctx, g):
+        x, w, y = ctx.saved_tensors
+        g = g.contiguous()
+        mask = y if ctx.relu else None
+        dx = None
+        if ctx.needs_input_grad[0]:
+            dx = dense(g, w.contiguous(), mask=mask, transposed=True)
+        dw, db = gemm_tn(x, g, mask=mask, colsum=ctx.has_b)
+        return dx, dw, db, None
+
+
+class SoftmaxXentFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, logits, labels):
+        loss, dl = softmax_xent(logits.contiguous(), labels)
+        ctx.save_for_backward(dl)
+        return loss
+
+    @staticmethod
+    def backward(ctx, g):
+        (dl,) = ctx.saved_tensors
+        return dl * g, None
+
+
+class Linear(nn.Module):
+    """fp32 Linear over DenseFn (weight stored [in x out])."""
+
+    def __init__(self, in_dim: int, out_dim: int, bias: bool = True, relu: bool = False,
+                 gen=None):
+        super().__init__()
+        self.weight = nn.Parameter(torch.randn(in_dim, out_dim, generator=gen) / math.sqrt(in_dim))
+        self.bias = nn.Parameter(torch.zeros(out_dim)) if bias else None
+        self.relu = relu
+
+    def forward(self, x):
+        return DenseFn.apply(x, self.weight, self.bias, self.relu)
+
+
+def cross_entropy(logits, labels):
+    return SoftmaxXentFn.apply(logits, labels)

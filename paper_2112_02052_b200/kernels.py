@@ -272,6 +272,18 @@ def sddmm_device(t: TiledGraph, xa, xb=None, *, mode="tf32", epilogue=_lib.EPI_N
     return out
 
 
+def permute_device(src, idx, out=None):
+    """out[k] = src[idx[k]] (tcg_permute_f32)."""
+    import torch
+
+    n = idx.shape[0]
+    if out is None:
+        out = torch.empty(n, dtype=torch.float32, device=src.device)
+    _lib.check(_lib.load().tcg_permute_f32(src.data_ptr(), idx.data_ptr(), out.data_ptr(), n,
+                                           _stream()), "tcg_permute_f32")
+    return out
+
+
 def agnn_forward_device(t: TiledGraph, z, *, p=None, out=None, win_range=None, y_row0=0):
     """Fused TF32 AGNN aggregation (tcg_agnn_forward): returns (Y, P)."""
     import torch

@@ -30,7 +30,14 @@ import torch.nn.functional as F
 
 from . import _lib
 from .dist import ShardPlan, allgather_edges, allgather_rows
-from .kernels import agnn_backward_device, agnn_forward_device, sddmm_device, spmm_device
+from .dense import DenseFn, Linear, cross_entropy  # noqa: F401  (re-exported)
+from .kernels import (
+    agnn_backward_device,
+    agnn_forward_device,
+    permute_device,
+    sddmm_device,
+    spmm_device,
+)
 from .sgt import TiledGraph
 
 
@@ -70,8 +77,13 @@ class GcnAggregate(torch.autograd.Function):
         g = g.contiguous()
         tt = t.transpose()
         out, r0, wr = _rows_out(t, g.shape[1], g, shard)
-        spmm_device(tt.tiled, g, _edge_weights(t), weight_idx=tt.perm if t.num_edges else None,
-                    mode=ctx.mode, out=out, win_range=wr, y_row0=r0)
+        wt = _edge_weights(t)
+        if wt is not None:  # stored edge values in A^T edge order (cached per tiling)
+            key = ("edge_values_T", wt.data_ptr())
+            if key not in t._aux:
+                t._aux[key] = permute_device(wt, tt.perm)
+            wt = t._aux[key]
+        spmm_device(tt.tiled, g, wt, mode=ctx.mode, out=out, win_range=wr, y_row0=r0)
         dh = _finish_rows(out, shard)
         db = g.sum(0) if ctx.has_bias else None
         return dh, db, None, None, None
@@ -126,8 +138,11 @@ class AgnnAggregate(torch.autograd.Function):
         if mode != "tf32":
             spmm_device(t, z, ds, mode=mode, out=out, win_range=wr, y_row0=r0)
         tt = t.transpose()
-        spmm_device(tt.tiled, g, p, weight_idx=tt.perm, x2=z, weights2=ds, weight_idx2=tt.perm,
-                    mode=mode, out=out, accumulate=True, win_range=wr, y_row0=r0)
+        # P and dS into A^T edge order once, then one dual SpMM on A^T
+        pt = permute_device(p, tt.perm)
+        dst = permute_device(ds, tt.perm)
+        spmm_device(tt.tiled, g, pt, x2=z, weights2=dst, mode=mode, out=out, accumulate=True,
+                    win_range=wr, y_row0=r0)
         return _finish_rows(out, shard), None, None, None
 
 
@@ -145,7 +160,8 @@ class GCNConv(nn.Module):
         self.mode = mode
 
     def forward(self, x, t: TiledGraph, shard: ShardPlan | None = None):
-        return GcnAggregate.apply(x @ self.weight, self.bias, t, self.mode, shard)
+        h = DenseFn.apply(x, self.weight, None, False)
+        return GcnAggregate.apply(h, self.bias, t, self.mode, shard)
 
 
 class AGNNConv(nn.Module):
@@ -157,11 +173,12 @@ class AGNNConv(nn.Module):
         self.mode = mode
 
     def forward(self, x, t: TiledGraph, shard: ShardPlan | None = None):
-        return AgnnAggregate.apply(x @ self.weight, t, self.mode, shard)
+        return AgnnAggregate.apply(DenseFn.apply(x, self.weight, None, False), t, self.mode, shard)
 
 
 class GCN(nn.Module):
-    """X -> GCNConv(F,h) -> ReLU -> GCNConv(h,C) -> log_softmax (PAPER.md:684)."""
+    """X -> GCNConv(F,h) -> ReLU -> GCNConv(h,C) -> logits (PAPER.md:684);
+    train with `cross_entropy` (log_softmax + NLL fused)."""
 
     def __init__(self, f_in, hidden, classes, mode="tf32", seed=3):
         super().__init__()
@@ -170,22 +187,22 @@ class GCN(nn.Module):
         self.c2 = GCNConv(hidden, classes, mode, gen)
 
     def forward(self, x, t, shard=None):
-        return F.log_softmax(self.c2(F.relu(self.c1(x, t, shard)), t, shard), dim=1)
+        return self.c2(F.relu(self.c1(x, t, shard)), t, shard)
 
 
 class AGNN(nn.Module):
-    """X -> Linear(F,h) -> ReLU -> L x AGNNConv(h,h) -> Linear(h,C) ->
-    log_softmax (PAPER.md:688-689)."""
+    """X -> Linear(F,h) -> ReLU -> L x AGNNConv(h,h) -> Linear(h,C) -> logits
+    (PAPER.md:688-689); train with `cross_entropy`."""
 
     def __init__(self, f_in, hidden, classes, layers=4, mode="tf32", seed=3):
         super().__init__()
         gen = torch.Generator().manual_seed(seed)
-        self.lin_in = nn.Linear(f_in, hidden)
+        self.lin_in = Linear(f_in, hidden, bias=True, relu=True, gen=gen)
         self.convs = nn.ModuleList([AGNNConv(hidden, hidden, mode, gen) for _ in range(layers)])
-        self.lin_out = nn.Linear(hidden, classes)
+        self.lin_out = Linear(hidden, classes, bias=True, gen=gen)
 
     def forward(self, x, t, shard=None):
-        h = F.relu(self.lin_in(x))
+        h = self.lin_in(x)
         for c in self.convs:
             h = c(h, t, shard)
-        return F.log_softmax(self.lin_out(h), dim=1)
+        return self.lin_out(h)

@@ -1,0 +1,113 @@
+"""Dense companions (csrc/dense.cu) against float64 torch, and the whole AGNN /
+GCN training step against the CPU oracle's restated epoch (same weights)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import TF32_REL_L2, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    import paper_2112_02052_b200 as tcg
+    from paper_2112_02052_b200 import dense, layers
+
+    return tcg, dense, layers, torch
+
+
+@pytest.mark.parametrize("n,ci,co", [(1000, 128, 32), (777, 32, 40), (50, 1433, 16), (3, 7, 3),
+                                     (4096, 32, 128)])
+def test_dense_forward_backward_kernels(env, n, ci, co):
+    _, dense, _, torch = env
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.randn(n, ci, device="cuda", generator=g)
+    w = torch.randn(ci, co, device="cuda", generator=g)
+    b = torch.randn(co, device="cuda", generator=g)
+    ref = (x.double() @ w.double() + b.double()).relu()
+    y = dense.dense(x, w, bias=b, relu=True)
+    assert rel_l2(y.cpu().numpy(), ref.cpu().numpy()) < 1e-6
+    gy = torch.randn(n, co, device="cuda", generator=g)
+    m = (ref > 0).double()
+    dx = dense.dense(gy, w, mask=y, transposed=True)  # mask: y [n x co] on the input gy
+    assert rel_l2(dx.cpu().numpy(), ((gy.double() * m) @ w.double().T).cpu().numpy()) < 1e-6
+    dw, db = dense.gemm_tn(x, gy, mask=y, colsum=True)
+    assert rel_l2(dw.cpu().numpy(), (x.double().T @ (gy.double() * m)).cpu().numpy()) < 1e-6
+    assert rel_l2(db.cpu().numpy(), (gy.double() * m).sum(0).cpu().numpy()) < 1e-6
+    # deterministic
+    dw2, _ = dense.gemm_tn(x, gy, mask=y, colsum=True)
+    assert torch.equal(dw, dw2)
+
+
+def test_softmax_xent(env):
+    _, dense, _, torch = env
+    logits = torch.randn(5000, 40, device="cuda") * 3
+    labels = torch.randint(0, 40, (5000,), device="cuda")
+    loss, dl = dense.softmax_xent(logits, labels)
+    lg = logits.double().requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(lg, labels)
+    ref.backward()
+    assert abs(float(loss) - float(ref)) < 1e-5 * max(1.0, abs(float(ref)))
+    assert rel_l2(dl.cpu().numpy(), lg.grad.cpu().numpy()) < 1e-5
+
+
+def _copy_weights_agnn(net, cpu):
+    cpu.w_in[...] = net.lin_in.weight.detach().cpu().numpy()
+    cpu.b_in[...] = net.lin_in.bias.detach().cpu().numpy()
+    for wc, conv in zip(cpu.ws, net.convs):
+        wc[...] = conv.weight.detach().cpu().numpy()
+    cpu.w_out[...] = net.lin_out.weight.detach().cpu().numpy()
+    cpu.b_out[...] = net.lin_out.bias.detach().cpu().numpy()
+
+
+def test_agnn_train_step_vs_oracle(env, oracle):
+    tcg, _, layers, torch = env
+    n, f, h, c = 3000, 64, 32, 10
+    g = tcg.synth.gen_uniform(n, 6, 5)
+    t = tcg.translate(g, tcg.BlockConfig())
+    x = tcg.synth.random_embeddings(n, f, 2)
+    lab = np.random.default_rng(4).integers(0, c, n)
+    net = layers.AGNN(f, h, c, layers=2).cuda()
+    cpu = oracle.AgnnModelCPU(f, h, c, layers=2)
+    _copy_weights_agnn(net, cpu)
+    params0 = [p.copy() for p in cpu.params]
+    loss = layers.cross_entropy(net(torch.from_numpy(x).cuda(), t),
+                                torch.from_numpy(lab).cuda())
+    loss.backward()
+    cpu_loss = cpu.epoch(g.node_pointer, g.edge_list, x, lab, mode="tf32")
+    assert abs(float(loss) - cpu_loss) <= TF32_REL_L2 * abs(cpu_loss)
+    # the CPU epoch took one Adam step: recover its gradients from m = (1-b1) g
+    grads_cpu = [m / (1 - cpu.opt.b1) for m in cpu.opt.m]
+    grads_gpu = [net.lin_in.weight.grad, net.lin_in.bias.grad,
+                 *[cv.weight.grad for cv in net.convs], net.lin_out.weight.grad,
+                 net.lin_out.bias.grad]
+    for gg, gc in zip(grads_gpu, grads_cpu):
+        assert rel_l2(gg.cpu().numpy(), gc) <= 2 * TF32_REL_L2
+    # the Adam step moved every parameter
+    assert all(not np.array_equal(a, b) for a, b in zip(params0, cpu.params))
+
+
+def test_gcn_train_step_vs_oracle(env, oracle):
+    tcg, _, layers, torch = env
+    n, f, h, c = 2000, 100, 16, 7
+    g = tcg.synth.gen_uniform(n, 5, 8)
+    t = tcg.translate(g, tcg.BlockConfig())
+    x = tcg.synth.random_embeddings(n, f, 2)
+    lab = np.random.default_rng(4).integers(0, c, n)
+    net = layers.GCN(f, h, c).cuda()
+    cpu = oracle.GcnModelCPU(f, h, c)
+    cpu.w1[...] = net.c1.weight.detach().cpu().numpy()
+    cpu.w2[...] = net.c2.weight.detach().cpu().numpy()
+    loss = layers.cross_entropy(net(torch.from_numpy(x).cuda(), t), torch.from_numpy(lab).cuda())
+    loss.backward()
+    cpu_loss = cpu.epoch(g.node_pointer, g.edge_list, x, lab, mode="tf32")
+    assert abs(float(loss) - cpu_loss) <= TF32_REL_L2 * abs(cpu_loss)
+    grads_cpu = [m / (1 - cpu.opt.b1) for m in cpu.opt.m]
+    grads_gpu = [net.c1.weight.grad, net.c1.bias.grad, net.c2.weight.grad, net.c2.bias.grad]
+    for gg, gc in zip(grads_gpu, grads_cpu):
+        assert rel_l2(gg.cpu().numpy(), gc) <= 2 * TF32_REL_L2

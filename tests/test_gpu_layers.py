@@ -94,7 +94,7 @@ def test_models_train_and_graph_capture(env):
         losses = []
         for _ in range(20):
             opt.zero_grad(set_to_none=False)
-            loss = torch.nn.functional.nll_loss(m(x, t), labels)
+            loss = layers.cross_entropy(m(x, t), labels)
             loss.backward()
             opt.step()
             losses.append(float(loss))
@@ -105,7 +105,7 @@ def test_models_train_and_graph_capture(env):
 
         def step(mod):
             mod.zero_grad(set_to_none=False)
-            out = torch.nn.functional.nll_loss(mod(x, t), labels)
+            out = layers.cross_entropy(mod(x, t), labels)
             out.backward()
             return out
 
