@@ -1,9 +1,10 @@
 // The row-window engine: every TF32 tensor-core op of the hot path.
 //
-// Warp-specialised, persistent: per CTA kProd PRODUCER warps and kCons
-// CONSUMER warps share a ring of kStages shared-memory stages; one stage
-// holds one 16-row window (reference tile dataflow: tiles.py:130-250,
-// kernels.py:254-538, Alg. 2/3):
+// Warp-specialised, persistent: per CTA kStages (producer warp, consumer
+// warp) pairs, pair s owning shared-memory stage s; one stage holds one
+// 16-row window (reference tile dataflow: tiles.py:130-250,
+// kernels.py:254-538, Alg. 2/3); task i of the CTA goes to pair
+// i % kStages:
 //
 //   producer (FetchDense): for window w, its condensed neighbour rows
 //     X[col_to_node[c]] (8 lanes per 128-B row, cp.async 16 B, so each warp
@@ -43,7 +44,6 @@
 namespace tcg {
 namespace win {
 
-constexpr int kCons = 4;  // consumer warps per CTA
 // producer warps per CTA = stages per CTA (one stage each, as many as fit)
 
 __host__ __device__ constexpr int brev3(int x) { return ((x & 1) << 2) | (x & 2) | ((x >> 2) & 1); }
@@ -112,12 +112,15 @@ struct Layout {
   static constexpr int c_frag = c_frag_a > c_frag_t ? c_frag_a : c_frag_t;
   static constexpr int c_esc = c_frag;
   static constexpr int cons = (c_esc + (kFused ? EPR * 4 : 0) + 127) & ~127;
-  // ---- stages that fit next to the consumers (<= 8, >= 2) ----
+  // ---- pipeline pairs: stage s is filled only by producer warp s and drained
+  // only by consumer warp kStages + s (so mbarrier phases never alias across
+  // warps); as many pairs as fit (<= 8, >= 2) ----
   static constexpr int budget = 220 * 1024;
-  static constexpr int fit = (budget - kCons * cons - 256) / stage;
-  static constexpr int kStages = fit > 8 ? 8 : fit;  // producer warp w fills stage w
+  static constexpr int fit = (budget - 256) / (stage + cons);
+  static constexpr int kStages = fit > 8 ? 8 : fit;
   static_assert(fit >= 2, "stages do not fit in shared memory");
   static constexpr int kProd = kStages;
+  static constexpr int kCons = kStages;
   static constexpr int kThreads = (kCons + kProd) * 32;
   static constexpr int bars = kStages * stage + kCons * cons;
   static constexpr int total = bars + 2 * kStages * 8;
@@ -169,6 +172,7 @@ __global__ void __launch_bounds__(Layout<NT, MODE>::kThreads, 1) window_kernel(c
   constexpr int TS = L::tile_stride;
   constexpr int XS2 = CPR * DS;
   constexpr int kProd = L::kProd;
+  constexpr int kCons = L::kCons;
   constexpr int kThreads = L::kThreads;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::bars);
@@ -715,7 +719,7 @@ int launch_full(Params& p, cudaStream_t s) {
   }
   p.use_tma = 0;
   const int64_t tasks = p.nwin * p.nchunks;
-  int64_t blocks = (tasks + kCons - 1) / kCons;
+  int64_t blocks = (tasks + L::kCons - 1) / L::kCons;
   const int64_t cap = (int64_t)num_sms() * per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) return TCG_OK;
