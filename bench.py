@@ -339,6 +339,7 @@ def run_ours(args):
     step_ms = []
     for _ in range(args.steps):
         flush()
+        torch.cuda._sleep(100000)  # GPU busy while the host launches the graph
         s, e = ev(), ev()
         s.record()
         step()
@@ -395,6 +396,9 @@ def run_ours(args):
             ts = []
             for _ in range(reps):
                 flush()
+                # keep the GPU busy while the host enqueues, so the events
+                # bracket device time only (no host launch gap)
+                torch.cuda._sleep(200000)
                 s, e = ev(), ev()
                 s.record()
                 fn()
@@ -404,11 +408,18 @@ def run_ours(args):
             return statistics.median(ts)
 
         def warm_ms(fn, reps=50):
+            # back-to-back launches replayed from a CUDA graph (L2-warm, no host gaps)
             fn()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(reps):
+                    fn()
+            g.replay()
+            torch.cuda._sleep(200000)
             s, e = ev(), ev()
             s.record()
-            for _ in range(reps):
-                fn()
+            g.replay()
             e.record()
             e.synchronize()
             return s.elapsed_time(e) / reps

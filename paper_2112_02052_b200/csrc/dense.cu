@@ -17,6 +17,7 @@
 // All fp32 FMA (no TF32) so the GEMMs keep full fp32 accuracy (SURVEY.md
 // fact 8: TF32 GEMMs would push the 4-layer AGNN past the 5e-3 budget).
 #include "common.cuh"
+#include "dense_rows.cuh"
 
 namespace tcg {
 namespace {
@@ -233,6 +234,133 @@ int launch_rows(const float* x, int64_t ldx, int64_t n, int ci, const float* m, 
   return TCG_OK;
 }
 
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <typename K>
+int set_smem(K kern, size_t bytes, int threads, int* per_sm) {
+  TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
+           "dense attr");
+  TCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, threads, bytes),
+           "dense occupancy");
+  if (*per_sm < 1) *per_sm = 1;
+  return TCG_OK;
+}
+
+template <int CI, int CO, bool TRANS, bool MASK>
+int run_dense_tile(const float* x, int64_t ldx, int64_t n, const float* m, int co,
+                   const float* bias, int relu, const float* mask, int64_t ldm, float* y,
+                   int64_t ldy, cudaStream_t s) {
+  using Cfg = dr::DenseCfg<CI, CO, MASK>;
+  static int dev_done = -1, per_sm = 1;
+  int dev = 0;
+  TCG_CUDA(cudaGetDevice(&dev), "dense device");
+  if (dev_done != dev) {
+    const int rc = set_smem(dr::dense_tile<CI, CO, TRANS, MASK>, Cfg::SMEM, Cfg::NT, &per_sm);
+    if (rc != TCG_OK) return rc;
+    dev_done = dev;
+  }
+  int64_t blocks = (n + Cfg::ROWS - 1) / Cfg::ROWS;
+  const int64_t cap = (int64_t)num_sms() * per_sm;
+  if (blocks > cap) blocks = cap;
+  const int vec_out = (ldy % 4 == 0) && al16(y);
+  dr::dense_tile<CI, CO, TRANS, MASK><<<(unsigned)blocks, Cfg::NT, Cfg::SMEM, s>>>(
+      x, ldx, n, m, co, bias, relu, mask, ldm, y, ldy, vec_out);
+  TCG_LAUNCHED("dense_tile");
+  return TCG_OK;
+}
+
+template <int CI, bool TRANS>
+int dense_co(const float* x, int64_t ldx, int64_t n, const float* m, int co, const float* bias,
+             int relu, const float* mask, int64_t ldm, float* y, int64_t ldy, cudaStream_t s) {
+#define TCG_DC(COV)                                                                          \
+  if (co <= COV)                                                                             \
+    return mask ? run_dense_tile<CI, COV, TRANS, true>(x, ldx, n, m, co, bias, relu, mask,   \
+                                                       ldm, y, ldy, s)                       \
+                : run_dense_tile<CI, COV, TRANS, false>(x, ldx, n, m, co, bias, relu, mask,  \
+                                                        ldm, y, ldy, s);
+  TCG_DC(8)
+  TCG_DC(16)
+  TCG_DC(32)
+  TCG_DC(40)
+  TCG_DC(64)
+#undef TCG_DC
+  return 1;
+}
+
+// Pipelined row-tile path for the models' shapes; returns 1 when not applicable.
+int fast_dense(const float* x, int64_t ldx, int64_t n, int ci, const float* m, int co, bool trans,
+               const float* bias, int relu, const float* mask, int64_t ldm, float* y, int64_t ldy,
+               cudaStream_t s) {
+  if (co > 64 || ldx % 4 || !al16(x) || (mask && (ldm % 4 || !al16(mask)))) return 1;
+#define TCG_FD(CIV)                                                                            \
+  if (ci == CIV)                                                                               \
+    return trans ? dense_co<CIV, true>(x, ldx, n, m, co, bias, relu, mask, ldm, y, ldy, s)     \
+                 : dense_co<CIV, false>(x, ldx, n, m, co, bias, relu, mask, ldm, y, ldy, s);
+  TCG_FD(16)
+  TCG_FD(32)
+  TCG_FD(40)
+  TCG_FD(64)
+  TCG_FD(128)
+#undef TCG_FD
+  return 1;
+}
+
+template <int CI, int CO, bool MASK>
+int run_gemm_tn_tile(const float* a, int64_t lda, const float* b, int64_t ldb, const float* mask,
+                     int64_t ldm, int64_t n, int co, float* part, float* colpart, int64_t cap_slabs,
+                     int64_t* used, cudaStream_t s) {
+  using Cfg = dr::GemmCfg<CI, CO, MASK>;
+  static int dev_done = -1, per_sm = 1;
+  int dev = 0;
+  TCG_CUDA(cudaGetDevice(&dev), "dense device");
+  if (dev_done != dev) {
+    const int rc = set_smem(dr::gemm_tn_tile<CI, CO, MASK>, Cfg::SMEM, Cfg::NT, &per_sm);
+    if (rc != TCG_OK) return rc;
+    dev_done = dev;
+  }
+  int64_t blocks = (n + Cfg::ROWS - 1) / Cfg::ROWS;
+  int64_t cap = (int64_t)num_sms() * per_sm;
+  if (cap > cap_slabs) cap = cap_slabs;
+  if (blocks > cap) blocks = cap;
+  dr::gemm_tn_tile<CI, CO, MASK><<<(unsigned)blocks, Cfg::NT, Cfg::SMEM, s>>>(
+      a, lda, b, ldb, mask, ldm, n, co, part, colpart);
+  TCG_LAUNCHED("gemm_tn_tile");
+  *used = blocks;
+  return TCG_OK;
+}
+
+template <int CI>
+int gemm_tn_co(const float* a, int64_t lda, const float* b, int64_t ldb, const float* mask,
+               int64_t ldm, int64_t n, int co, float* part, float* colpart, int64_t cap_slabs,
+               int64_t* used, cudaStream_t s) {
+#define TCG_GC(COV)                                                                            \
+  if (co <= COV)                                                                               \
+    return mask ? run_gemm_tn_tile<CI, COV, true>(a, lda, b, ldb, mask, ldm, n, co, part,      \
+                                                  colpart, cap_slabs, used, s)                 \
+                : run_gemm_tn_tile<CI, COV, false>(a, lda, b, ldb, mask, ldm, n, co, part,     \
+                                                   colpart, cap_slabs, used, s);
+  TCG_GC(8)
+  TCG_GC(16)
+  TCG_GC(32)
+  TCG_GC(40)
+  TCG_GC(64)
+#undef TCG_GC
+  return 1;
+}
+
+int fast_gemm_tn(const float* a, int64_t lda, const float* b, int64_t ldb, const float* mask,
+                 int64_t ldm, int64_t n, int k, int c, float* part, float* colpart,
+                 int64_t cap_slabs, int64_t* used, cudaStream_t s) {
+  if (c > 64 || lda % 4 || ldb % 4 || !al16(a) || !al16(b) || (mask && (ldm % 4 || !al16(mask))))
+    return 1;
+  if (k == 16) return gemm_tn_co<16>(a, lda, b, ldb, mask, ldm, n, c, part, colpart, cap_slabs, used, s);
+  if (k == 32) return gemm_tn_co<32>(a, lda, b, ldb, mask, ldm, n, c, part, colpart, cap_slabs, used, s);
+  if (k == 40) return gemm_tn_co<40>(a, lda, b, ldb, mask, ldm, n, c, part, colpart, cap_slabs, used, s);
+  if (k == 64) return gemm_tn_co<64>(a, lda, b, ldb, mask, ldm, n, c, part, colpart, cap_slabs, used, s);
+  if (k == 128) return gemm_tn_co<128>(a, lda, b, ldb, mask, ldm, n, c, part, colpart, cap_slabs, used, s);
+  return 1;
+}
+
 int64_t slabs_for(int64_t n) {
   int64_t s = (n + 63) / 64;  // >= 64 rows per slab; ~4 CTAs per SM per output tile
   const int64_t cap = 4LL * num_sms();
@@ -252,6 +380,11 @@ extern "C" int tcg_dense(const float* x, int64_t ldx, int64_t n, int64_t ci, con
   if (n == 0) return TCG_OK;
   TCG_REQUIRE(x && m && y, "tcg_dense: null pointer");
   cudaStream_t s = as_stream(stream);
+  {
+    const int rc = fast_dense(x, ldx, n, (int)ci, m, (int)co, m_transposed != 0, bias, relu, mask,
+                              ldm, y, ldy, s);
+    if (rc != 1) return rc;  // 1: shape not covered by the warp-tile kernels
+  }
   return m_transposed ? launch_rows<true>(x, ldx, n, (int)ci, m, (int)co, bias, relu, mask, ldm, y,
                                           ldy, s)
                       : launch_rows<false>(x, ldx, n, (int)ci, m, (int)co, bias, relu, mask, ldm,
@@ -281,6 +414,21 @@ extern "C" int tcg_gemm_tn(const float* a, int64_t lda, const float* b, int64_t 
     TCG_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * k * c, s), "tcg_gemm_tn memset");
     if (colsum) TCG_CUDA(cudaMemsetAsync(colsum, 0, sizeof(float) * c, s), "tcg_gemm_tn memset");
     return TCG_OK;
+  }
+  {
+    int64_t used = 0;
+    const int rc = fast_gemm_tn(a, lda, b, ldb, mask, ldm, n, (int)k, (int)c, part,
+                                colsum ? colpart : nullptr, slabs, &used, s);
+    if (rc == TCG_OK) {
+      sum_slabs<<<(unsigned)((k * c + 31) / 32), 256, 0, s>>>(part, (int)used, k * c, out);
+      TCG_LAUNCHED("sum_slabs");
+      if (colsum) {
+        sum_slabs<<<(unsigned)((c + 31) / 32), 256, 0, s>>>(colpart, (int)used, c, colsum);
+        TCG_LAUNCHED("sum_slabs");
+      }
+      return TCG_OK;
+    }
+    if (rc != 1) return rc;
   }
   dim3 grid((unsigned)slabs, (unsigned)((k + 31) / 32), (unsigned)((c + 31) / 32));
   gemm_tn_partial<<<grid, 256, 0, s>>>(a, lda, b, ldb, mask, ldm, n, (int)k, (int)c, rows, part,
