@@ -18,7 +18,12 @@ import torch  # noqa: E402
 
 import paper_2112_02052_b200 as tcg  # noqa: E402
 from paper_2112_02052_b200 import _lib  # noqa: E402
-from paper_2112_02052_b200.kernels import sddmm_device, spmm_device  # noqa: E402
+from paper_2112_02052_b200.kernels import (  # noqa: E402
+    agnn_backward_device,
+    agnn_forward_device,
+    sddmm_device,
+    spmm_device,
+)
 
 
 def main():
@@ -39,6 +44,8 @@ def main():
         spmm_device(tt.tiled, gy, p, weight_idx=tt.perm, x2=z, weights2=ds, weight_idx2=tt.perm,
                     out=out, accumulate=True)
         spmm_device(t, z, p, mode="f32", out=out)
+        agnn_forward_device(t, z, p=p, out=out)
+        agnn_backward_device(t, z, gy, p, ds=ds, out=out)
     torch.cuda.synchronize()
 
 
