@@ -56,7 +56,17 @@ typedef struct tcg_tiling {
                                    its 16x8 A tile (tcg_edge_frag; TF32 only) */
   int64_t max_window_edges;     /* max edges of one window (0 = unknown)       */
   int64_t max_window_unique;    /* max condensed columns of one window         */
+  /* Block stream (tcg_block_stream; optional, TF32 16x8 only; null => the
+   * window engine runs): */
+  const int32_t* block_offsets; /* i32[W+1] exclusive cumsum of win_partition:
+                                   the per-window TC-block offsets            */
+  const uint32_t* col_stream;   /* u32[8*(TB+TCG_STREAM_PAD)], TB = block_offsets[W]:
+                                   col_to_node padded per window to whole
+                                   8-column blocks, pair-interleaved          */
 } tcg_tiling;
+
+/* Blocks of padding tcg_block_stream appends after the column stream. */
+#define TCG_STREAM_PAD 16
 
 /* ---- library ---------------------------------------------------------- */
 const char* tcg_last_error(void);
@@ -86,6 +96,14 @@ int tcg_sgt(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_node
  * (kernels.py:173-188: r_local, b_of_edge, c_local). */
 int tcg_edge_frag(const tcg_tiling* t, uint32_t* edge_frag, void* stream);
 
+/* Per-window TC-block offsets (block_offsets[w] = sum of win_partition[0..w),
+ * W+1 entries; the "counts and offsets" the reference derives as
+ * tile_base, kernels.py:461-462) and the block-padded column stream the SpMM
+ * block-stream engine reads (col_stream may be null: offsets only, so the
+ * caller can read TB = block_offsets[W] and size col_stream as
+ * 8*(TB+TCG_STREAM_PAD) u32). Derived once per tiling. */
+int tcg_block_stream(const tcg_tiling* t, int32_t* block_offsets, uint32_t* col_stream,
+                     void* stream);
 /* dst[k] = src[idx[k]] — carries A's edge weights (P, dS, edge values) into
  * A^T edge order once per backward, so the A^T SpMM reads them coalesced. */
 int tcg_permute_f32(const float* src, const uint32_t* idx, float* dst, int64_t n, void* stream);

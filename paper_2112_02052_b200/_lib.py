@@ -19,6 +19,7 @@ PREC_TF32 = 1
 EPI_NONE = 0
 EPI_SOFTMAX = 1
 EPI_SOFTMAX_BWD = 2
+STREAM_PAD = 16  # TCG_STREAM_PAD
 
 
 class TcgTiling(C.Structure):
@@ -40,6 +41,8 @@ class TcgTiling(C.Structure):
         ("edge_frag", C.c_void_p),
         ("max_window_edges", C.c_int64),
         ("max_window_unique", C.c_int64),
+        ("block_offsets", C.c_void_p),
+        ("col_stream", C.c_void_p),
     ]
 
 
@@ -57,6 +60,7 @@ SIGNATURES = {
     "tcg_sgt_workspace_bytes": (_SZ, [_I64, _I64, _I32]),
     "tcg_sgt": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
     "tcg_edge_frag": (C.c_int, [C.POINTER(TcgTiling), _P, _P]),
+    "tcg_block_stream": (C.c_int, [C.POINTER(TcgTiling), _P, _P, _P]),
     "tcg_permute_f32": (C.c_int, [_P, _P, _I64, _P, _P]),
     "tcg_csr_transpose_workspace_bytes": (_SZ, [_I64, _I64]),
     "tcg_csr_transpose": (C.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P, _SZ, _P]),

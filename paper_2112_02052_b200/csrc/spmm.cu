@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Neighbour aggregation Y = (F .* A) X over the SGT tiling — replaces the
 // reference kernels.spmm (/root/reference/pkg/src/tcgraph/kernels.py:213-374,
 // Alg. 2 of the paper).
@@ -207,5 +208,10 @@ extern "C" int tcg_spmm(const tcg_tiling* t, const float* x, int64_t ldx, int64_
   q.x = x, q.ldx = ldx, q.x2 = x2, q.ldx2 = ldx2;
   q.w = weights, q.widx = weight_idx, q.w2 = weights2, q.widx2 = weight_idx2;
   q.bias = bias, q.y = y, q.ldy = ldy, q.y_row0 = y_row0, q.accumulate = accumulate;
+  static const bool no_stream = std::getenv("TCG_NO_STREAM") != nullptr;
+  if (!no_stream) {
+    const int rc = stream_spmm(t, q, s);
+    if (rc != TCG_E_UNSUPPORTED) return rc;
+  }
   return win::launch(x2 ? win::MODE_SPMM_DUAL : win::MODE_SPMM, nt, q, s);
 }

@@ -1,0 +1,502 @@
+// Block-stream SpMM engine: the TF32 tensor-core SpMM of the hot path
+// (reference kernels.spmm, kernels.py:213-374; paper Alg. 2) for 16x8 tilings.
+//
+// Why a second engine: on B200 the aggregation is bound by the per-SM L1
+// data pipe that every gathered 32-B sector crosses (ncu:
+// l1tex__data_pipe_lsu_wavefronts ~85% busy; a bare 128-B row gather tops
+// out near 9 TB/s), and by per-warp issue latency, not by HBM. This engine
+// is shaped for that:
+//
+//  * Flat block stream. The SGT's condensed columns, padded per window to
+//    whole 8-column TC blocks (win_partition[w] blocks), form one stream of
+//    TB = sum(win_partition) blocks (`col_stream`, built once per tiling by
+//    tcg_block_stream; within a block the columns are stored pair-interleaved
+//    (c, c+4) so each mma lane reads its two B rows with one 8-B load; padding
+//    repeats the window's first node, which the zero A entries cancel).
+//  * One warp owns a contiguous slice of the stream, balanced by blocks
+//    (block_offsets = exclusive cumsum of win_partition, the per-window
+//    TC-block offsets; the slice bounds are found with a 32-ary warp search).
+//  * Per warp, a private shared-memory ring of NB blocks: block s + NB's
+//    neighbour rows are requested with cp.async as block s is consumed, and
+//    block s + 2NB's column ids one step earlier (lanes 0-1), so two levels
+//    of dependent loads stay in flight without cross-warp synchronisation.
+//  * InitSparse per window: the window's edges (prefetched one window ahead
+//    into registers) are scattered into the A fragments (per-edge fragment
+//    slot `edge_frag`, the analogue of the reference's _spmm_aux cache,
+//    kernels.py:173-188) and un-scattered after the window, so the fragment
+//    area is never bulk-cleared.
+//  * mma.sync.m16n8k8 TF32 (cvt.rn.tf32 operands = reference quantize_tf32,
+//    fp32 accumulate); features are permuted so each lane's B slice and C
+//    slice are contiguous (one vector load / store).
+//
+// Modes: Y = A_w X (+bias) (+= Y), and the dual form Y = A_w1 X1 + A_w2 X2
+// used by the A^T pass of the AGNN backward. Feature chunks of 8*NT (NT = 1,
+// 2, 4) run as gridDim.y slices.
+#include "common.cuh"
+#include "window.cuh"
+
+namespace tcg {
+namespace stream {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async(uint32_t s, const void* g) {
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(g), "n"(BYTES)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int NT>
+__device__ __forceinline__ void lds_slice(float (&v)[NT], uint32_t a) {
+  if constexpr (NT == 4) {
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+                 : "r"(a)
+                 : "memory");
+  } else if constexpr (NT == 2) {
+    asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];\n" : "=f"(v[0]), "=f"(v[1]) : "r"(a) : "memory");
+  } else {
+    asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v[0]) : "r"(a) : "memory");
+  }
+}
+__device__ __forceinline__ uint4 lds_frag(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+
+// Byte offset of (staged row r, lane slice g) inside one ring slot: rows of
+// 32*NT bytes, slices of 4*NT bytes, XOR-swizzled so the SpMM fragment reads
+// (rows t / t+4, slices g) are bank-conflict free.
+template <int NT>
+__device__ __forceinline__ uint32_t slot_off(int r, int g) {
+  if constexpr (NT == 4) return r * 128 + ((g ^ (2 * r)) & 7) * 16;
+  else if constexpr (NT == 2) return r * 64 + (g ^ (4 * ((r >> 1) & 1))) * 8;
+  else return r * 32 + g * 4;
+}
+
+struct Args {
+  const int64_t* ptr;
+  const uint32_t* efrag;
+  const int32_t* boff;   // block offsets [W+1]
+  const uint32_t* cs;    // column stream, pair-interleaved, padded past the end
+  int64_t n;
+  int win_begin, win_end;
+  int nwarps;            // warps per feature chunk
+  int d0, ldx, ldx2;     // first feature of chunk 0 (chunk y adds y * 8 * NT)
+  const float* x;
+  const float* x2;
+  const float* w;
+  const uint32_t* widx;
+  const float* w2;
+  const uint32_t* widx2;
+  const float* bias;
+  float* y;
+  int64_t ldy, y_row0;
+  int accumulate;
+};
+
+constexpr int kMaxB = 16;  // A-fragment blocks resident per warp (8 KB per operand)
+constexpr int kEPL = 5;    // edges per lane prefetched for the next window (160)
+
+template <int NT, bool DUAL>
+struct Cfg {
+  static constexpr int NB = 4;                     // ring depth (blocks)
+  static constexpr int NI = 2 * NB;                // column-id ring
+  static constexpr int SLOT = 8 * 32 * NT;         // bytes of one operand's block
+  static constexpr int OPS = DUAL ? 2 : 1;
+  static constexpr int RING = NB * SLOT * OPS;
+  static constexpr int IDX = NI * 32;
+  static constexpr int AFR = kMaxB * 512 * OPS;
+  static constexpr int WARP = RING + IDX + AFR;
+  static constexpr int WPC = 8;                    // warps per CTA
+  static constexpr int SMEM = WPC * WARP;
+};
+
+// first p in [lo, hi) with a[p] >= v (hi if none); whole warp, 32-ary
+__device__ __forceinline__ int warp_lower_bound(const int32_t* __restrict__ a, int lo, int hi,
+                                                int v) {
+  const int lane = threadIdx.x & 31;
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) >> 5;
+    const int p = lo + lane * step;
+    const bool pr = p < hi && __ldg(a + p) < v;
+    const int c = __popc(__ballot_sync(0xffffffffu, pr));
+    if (c == 0) return lo;
+    const int nlo = lo + (c - 1) * step + 1;
+    hi = min(hi, lo + c * step);
+    lo = nlo;
+  }
+  const int p = lo + lane;
+  const bool pr = p < hi && __ldg(a + p) < v;
+  return lo + __popc(__ballot_sync(0xffffffffu, pr));
+}
+
+template <int NT, bool DUAL>
+__global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32, 1) spmm_stream(const Args a) {
+  using C = Cfg<NT, DUAL>;
+  constexpr int NB = C::NB, NI = C::NI, SLOT = C::SLOT;
+  constexpr int CP = 4 * NT;  // bytes per lane per staged row
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gw = blockIdx.x * C::WPC + wid;
+  const int g = lane >> 2, t = lane & 3;
+  unsigned char* wsm = smem + wid * C::WARP;
+  const uint32_t ring = smem_u32(wsm);
+  const uint32_t iring = ring + C::RING;
+  const unsigned char* iring_p = wsm + C::RING;
+  uint32_t* afr = reinterpret_cast<uint32_t*>(wsm + C::RING + C::IDX);
+  uint32_t* afr2 = afr + kMaxB * 128;
+
+  // ---- this warp's slice of the block stream ----
+  const int B0 = __ldg(a.boff + a.win_begin), B1 = __ldg(a.boff + a.win_end);
+  const int64_t TBr = B1 - B0;
+  const int lo_b = B0 + (int)(TBr * gw / a.nwarps);
+  const int hi_b = B0 + (int)(TBr * (gw + 1) / a.nwarps);
+  const int ws = warp_lower_bound(a.boff, a.win_begin, a.win_end, lo_b);
+  const int we = gw + 1 == a.nwarps ? a.win_end : warp_lower_bound(a.boff, ws, a.win_end, hi_b);
+  if (ws >= we) return;
+  const int gb0 = __ldg(a.boff + ws);
+
+  const int d0 = a.d0 + blockIdx.y * 8 * NT;
+  const char* xb = reinterpret_cast<const char*>(a.x + d0 + g * NT);
+  const char* xb2 = DUAL ? reinterpret_cast<const char*>(a.x2 + d0 + g * NT) : nullptr;
+  const uint64_t xrow = (uint64_t)a.ldx * 4, xrow2 = (uint64_t)a.ldx2 * 4;
+  const uint32_t so0 = slot_off<NT>(t, g), so1 = slot_off<NT>(t + 4, g);
+  const uint32_t* csw = a.cs + 8 * (int64_t)gb0;
+
+  auto issue_idx = [&](int s) {
+    if (lane < 2) cp_async<16>(iring + (s & (NI - 1)) * 32 + lane * 16, csw + 8 * (int64_t)s + 4 * lane);
+  };
+  auto issue_x = [&](int s) {
+    const uint2 id = *reinterpret_cast<const uint2*>(iring_p + (s & (NI - 1)) * 32 + 8 * t);
+    const uint32_t sb = ring + (s & (NB - 1)) * SLOT * C::OPS;
+    cp_async<CP>(sb + so0, xb + id.x * xrow);
+    cp_async<CP>(sb + so1, xb + id.y * xrow);
+    if constexpr (DUAL) {
+      cp_async<CP>(sb + SLOT + so0, xb2 + id.x * xrow2);
+      cp_async<CP>(sb + SLOT + so1, xb2 + id.y * xrow2);
+    }
+  };
+  for (int s = 0; s < NB; ++s) issue_idx(s);
+  cp_commit();
+  cp_wait<0>();
+  __syncwarp();
+  for (int s = 0; s < NB; ++s) {
+    issue_x(s);
+    issue_idx(s + NB);
+    cp_commit();
+  }
+
+  // ---- window metadata, rolled 3 windows ahead ----
+  auto ptr_of = [&](int w) { return (int64_t)__ldg(a.ptr + min((int64_t)w * 16, a.n)); };
+  auto blk_of = [&](int w) { return __ldg(a.boff + min(w, a.win_end)) - gb0; };
+  int cb0 = 0, cb1 = blk_of(ws + 1), nb2 = blk_of(ws + 2), nb3 = blk_of(ws + 3);
+  int64_t e0 = ptr_of(ws), e1 = ptr_of(ws + 1), e2 = ptr_of(ws + 2), e3 = ptr_of(ws + 3);
+  uint32_t pf[kEPL], of[kEPL];
+  float pw[kEPL], pw2[kEPL];
+  auto weight = [&](const float* w, const uint32_t* widx, int64_t e) {
+    return w ? (widx ? __ldg(w + __ldg(widx + e)) : __ldg(w + e)) : 1.f;
+  };
+  auto prefetch = [&](int64_t lo, int64_t hi) {
+#pragma unroll
+    for (int k = 0; k < kEPL; ++k) {
+      const int64_t e = lo + lane + 32 * k;
+      const bool ok = e < hi;
+      pf[k] = ok ? __ldg(a.efrag + e) : 0xffffffffu;
+      pw[k] = ok ? weight(a.w, a.widx, e) : 0.f;
+      if constexpr (DUAL) pw2[k] = ok ? weight(a.w2, a.widx2, e) : 0.f;
+    }
+  };
+  for (int q = lane; q < kMaxB * 32 * C::OPS; q += 32)
+    reinterpret_cast<uint4*>(afr)[q] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (int k = 0; k < kEPL; ++k) of[k] = 0xffffffffu;
+  prefetch(e0, e1);
+
+  const uint32_t as = smem_u32(afr) + lane * 16;
+  float acc[NT][4];
+  auto clear_frags = [&]() {
+    __syncwarp();
+    for (int q = lane; q < kMaxB * 32 * C::OPS; q += 32)
+      reinterpret_cast<uint4*>(afr)[q] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+  };
+  auto hub_load = [&](int r0) {  // windows with > kMaxB blocks or > 32*kEPL edges
+    clear_frags();
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const uint32_t f = __ldg(a.efrag + e) - (uint32_t)(r0 * 128);
+      if (f < (uint32_t)(kMaxB * 128)) {
+        afr[f] = tf32_rn(weight(a.w, a.widx, e));
+        if constexpr (DUAL) afr2[f] = tf32_rn(weight(a.w2, a.widx2, e));
+      }
+    }
+    __syncwarp();
+  };
+  auto store = [&](int wv) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t r = (int64_t)wv * 16 + g + 8 * h;
+      if (r >= a.n) continue;
+      float o[2 * NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) o[j] = acc[j][2 * h] + 0.f, o[NT + j] = acc[j][2 * h + 1] + 0.f;
+      const int fo = d0 + 2 * t * NT;
+      float* yr = a.y + (r - a.y_row0) * a.ldy + fo;
+#pragma unroll
+      for (int q = 0; q < 2 * NT; ++q) {
+        if (a.bias) o[q] += __ldg(a.bias + fo + q);
+      }
+      if (a.accumulate) {
+#pragma unroll
+        for (int q = 0; q < 2 * NT; ++q) o[q] += yr[q];
+      }
+      if constexpr (NT == 4) {
+        reinterpret_cast<float4*>(yr)[0] = make_float4(o[0], o[1], o[2], o[3]);
+        reinterpret_cast<float4*>(yr)[1] = make_float4(o[4], o[5], o[6], o[7]);
+      } else if constexpr (NT == 2) {
+        reinterpret_cast<float4*>(yr)[0] = make_float4(o[0], o[1], o[2], o[3]);
+      } else {
+        reinterpret_cast<float2*>(yr)[0] = make_float2(o[0], o[1]);
+      }
+    }
+  };
+
+  int s = 0;
+  for (int w = ws; w < we; ++w) {
+    const int nbw = cb1 - cb0;
+    const bool hub = nbw > kMaxB || e1 - e0 > 32 * kEPL;
+    // InitSparse
+    __syncwarp();
+    if (!hub) {
+#pragma unroll
+      for (int k = 0; k < kEPL; ++k)
+        if (pf[k] < (uint32_t)(kMaxB * 128)) {
+          afr[pf[k]] = tf32_rn(pw[k]);
+          if constexpr (DUAL) afr2[pf[k]] = tf32_rn(pw2[k]);
+        }
+#pragma unroll
+      for (int k = 0; k < kEPL; ++k) of[k] = pf[k];
+      __syncwarp();
+    } else {
+      hub_load(0);
+    }
+    prefetch(e1, e2);
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+    for (int lb = 0; lb < nbw; ++lb, ++s) {
+      if (lb >= kMaxB && (lb & (kMaxB - 1)) == 0) hub_load(lb);
+      cp_wait<NB - 1>();
+      __syncwarp();
+      const uint32_t sb = ring + (s & (NB - 1)) * SLOT * C::OPS;
+      const uint32_t fa = as + (lb & (kMaxB - 1)) * 512;
+      {
+        float x0[NT], x1[NT];
+        lds_slice<NT>(x0, sb + so0);
+        lds_slice<NT>(x1, sb + so1);
+        const uint4 af = lds_frag(fa);
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+          mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
+      }
+      if constexpr (DUAL) {
+        float x0[NT], x1[NT];
+        lds_slice<NT>(x0, sb + SLOT + so0);
+        lds_slice<NT>(x1, sb + SLOT + so1);
+        const uint4 af = lds_frag(fa + kMaxB * 512);
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+          mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
+      }
+      __syncwarp();
+      issue_x(s + NB);
+      issue_idx(s + 2 * NB);
+      cp_commit();
+    }
+    store(w);
+    // un-scatter this window's fragment slots
+    __syncwarp();
+    if (!hub) {
+#pragma unroll
+      for (int k = 0; k < kEPL; ++k)
+        if (of[k] < (uint32_t)(kMaxB * 128)) {
+          afr[of[k]] = 0u;
+          if constexpr (DUAL) afr2[of[k]] = 0u;
+        }
+    } else {
+      clear_frags();
+    }
+    cb0 = cb1, cb1 = nb2, nb2 = nb3, nb3 = blk_of(w + 4);
+    e0 = e1, e1 = e2, e2 = e3, e3 = ptr_of(w + 4);
+  }
+  cp_wait<0>();
+}
+
+// ---- tiling preprocessing ---------------------------------------------------
+
+// block_offsets[w] = sum of win_partition[0..w) (single CTA; once per tiling)
+__global__ void block_offsets_kernel(const uint32_t* __restrict__ wp, int64_t W, int32_t* boff) {
+  __shared__ int scratch[33];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < W; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const int v = i < W ? (int)wp[i] : 0;
+    int total;
+    const int ex = block_excl_scan<1024>(v, scratch, &total);
+    if (i < W) boff[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) boff[W] = carry;
+}
+
+// col_stream[8 b + 2 i + j] = col_to_node[col_offsets[w] + 8 (b - boff[w]) + i + 4 j]
+// (pair-interleaved); columns past the window's last repeat its first node;
+// the kStreamPad blocks past the end repeat the stream's first block.
+__global__ void col_stream_kernel(const int64_t* __restrict__ coff, const uint32_t* __restrict__ c2n,
+                                  const int32_t* __restrict__ boff, int64_t W, uint32_t* cs) {
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= W) return;
+  const int64_t c0 = coff[w], u = coff[w + 1] - c0;
+  const int64_t b0 = boff[w], nb = boff[w + 1] - b0;
+  for (int64_t q = lane; q < nb * 8; q += 32) {
+    const int64_t b = q >> 3, k = q & 7;
+    const int64_t c = b * 8 + (k >> 1) + 4 * (k & 1);
+    cs[8 * b0 + q] = c2n[c0 + (c < u ? c : 0)];
+  }
+}
+
+__global__ void stream_pad_kernel(const int32_t* __restrict__ boff, int64_t W, uint32_t* cs,
+                                  const uint32_t* __restrict__ c2n) {
+  const int64_t tb = boff[W];
+  const uint32_t fill = tb > 0 ? cs[0] : (c2n ? c2n[0] : 0u);
+  for (int q = threadIdx.x; q < 8 * TCG_STREAM_PAD; q += blockDim.x) cs[8 * tb + q] = fill;
+}
+
+template <int NT, bool DUAL>
+int launch_t(Args& a, int nchunks, cudaStream_t s) {
+  using C = Cfg<NT, DUAL>;
+  auto kern = spmm_stream<NT, DUAL>;
+  static int configured = -1;
+  int dev = 0;
+  TCG_CUDA(cudaGetDevice(&dev), "spmm_stream device");
+  if (configured != dev) {
+    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
+             "spmm_stream attr");
+    configured = dev;
+  }
+  int per_sm = 1;
+  TCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPC * 32, C::SMEM),
+           "spmm_stream occupancy");
+  if (per_sm < 1) per_sm = 1;
+  int64_t ctas = (int64_t)num_sms() * per_sm;
+  // a handful of blocks per warp at least (tiny graphs)
+  const int64_t tb = 0;  // unknown on the host; the kernel tolerates idle warps
+  (void)tb;
+  a.nwarps = (int)(ctas * C::WPC);
+  dim3 grid((unsigned)ctas, (unsigned)nchunks);
+  kern<<<grid, C::WPC * 32, C::SMEM, s>>>(a);
+  TCG_LAUNCHED("spmm_stream");
+  return TCG_OK;
+}
+
+}  // namespace stream
+
+// Returns TCG_E_UNSUPPORTED (nothing launched) when the operands do not fit
+// the engine's vector paths; the caller then uses the window engine.
+int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
+  if (!t->block_offsets || !t->col_stream) return TCG_E_UNSUPPORTED;
+  const int dim = q.dim;
+  const bool dual = q.x2 != nullptr;
+  if (dim % 8 != 0 || !q.vec_out || q.nwin <= 0) return TCG_E_UNSUPPORTED;
+  auto al = [](const void* p, int b) { return (reinterpret_cast<uintptr_t>(p) % b) == 0; };
+  // each chunk width must keep per-lane slices aligned
+  const int full = dim / 32, rem = dim % 32;
+  auto ok_for = [&](int nt) {
+    const int b = 4 * nt;
+    return al(q.x, b) && (q.ldx * 4) % b == 0 &&
+           (!dual || (al(q.x2, b) && (q.ldx2 * 4) % b == 0));
+  };
+  if (full > 0 && !ok_for(4)) return TCG_E_UNSUPPORTED;
+  if (rem >= 16 && !ok_for(2)) return TCG_E_UNSUPPORTED;
+  if (rem % 16 == 8 && !ok_for(1)) return TCG_E_UNSUPPORTED;
+  stream::Args a{};
+  a.ptr = t->node_ptr;
+  a.efrag = t->edge_frag;
+  a.boff = t->block_offsets;
+  a.cs = t->col_stream;
+  a.n = t->num_nodes;
+  a.win_begin = (int)q.win_begin;
+  a.win_end = (int)(q.win_begin + q.nwin);
+  a.ldx = (int)q.ldx, a.ldx2 = (int)q.ldx2;
+  a.x = q.x, a.x2 = q.x2, a.w = q.w, a.widx = q.widx, a.w2 = q.w2, a.widx2 = q.widx2;
+  a.bias = q.bias, a.y = q.y, a.ldy = q.ldy, a.y_row0 = q.y_row0, a.accumulate = q.accumulate;
+  int rc = TCG_OK;
+  int d = 0;
+  if (full > 0) {
+    a.d0 = 0;
+    rc = dual ? stream::launch_t<4, true>(a, full, s) : stream::launch_t<4, false>(a, full, s);
+    if (rc != TCG_OK) return rc;
+    d = 32 * full;
+  }
+  if (rem >= 16) {
+    a.d0 = d;
+    rc = dual ? stream::launch_t<2, true>(a, 1, s) : stream::launch_t<2, false>(a, 1, s);
+    if (rc != TCG_OK) return rc;
+    d += 16;
+  }
+  if (d < dim) {
+    a.d0 = d;
+    rc = dual ? stream::launch_t<1, true>(a, 1, s) : stream::launch_t<1, false>(a, 1, s);
+  }
+  return rc;
+}
+
+}  // namespace tcg
+
+using namespace tcg;
+
+extern "C" int tcg_block_stream(const tcg_tiling* t, int32_t* block_offsets,
+                                uint32_t* col_stream, void* stream) {
+  TCG_REQUIRE(t != nullptr, "tcg_block_stream: null tiling");
+  TCG_REQUIRE(t->blk_h == 16 && t->blk_w == 8,
+              "tf32 mode requires the 16x8 tile shape, got %dx%d", t->blk_h, t->blk_w);
+  TCG_REQUIRE(block_offsets != nullptr, "tcg_block_stream: null block_offsets");
+  TCG_REQUIRE(t->num_windows < (1LL << 31) && t->num_unique < (1LL << 34),
+              "tcg_block_stream: graph too large for 32-bit block offsets");
+  cudaStream_t s = as_stream(stream);
+  const int64_t W = t->num_windows;
+  if (W == 0) {
+    TCG_CUDA(cudaMemsetAsync(block_offsets, 0, sizeof(int32_t), s), "tcg_block_stream memset");
+    return TCG_OK;
+  }
+  TCG_REQUIRE(t->win_partition && t->col_offsets, "tcg_block_stream: tiling arrays missing");
+  stream::block_offsets_kernel<<<1, 1024, 0, s>>>(t->win_partition, W, block_offsets);
+  TCG_LAUNCHED("block_offsets");
+  if (col_stream == nullptr) return TCG_OK;  // offsets only (caller sizes the stream)
+  if (t->num_unique > 0) {
+    TCG_REQUIRE(t->col_to_node != nullptr, "tcg_block_stream: null col_to_node");
+    stream::col_stream_kernel<<<(unsigned)((W + 7) / 8), 256, 0, s>>>(
+        t->col_offsets, t->col_to_node, block_offsets, W, col_stream);
+    TCG_LAUNCHED("col_stream");
+  }
+  stream::stream_pad_kernel<<<1, 256, 0, s>>>(block_offsets, W, col_stream, t->col_to_node);
+  TCG_LAUNCHED("stream_pad");
+  return TCG_OK;
+}

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/tcg.h"
+
 namespace tcg {
 namespace win {
 
@@ -75,4 +77,8 @@ inline int nt_for(int64_t dim) {
 }
 
 }  // namespace win
+
+// Block-stream SpMM engine (stream.cu); TCG_E_UNSUPPORTED => nothing launched.
+int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s);
+
 }  // namespace tcg

@@ -138,6 +138,20 @@ class TiledGraph:
                            "tcg_edge_frag")
                 d["edge_frag"] = ef
                 s.edge_frag = ef.data_ptr()
+                # block stream for the SpMM engine (tcg_block_stream)
+                W = self.num_row_windows
+                bo = torch.empty(W + 1, dtype=torch.int32, device=self.device)
+                lib = _lib.load()
+                _lib.check(lib.tcg_block_stream(C.byref(s), bo.data_ptr(), None, _stream_ptr()),
+                           "tcg_block_stream")
+                tb = int(bo[W].item())
+                cs = torch.empty(8 * (tb + _lib.STREAM_PAD), dtype=torch.int32, device=self.device)
+                _lib.check(lib.tcg_block_stream(C.byref(s), bo.data_ptr(), cs.data_ptr(),
+                                                _stream_ptr()), "tcg_block_stream")
+                d["block_offsets"] = bo
+                d["col_stream"] = cs
+                s.block_offsets = bo.data_ptr()
+                s.col_stream = cs.data_ptr()
             self._aux["abi"] = s
         return s
 

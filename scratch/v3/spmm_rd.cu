@@ -1,0 +1,332 @@
+// Standalone design study: register-direct, warp-per-window-stream TF32 SpMM
+// (arxiv-shaped uniform graph, D=32). Build: nvcc -O3 -gencode
+// arch=compute_100a,code=sm_100a -lineinfo spmm_rd.cu -o spmm_rd
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <numeric>
+#include <random>
+#include <vector>
+
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e = (x);                                                        \
+    if (e != cudaSuccess) {                                                     \
+      printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+      exit(1);                                                                  \
+    }                                                                           \
+  } while (0)
+
+__device__ __forceinline__ uint32_t tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+struct P {
+  int64_t n, nwin;
+  const int64_t* ptr;    // N+1
+  const int64_t* boff;   // W+1 block offsets (exclusive cumsum of wp)
+  const int* c2np;       // 8*TB padded col_to_node (-1 pad)
+  const uint32_t* efl;   // per-edge local fragment slot lb*128 + lane*4 + slot
+  const float* w;        // edge weights (nullable)
+  const float* x;        // N x 32
+  float* y;              // N x 32
+  int nwarps;
+};
+
+constexpr int MAXB = 16;  // A-frag blocks per warp in smem (8 KB)
+constexpr int NB = 8;     // ring depth (blocks)
+constexpr int EPL = 6;    // prefetched edges per lane (192 per window)
+constexpr int WPC = 8;    // warps per CTA
+
+// window metadata prefetch
+struct WinMeta {
+  int64_t e0, e1, b0, b1;
+};
+
+__device__ __forceinline__ int lower_bound64(const int64_t* a, int64_t n, int64_t v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t m = (lo + hi) >> 1;
+    if (__ldg(a + m) < v) lo = m + 1;
+    else hi = m;
+  }
+  return (int)lo;
+}
+
+__global__ void __launch_bounds__(WPC * 32, 2) spmm_rd(const P p) {
+  extern __shared__ __align__(16) uint32_t afr_all_[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gw = blockIdx.x * WPC + wid;
+  uint32_t* afr = afr_all_ + wid * MAXB * 128;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t TB = __ldg(p.boff + p.nwin);
+  // window range [ws, we) of this warp: balanced by blocks
+  const int ws = lower_bound64(p.boff, p.nwin, (TB * gw) / p.nwarps);
+  const int we = lower_bound64(p.boff, p.nwin, (TB * (gw + 1)) / p.nwarps);
+  if (ws >= we) return;
+  const int64_t gb0 = __ldg(p.boff + ws), gb1 = __ldg(p.boff + we);
+  const int64_t nblk = gb1 - gb0;
+
+  // ---- the X ring: block k of the stream lands in slot k % NB ----
+  float4 xr[NB][2];
+  int idx[2];  // c2np of a 4-block group: lane l -> col 8*gbase + l (two groups ahead)
+  auto load_idx = [&](int64_t kb) -> int {  // kb: stream block index (multiple of 4)
+    const int64_t c = 8 * (gb0 + kb) + lane;
+    return (kb + lane / 8 < nblk) ? __ldg(p.c2np + c) : -1;
+  };
+  auto issue_group = [&](int slot0, int id) {  // 4 blocks from one idx word
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int n0 = __shfl_sync(0xffffffffu, id, 8 * k + t);
+      const int n1 = __shfl_sync(0xffffffffu, id, 8 * k + t + 4);
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      xr[slot0 + k][0] = n0 >= 0 ? __ldg(reinterpret_cast<const float4*>(p.x + (int64_t)n0 * 32) + g) : z;
+      xr[slot0 + k][1] = n1 >= 0 ? __ldg(reinterpret_cast<const float4*>(p.x + (int64_t)n1 * 32) + g) : z;
+    }
+  };
+  // prime: groups 0..NB/4-1 loaded, idx for groups NB/4, NB/4+1
+  {
+    int i0 = load_idx(0), i1 = load_idx(4);
+    issue_group(0, i0);
+    issue_group(4, i1);
+    idx[0] = load_idx(8);
+    idx[1] = load_idx(12);
+  }
+  // window metadata: current and next
+  auto meta = [&](int w, WinMeta& m) {
+    if (w < we) {
+      m.e0 = __ldg(p.ptr + min((int64_t)w * 16, p.n));
+      m.e1 = __ldg(p.ptr + min((int64_t)w * 16 + 16, p.n));
+      m.b0 = __ldg(p.boff + w) - gb0;
+      m.b1 = __ldg(p.boff + w + 1) - gb0;
+    } else {
+      m.e0 = m.e1 = 0;
+      m.b0 = m.b1 = nblk;
+    }
+  };
+  uint32_t pf[EPL];
+  float pw[EPL];
+  auto prefetch_edges = [&](const WinMeta& m) {
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) {
+      const int64_t e = m.e0 + lane + 32 * k;
+      const bool ok = e < m.e1;
+      pf[k] = ok ? __ldg(p.efl + e) : 0xffffffffu;
+      pw[k] = ok ? (p.w ? __ldg(p.w + e) : 1.f) : 0.f;
+    }
+  };
+  int w = ws;
+  WinMeta cur, nxt;
+  meta(w, cur);
+  meta(w + 1, nxt);
+  prefetch_edges(cur);
+  // scatter current window's A frags (prefetched regs), prefetch next
+  auto scatter = [&](const WinMeta& m) {
+    const int nbw = (int)min(m.b1 - m.b0, (int64_t)MAXB);
+    __syncwarp();
+    for (int q = lane; q < nbw * 32; q += 32) reinterpret_cast<uint4*>(afr)[q] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < EPL; ++k)
+      if (pf[k] < (uint32_t)(MAXB * 128)) afr[pf[k]] = tf32_rn(pw[k]);
+    if (m.e1 - m.e0 > 32 * EPL) {
+      for (int64_t e = m.e0 + 32 * EPL + lane; e < m.e1; e += 32) {
+        const uint32_t f = __ldg(p.efl + e);
+        if (f < (uint32_t)(MAXB * 128)) afr[f] = tf32_rn(p.w ? __ldg(p.w + e) : 1.f);
+      }
+    }
+    __syncwarp();
+  };
+  scatter(cur);
+  prefetch_edges(nxt);
+  float acc[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+
+  auto epilogue = [&](int wv) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t r = (int64_t)wv * 16 + g + 8 * h;
+      if (r < p.n) {
+        float4* yr = reinterpret_cast<float4*>(p.y + r * 32 + 8 * t);
+        yr[0] = make_float4(acc[0][2 * h], acc[1][2 * h], acc[2][2 * h], acc[3][2 * h]);
+        yr[1] = make_float4(acc[0][2 * h + 1], acc[1][2 * h + 1], acc[2][2 * h + 1], acc[3][2 * h + 1]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  };
+
+  for (int64_t kb = 0; kb < nblk; kb += NB) {
+#pragma unroll
+    for (int half = 0; half < NB / 4; ++half) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t b = kb + half * 4 + k;
+        if (b < nblk) {
+          // window transition(s): b is past the current window
+          while (b >= cur.b1) {
+            epilogue(w);
+            ++w;
+            cur = nxt;
+            meta(w + 1, nxt);
+            scatter(cur);
+            prefetch_edges(nxt);
+          }
+          const int lb = (int)(b - cur.b0);
+          if (lb >= MAXB && lb % MAXB == 0) {
+            // hub window: re-scatter the next MAXB blocks from global
+            __syncwarp();
+            for (int q = lane; q < MAXB * 32; q += 32) reinterpret_cast<uint4*>(afr)[q] = make_uint4(0, 0, 0, 0);
+            __syncwarp();
+            for (int64_t e = cur.e0 + lane; e < cur.e1; e += 32) {
+              const int f = (int)__ldg(p.efl + e) - lb * 128;
+              if (f >= 0 && f < MAXB * 128) afr[f] = tf32_rn(p.w ? __ldg(p.w + e) : 1.f);
+            }
+            __syncwarp();
+          }
+          const uint4 af = reinterpret_cast<const uint4*>(afr)[(lb % MAXB) * 32 + lane];
+          const int s = half * 4 + k;
+          const float* x0 = reinterpret_cast<const float*>(&xr[s][0]);
+          const float* x1 = reinterpret_cast<const float*>(&xr[s][1]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
+        }
+      }
+      // refill the 4 slots just consumed with the group NB blocks ahead
+      issue_group(half * 4, idx[half]);
+      idx[half] = load_idx(kb + half * 4 + NB + NB);
+    }
+  }
+  for (; w < we; ++w) epilogue(w);
+}
+
+// ------------------------------------------------------------------ host
+int main(int argc, char** argv) {
+  const int64_t N = 169343;
+  const double avg = 1166243.0 / N;
+  std::mt19937_64 rng(1);
+  const int64_t Mreq = (int64_t)(avg * N);
+  std::vector<std::pair<uint32_t, uint32_t>> ed(Mreq);
+  std::uniform_int_distribution<uint32_t> U(0, (uint32_t)N - 1);
+  for (auto& e : ed) e = {U(rng), U(rng)};
+  std::sort(ed.begin(), ed.end());
+  ed.erase(std::unique(ed.begin(), ed.end()), ed.end());
+  const int64_t M = ed.size();
+  std::vector<int64_t> ptr(N + 1, 0);
+  std::vector<uint32_t> col(M);
+  for (int64_t i = 0; i < M; ++i) ptr[ed[i].first + 1]++, col[i] = ed[i].second;
+  for (int64_t i = 0; i < N; ++i) ptr[i + 1] += ptr[i];
+  const int64_t W = (N + 15) / 16;
+  std::vector<int64_t> boff(W + 1, 0);
+  std::vector<int> c2np;
+  std::vector<uint32_t> efl(M);
+  int maxb = 0;
+  for (int64_t w = 0; w < W; ++w) {
+    int64_t e0 = ptr[w * 16], e1 = ptr[std::min(w * 16 + 16, N)];
+    std::vector<uint32_t> u(col.begin() + e0, col.begin() + e1);
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    int nb = (int)((u.size() + 7) / 8);
+    maxb = std::max(maxb, nb);
+    boff[w + 1] = boff[w] + nb;
+    for (int i = 0; i < nb * 8; ++i) c2np.push_back(i < (int)u.size() ? (int)u[i] : -1);
+    for (int64_t r = w * 16; r < std::min(w * 16 + 16, N); ++r)
+      for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) {
+        int c = (int)(std::lower_bound(u.begin(), u.end(), col[e]) - u.begin());
+        int rl = (int)(r & 15), k = c & 7;
+        efl[e] = (c >> 3) * 128 + ((((rl & 7) << 2) | (k & 3)) << 2) + (rl >> 3) + 2 * (k >> 2);
+      }
+  }
+  const int64_t TB = boff[W];
+  printf("N=%ld M=%ld W=%ld TB=%ld maxb=%d\n", N, M, W, TB, maxb);
+  std::vector<float> x(N * 32), wv(M);
+  std::normal_distribution<float> nd;
+  for (auto& v : x) v = nd(rng);
+  std::uniform_real_distribution<float> ud(0.f, 1.f);
+  for (auto& v : wv) v = ud(rng);
+  // reference (double)
+  std::vector<double> yref(N * 32, 0.0);
+  for (int64_t r = 0; r < N; ++r)
+    for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e)
+      for (int d = 0; d < 32; ++d) yref[r * 32 + d] += (double)wv[e] * x[col[e] * 32 + d];
+
+  int64_t *dptr, *dboff;
+  int* dc2np;
+  uint32_t* defl;
+  float *dw, *dx, *dy;
+  CK(cudaMalloc(&dptr, 8 * (N + 1)));
+  CK(cudaMalloc(&dboff, 8 * (W + 1)));
+  CK(cudaMalloc(&dc2np, 4 * c2np.size()));
+  CK(cudaMalloc(&defl, 4 * M));
+  CK(cudaMalloc(&dw, 4 * M));
+  CK(cudaMalloc(&dx, 4 * N * 32));
+  CK(cudaMalloc(&dy, 4 * N * 32));
+  CK(cudaMemcpy(dptr, ptr.data(), 8 * (N + 1), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dboff, boff.data(), 8 * (W + 1), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dc2np, c2np.data(), 4 * c2np.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(defl, efl.data(), 4 * M, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dw, wv.data(), 4 * M, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dx, x.data(), 4 * N * 32, cudaMemcpyHostToDevice));
+  char* flush;
+  const size_t FL = 512ull << 20;
+  CK(cudaMalloc(&flush, FL));
+  int nsm;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+  const int ctas_per_sm = argc > 1 ? atoi(argv[1]) : 2;
+  P p{N, W, dptr, dboff, dc2np, defl, dw, dx, dy, 0};
+  const int blocks = nsm * ctas_per_sm;
+  const int SMEM = WPC * MAXB * 128 * 4;
+  CK(cudaFuncSetAttribute(spmm_rd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  p.nwarps = blocks * WPC;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  std::vector<float> cold, warm;
+  for (int it = 0; it < 30; ++it) {
+    CK(cudaMemsetAsync(flush, it & 255, FL));
+    cudaEventRecord(a);
+    spmm_rd<<<blocks, WPC * 32, SMEM>>>(p);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (it >= 3) cold.push_back(ms * 1000);
+  }
+  for (int it = 0; it < 30; ++it) {
+    cudaEventRecord(a);
+    spmm_rd<<<blocks, WPC * 32, SMEM>>>(p);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (it >= 3) warm.push_back(ms * 1000);
+  }
+  CK(cudaGetLastError());
+  std::sort(cold.begin(), cold.end());
+  std::sort(warm.begin(), warm.end());
+  std::vector<float> y(N * 32);
+  CK(cudaMemcpy(y.data(), dy, 4 * N * 32, cudaMemcpyDeviceToHost));
+  double num = 0, den = 0;
+  for (int64_t i = 0; i < N * 32; ++i) num += (y[i] - yref[i]) * (y[i] - yref[i]), den += yref[i] * yref[i];
+  const double U_ = (double)c2np.size();
+  const double bytes = 8.0 * N * 32 + 8.0 * M + 4 * U_ + 8.0 * (N + 1) + 8.0 * (W + 1) + 4 * W;
+  printf("ctas/sm=%d cold median %.2f us (min %.2f)  warm median %.2f us  relL2 %.3e  alg %.1f GB/s (frac %.3f)\n",
+         ctas_per_sm, cold[cold.size() / 2], cold[0], warm[warm.size() / 2], std::sqrt(num / den),
+         bytes / (cold[cold.size() / 2] * 1e3), bytes / (cold[cold.size() / 2] * 1e3) / 6549.8);
+  return 0;
+}

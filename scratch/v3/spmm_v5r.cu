@@ -1,0 +1,332 @@
+// Standalone design study: register-direct, warp-per-window-stream TF32 SpMM
+// (arxiv-shaped uniform graph, D=32). Build: nvcc -O3 -gencode
+// arch=compute_100a,code=sm_100a -lineinfo spmm_rd.cu -o spmm_rd
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <numeric>
+#include <random>
+#include <vector>
+
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e = (x);                                                        \
+    if (e != cudaSuccess) {                                                     \
+      printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+      exit(1);                                                                  \
+    }                                                                           \
+  } while (0)
+
+__device__ __forceinline__ uint32_t tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+struct P {
+  int64_t n, nwin;
+  const int64_t* ptr;    // N+1
+  const int64_t* boff;   // W+1 block offsets (exclusive cumsum of wp)
+  const int* c2np;       // 8*TB padded col_to_node (-1 pad)
+  const uint32_t* efl;   // per-edge local fragment slot lb*128 + lane*4 + slot
+  const float* w;        // edge weights (nullable)
+  const float* x;        // N x 32
+  float* y;              // N x 32
+  int nwarps;
+  const int* wstart;  // nwarps+1 window starts
+};
+
+#ifndef WPC
+#define WPC 4             // warps per CTA
+#endif
+#ifndef MINB
+#define MINB 3
+#endif
+#ifndef NB
+#define NB 12             // X ring depth (blocks)
+#endif
+#ifndef MAXB
+#define MAXB 8            // A-frag blocks resident per warp
+#endif
+#ifndef EPL
+#define EPL 5             // prefetched edges per lane
+#endif
+constexpr int NI = 2 * NB;  // idx ring
+constexpr int WARP_SMEM = NB * 1024 + NI * 32 + MAXB * 512;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async16(uint32_t s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__global__ void __launch_bounds__(WPC * 32, MINB) spmm_rd(const P p) {
+  extern __shared__ __align__(128) unsigned char smem_[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gw = blockIdx.x * WPC + wid;
+  unsigned char* wsm = smem_ + wid * WARP_SMEM;
+  const uint32_t xring = smem_u32(wsm);
+  const int* iring = reinterpret_cast<const int*>(wsm + NB * 1024);
+  const uint32_t iring_s = smem_u32(iring);
+  uint32_t* afr = reinterpret_cast<uint32_t*>(wsm + NB * 1024 + NI * 32);
+  const int g = lane >> 2, t = lane & 3;
+  const int nwin = (int)p.nwin;
+  const int ws = __ldg(p.wstart + gw), we = __ldg(p.wstart + gw + 1);
+  if (ws >= we) return;
+#ifndef REPS
+#define REPS 1
+#endif
+  for (int rep = 0; rep < REPS; ++rep) {
+  const int64_t gb0 = __ldg(p.boff + ws);
+  const int nblk = (int)(__ldg(p.boff + we) - gb0);
+  const int* c2n = p.c2np + 8 * gb0;
+  const float* xg = p.x + 4 * g;
+  const uint32_t so0 = t * 128 + ((g ^ (2 * t)) & 7) * 16;
+  const uint32_t so1 = (t + 4) * 128 + ((g ^ (2 * t)) & 7) * 16;
+
+  auto issue_idx = [&](int s) {
+    if (lane < 2 && s < nblk) cp_async16(iring_s + (s % NI) * 32 + lane * 16, c2n + 8 * s + 4 * lane);
+  };
+  auto issue_x = [&](int s) {
+    if (s < nblk) {
+      const int2 id = *reinterpret_cast<const int2*>(iring + (s % NI) * 8 + 2 * t);
+      const uint32_t sb = xring + (s % NB) * 1024;
+      cp_async16(sb + so0, xg + (int64_t)id.x * 32);
+      cp_async16(sb + so1, xg + (int64_t)id.y * 32);
+    }
+  };
+  // prologue: idx 0..NB-1, then X 0..NB-1 with idx NB..2NB-1
+  for (int s = 0; s < NB; ++s) issue_idx(s);
+  cp_commit();
+  cp_wait<0>();
+  __syncwarp();
+  for (int s = 0; s < NB; ++s) {
+    issue_x(s);
+    issue_idx(s + NB);
+    cp_commit();
+  }
+  // window metadata (rolling): cur = w, nx = w+1, nn = w+2
+  auto ptr_of = [&](int w) { return (int)__ldg(p.ptr + min((int64_t)w * 16, p.n)); };
+  auto blk_of = [&](int w) { return (int)(__ldg(p.boff + min(w, nwin)) - gb0); };
+  int cb0 = 0, cb1 = blk_of(ws + 1), nb2 = blk_of(ws + 2), nb3 = blk_of(ws + 3);
+  int e0 = ptr_of(ws), e1 = ptr_of(ws + 1), e2 = ptr_of(ws + 2), e3 = ptr_of(ws + 3);
+  uint32_t pf[EPL];
+  float pw[EPL];
+  auto prefetch = [&](int a, int b) {
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) {
+      const int e = a + lane + 32 * k;
+      const bool ok = e < b;
+      pf[k] = ok ? __ldg(p.efl + e) : 0xffffffffu;
+      pw[k] = ok && p.w ? __ldg(p.w + e) : 1.f;
+    }
+  };
+  auto scatter = [&](int base, int a, int b) {  // slots [base*128, (base+MAXB)*128)
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < MAXB; ++q) reinterpret_cast<uint4*>(afr)[q * 32 + lane] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    const uint32_t lo = base * 128;
+#pragma unroll
+    for (int k = 0; k < EPL; ++k)
+      if (pf[k] - lo < (uint32_t)(MAXB * 128)) afr[pf[k] - lo] = tf32_rn(pw[k]);
+    for (int e = a + 32 * EPL + lane; e < b; e += 32) {
+      const uint32_t f = __ldg(p.efl + e) - lo;
+      if (f < (uint32_t)(MAXB * 128)) afr[f] = tf32_rn(p.w ? __ldg(p.w + e) : 1.f);
+    }
+    __syncwarp();
+  };
+  prefetch(e0, e1);
+  float acc[4][4];
+  int s = 0;
+  for (int w = ws; w < we; ++w) {
+    // InitSparse for w (edges prefetched), then prefetch w+1
+    const int nbw = cb1 - cb0;
+    scatter(0, e0, e1);
+    const int we0 = e0, we1 = e1;  // keep for hub rescatter
+    prefetch(e1, e2);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+    for (int lb = 0; lb < nbw; ++lb, ++s) {
+      if (lb >= MAXB && lb % MAXB == 0) {
+        // hub window: reload this round's slots from global
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < MAXB; ++q) reinterpret_cast<uint4*>(afr)[q * 32 + lane] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        for (int e = we0 + lane; e < we1; e += 32) {
+          const uint32_t f = __ldg(p.efl + e) - lb * 128;
+          if (f < (uint32_t)(MAXB * 128)) afr[f] = tf32_rn(p.w ? __ldg(p.w + e) : 1.f);
+        }
+        __syncwarp();
+      }
+      cp_wait<NB - 1>();
+      __syncwarp();
+      const unsigned char* sb = wsm + (s % NB) * 1024;
+      const float4 xa = *reinterpret_cast<const float4*>(sb + so0);
+      const float4 xb = *reinterpret_cast<const float4*>(sb + so1);
+      const uint4 af = reinterpret_cast<const uint4*>(afr)[(lb % MAXB) * 32 + lane];
+      mma_tf32(acc[0], af.x, af.y, af.z, af.w, tf32_rn(xa.x), tf32_rn(xb.x));
+      mma_tf32(acc[1], af.x, af.y, af.z, af.w, tf32_rn(xa.y), tf32_rn(xb.y));
+      mma_tf32(acc[2], af.x, af.y, af.z, af.w, tf32_rn(xa.z), tf32_rn(xb.z));
+      mma_tf32(acc[3], af.x, af.y, af.z, af.w, tf32_rn(xa.w), tf32_rn(xb.w));
+      __syncwarp();  // slot s % NB fully read before it is refilled
+      issue_x(s + NB);
+      issue_idx(s + 2 * NB);
+      cp_commit();
+    }
+    // epilogue (StoreDense): lane (g,t) holds features 8t..8t+7 of rows g, g+8
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = w * 16 + g + 8 * h;
+      if (r < p.n) {
+        float4* yr = reinterpret_cast<float4*>(p.y + (int64_t)r * 32 + 8 * t);
+        yr[0] = make_float4(acc[0][2 * h] + 0.f, acc[1][2 * h] + 0.f, acc[2][2 * h] + 0.f, acc[3][2 * h] + 0.f);
+        yr[1] = make_float4(acc[0][2 * h + 1] + 0.f, acc[1][2 * h + 1] + 0.f, acc[2][2 * h + 1] + 0.f, acc[3][2 * h + 1] + 0.f);
+      }
+    }
+    // roll metadata
+    cb0 = cb1; cb1 = nb2; nb2 = nb3; nb3 = blk_of(w + 4);
+    e0 = e1; e1 = e2; e2 = e3; e3 = ptr_of(w + 4);
+  }
+  cp_wait<0>();
+  }
+}
+
+// ------------------------------------------------------------------ host
+int main(int argc, char** argv) {
+  const int64_t N = 169343;
+  const double avg = 1166243.0 / N;
+  std::mt19937_64 rng(1);
+  const int64_t Mreq = (int64_t)(avg * N);
+  std::vector<std::pair<uint32_t, uint32_t>> ed(Mreq);
+  std::uniform_int_distribution<uint32_t> U(0, (uint32_t)N - 1);
+  for (auto& e : ed) e = {U(rng), U(rng)};
+  std::sort(ed.begin(), ed.end());
+  ed.erase(std::unique(ed.begin(), ed.end()), ed.end());
+  const int64_t M = ed.size();
+  std::vector<int64_t> ptr(N + 1, 0);
+  std::vector<uint32_t> col(M);
+  for (int64_t i = 0; i < M; ++i) ptr[ed[i].first + 1]++, col[i] = ed[i].second;
+  for (int64_t i = 0; i < N; ++i) ptr[i + 1] += ptr[i];
+  const int64_t W = (N + 15) / 16;
+  std::vector<int64_t> boff(W + 1, 0);
+  std::vector<int> c2np;
+  std::vector<uint32_t> efl(M);
+  int maxb = 0;
+  for (int64_t w = 0; w < W; ++w) {
+    int64_t e0 = ptr[w * 16], e1 = ptr[std::min(w * 16 + 16, N)];
+    std::vector<uint32_t> u(col.begin() + e0, col.begin() + e1);
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    int nb = (int)((u.size() + 7) / 8);
+    maxb = std::max(maxb, nb);
+    boff[w + 1] = boff[w] + nb;
+    for (int bb = 0; bb < nb; ++bb) for (int i = 0; i < 8; ++i) { int c = bb * 8 + ((i & 1) ? 4 + i / 2 : i / 2); c2np.push_back(c < (int)u.size() ? (int)u[c] : (int)u[0]); }
+    for (int64_t r = w * 16; r < std::min(w * 16 + 16, N); ++r)
+      for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) {
+        int c = (int)(std::lower_bound(u.begin(), u.end(), col[e]) - u.begin());
+        int rl = (int)(r & 15), k = c & 7;
+        efl[e] = (c >> 3) * 128 + ((((rl & 7) << 2) | (k & 3)) << 2) + (rl >> 3) + 2 * (k >> 2);
+      }
+  }
+  const int64_t TB = boff[W];
+  printf("N=%ld M=%ld W=%ld TB=%ld maxb=%d\n", N, M, W, TB, maxb);
+  std::vector<float> x(N * 32), wv(M);
+  std::normal_distribution<float> nd;
+  for (auto& v : x) v = nd(rng);
+  std::uniform_real_distribution<float> ud(0.f, 1.f);
+  for (auto& v : wv) v = ud(rng);
+  // reference (double)
+  std::vector<double> yref(N * 32, 0.0);
+  for (int64_t r = 0; r < N; ++r)
+    for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e)
+      for (int d = 0; d < 32; ++d) yref[r * 32 + d] += (double)wv[e] * x[col[e] * 32 + d];
+
+  int64_t *dptr, *dboff;
+  int* dc2np;
+  uint32_t* defl;
+  float *dw, *dx, *dy;
+  CK(cudaMalloc(&dptr, 8 * (N + 1)));
+  CK(cudaMalloc(&dboff, 8 * (W + 1)));
+  CK(cudaMalloc(&dc2np, 4 * c2np.size()));
+  CK(cudaMalloc(&defl, 4 * M));
+  CK(cudaMalloc(&dw, 4 * M));
+  CK(cudaMalloc(&dx, 4 * N * 32));
+  CK(cudaMalloc(&dy, 4 * N * 32));
+  CK(cudaMemcpy(dptr, ptr.data(), 8 * (N + 1), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dboff, boff.data(), 8 * (W + 1), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dc2np, c2np.data(), 4 * c2np.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(defl, efl.data(), 4 * M, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dw, wv.data(), 4 * M, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dx, x.data(), 4 * N * 32, cudaMemcpyHostToDevice));
+  char* flush;
+  const size_t FL = 512ull << 20;
+  CK(cudaMalloc(&flush, FL));
+  int nsm;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+  const int ctas_per_sm = argc > 1 ? atoi(argv[1]) : MINB;
+  printf("WPC %d NB %d MAXB %d smem/cta %d\n", WPC, NB, MAXB, WPC * WARP_SMEM);
+  const int blocks = nsm * ctas_per_sm;
+  const int nwarps = blocks * WPC;
+  std::vector<int> wst(nwarps + 1);
+  for (int k = 0; k <= nwarps; ++k)
+    wst[k] = (int)(std::lower_bound(boff.begin(), boff.begin() + W, (TB * k) / nwarps) - boff.begin());
+  int* dwst;
+  CK(cudaMalloc(&dwst, 4 * (nwarps + 1)));
+  CK(cudaMemcpy(dwst, wst.data(), 4 * (nwarps + 1), cudaMemcpyHostToDevice));
+  P p{N, W, dptr, dboff, dc2np, defl, dw, dx, dy, 0, dwst};
+  const int SMEM = WPC * WARP_SMEM;
+  CK(cudaFuncSetAttribute(spmm_rd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  p.nwarps = nwarps;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  std::vector<float> cold, warm;
+  for (int it = 0; it < 30; ++it) {
+    CK(cudaMemsetAsync(flush, it & 255, FL));
+    cudaEventRecord(a);
+    spmm_rd<<<blocks, WPC * 32, SMEM>>>(p);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (it >= 3) cold.push_back(ms * 1000);
+  }
+  for (int it = 0; it < 30; ++it) {
+    cudaEventRecord(a);
+    spmm_rd<<<blocks, WPC * 32, SMEM>>>(p);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (it >= 3) warm.push_back(ms * 1000);
+  }
+  CK(cudaGetLastError());
+  std::sort(cold.begin(), cold.end());
+  std::sort(warm.begin(), warm.end());
+  std::vector<float> y(N * 32);
+  CK(cudaMemcpy(y.data(), dy, 4 * N * 32, cudaMemcpyDeviceToHost));
+  double num = 0, den = 0;
+  for (int64_t i = 0; i < N * 32; ++i) num += (y[i] - yref[i]) * (y[i] - yref[i]), den += yref[i] * yref[i];
+  const double U_ = (double)c2np.size();
+  const double bytes = 8.0 * N * 32 + 8.0 * M + 4 * U_ + 8.0 * (N + 1) + 8.0 * (W + 1) + 4 * W;
+  printf("ctas/sm=%d cold median %.2f us (min %.2f)  warm median %.2f us  relL2 %.3e  alg %.1f GB/s (frac %.3f)\n",
+         ctas_per_sm, cold[cold.size() / 2], cold[0], warm[warm.size() / 2], std::sqrt(num / den),
+         bytes / (cold[cold.size() / 2] * 1e3), bytes / (cold[cold.size() / 2] * 1e3) / 6549.8);
+  return 0;
+}
