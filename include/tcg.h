@@ -173,6 +173,15 @@ int tcg_agnn_backward(const tcg_tiling* t, const float* z, int64_t ldz, const fl
                       int64_t lddz, int64_t dz_row0, int64_t win_begin, int64_t win_end,
                       void* stream);
 
+/* Same A-side half in one pass per window with the row term taken from the
+ * forward output: rs_i = sum_j P_ij dP_ij = <G_i, Y_i> (y_fwd: the layer's
+ * forward output, absolute rows), so dS_e = P_e (dP_e - rs_i) is exact per
+ * 16x8 block and dS and A_dS Z come from a single gather of Z. Falls back to
+ * tcg_agnn_backward where the block-stream engine does not apply. */
+int tcg_agnn_backward_fused(const tcg_tiling* t, const float* z, int64_t ldz, const float* gy,
+                            int64_t ldg, const float* y_fwd, int64_t ld_yfwd, int64_t dim,
+                            const float* p, float* ds, float* dz, int64_t lddz, int64_t dz_row0,
+                            int64_t win_begin, int64_t win_end, void* stream);
 /* ---- dense companions of the layers (fp32; no reference counterpart beyond
  * gcn_layer's `agg @ w + b`, kernels.py:577-582) ---------------------------- */
 /* y[n x co] = act((x .* [mask > 0]) . M + bias) (mask: [n x ci]); M is [ci x co]

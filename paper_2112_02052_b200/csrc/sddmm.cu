@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Edge attention scores F[e] = <Xa[row e], Xb[col e]> over the SGT tiling —
 // replaces the reference kernels.sddmm (/root/reference/pkg/src/tcgraph/
 // kernels.py:377-538, Alg. 3) and, fused into its epilogue, the row softmax
@@ -194,6 +195,12 @@ extern "C" int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz
   TCG_REQUIRE(0 <= win_begin && win_begin <= win_end && win_end <= t->num_windows,
               "tcg_agnn_forward: window range outside [0, %lld)", (long long)t->num_windows);
   const int nt = win::nt_for(dim);
+  static const bool no_stream = std::getenv("TCG_NO_STREAM") != nullptr;
+  if (!no_stream && dim == 32 && t->num_edges > 0 && win_begin < win_end && z && p && y) {
+    const int rc = stream_agnn(t, false, z, ldz, z, ldz, nullptr, 0, nullptr, p, y, ldy, y_row0,
+                               win_begin, win_end, as_stream(stream));
+    if (rc != TCG_E_UNSUPPORTED) return rc;
+  }
   if (t->num_edges == 0 || dim > 64 || !fits_fused(t, nt)) {
     if (t->num_edges) {
       int rc = tcg_sddmm(t, z, ldz, z, ldz, dim, nullptr, p, win_begin, win_end, TCG_PREC_TF32,
@@ -212,6 +219,30 @@ extern "C" int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz
   q.x = z, q.ldx = ldz, q.xa = z, q.lda = ldz;
   q.eout = p, q.y = y, q.ldy = ldy, q.y_row0 = y_row0;
   return win::launch(win::MODE_AGNN_FWD, nt, q, as_stream(stream));
+}
+
+extern "C" int tcg_agnn_backward_fused(const tcg_tiling* t, const float* z, int64_t ldz,
+                                       const float* gy, int64_t ldg, const float* y_fwd,
+                                       int64_t ld_yfwd, int64_t dim, const float* p, float* ds,
+                                       float* dz, int64_t lddz, int64_t dz_row0,
+                                       int64_t win_begin, int64_t win_end, void* stream) {
+  TCG_REQUIRE(t != nullptr && dim >= 1 && ldz >= dim && ldg >= dim && lddz >= dim &&
+                  ld_yfwd >= dim,
+              "tcg_agnn_backward_fused: bad arguments");
+  TCG_REQUIRE(t->blk_h == 16 && t->blk_w == 8,
+              "tf32 mode requires the 16x8 tile shape, got %dx%d", t->blk_h, t->blk_w);
+  TCG_REQUIRE(0 <= win_begin && win_begin <= win_end && win_end <= t->num_windows,
+              "tcg_agnn_backward_fused: window range outside [0, %lld)",
+              (long long)t->num_windows);
+  static const bool no_stream = std::getenv("TCG_NO_STREAM") != nullptr;
+  if (!no_stream && dim == 32 && t->num_edges > 0 && win_begin < win_end) {
+    TCG_REQUIRE(z && gy && y_fwd && p && ds && dz, "tcg_agnn_backward_fused: null pointer");
+    const int rc = stream_agnn(t, true, z, ldz, gy, ldg, y_fwd, ld_yfwd, p, ds, dz, lddz, dz_row0,
+                               win_begin, win_end, as_stream(stream));
+    if (rc != TCG_E_UNSUPPORTED) return rc;
+  }
+  return tcg_agnn_backward(t, z, ldz, gy, ldg, dim, p, ds, dz, lddz, dz_row0, win_begin, win_end,
+                           stream);
 }
 
 extern "C" int tcg_agnn_backward(const tcg_tiling* t, const float* z, int64_t ldz,

@@ -344,6 +344,342 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32, 1) spmm_stream(const 
   cp_wait<0>();
 }
 
+// ---- fused AGNN aggregation on the block stream (D = 32) -------------------
+//
+// Forward (reference kernels.agnn_layer, kernels.py:586-601):
+//   S_e = <Z_i, Z_j> (TF32 mma; A = the window's own 16 rows in registers,
+//   B = the staged neighbour rows), P = rowsoftmax(S), Y = A_P Z.
+// One pass per window with an online (running-max) softmax: per block the
+// scores are computed, the row maxima updated, the accumulator rescaled and
+// the unnormalised probabilities fed straight into the SpMM mma. The SDDMM's
+// 8 output columns are permuted (C column 2t <-> column t, 2t+1 <-> t+4) so
+// its C fragment IS the SpMM's A fragment: no shuffles between the two mmas.
+// Raw scores are kept per edge in shared memory; P_e = exp(S_e - m_i) / l_i
+// is written at the window end.
+//
+// Backward, A-side half (no reference counterpart):
+//   dP_e = <G_i, Z_j>, dS_e = P_e (dP_e - rs_i), dZ_i = sum_e dS_e Z_j with
+//   rs_i = sum_j P_ij dP_ij = <G_i, Y_i> (Y = the forward output; the
+//   FlashAttention D_i identity), so dS is exact per block and one pass does
+//   both products.
+struct AgnnArgs {
+  const int64_t* ptr;
+  const uint32_t* efrag;
+  const int32_t* boff;
+  const uint32_t* cs;
+  int64_t n;
+  int win_begin, win_end, nwarps;
+  const float* z;    // gathered operand (neighbour rows)
+  int64_t ldz;
+  const float* za;   // own-row operand: Z (fwd) / G (bwd)
+  int64_t lda;
+  const float* yf;   // bwd: forward output Y (absolute rows)
+  int64_t ldyf;
+  const float* pin;  // bwd: P
+  float* eout;       // fwd: P, bwd: dS
+  float* y;          // fwd: Y, bwd: dZ (A-side)
+  int64_t ldy, y_row0;
+};
+
+constexpr int kMapB = 24;   // blocks per window covered by the slot map (192 columns)
+constexpr int kMaxE = 255;  // edges per window (u8 slot map)
+
+template <bool BWD>
+struct AgnnCfg {
+  static constexpr int NB = 4, NI = 8;
+  static constexpr int RING = NB * 1024;
+  static constexpr int IDX = NI * 32;
+  static constexpr int MAP = kMapB * 128;      // u8 per fragment slot: local edge + 1
+  static constexpr int ESC = 256 * 4;          // per-edge scores (fwd) / P (bwd)
+  static constexpr int ROW = 64 * 4;           // row stats
+  static constexpr int WARP = RING + IDX + MAP + ESC + ROW;
+  static constexpr int WPC = 8;
+  static constexpr int SMEM = WPC * WARP;
+};
+
+// staged-row swizzle serving both fragment patterns: SpMM (rows t, t+4;
+// chunk g) and the column-permuted SDDMM (row (g>>1) + 4(g&1); chunks t, t+4)
+__device__ __forceinline__ uint32_t agnn_off(int r, int c) {
+  const int h = ((2 * (r & 3)) ^ (4 * (r >> 2))) & 7;
+  return r * 128 + ((c ^ h) & 7) * 16;
+}
+
+template <bool BWD>
+__global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 1) agnn_stream(const AgnnArgs a) {
+  using C = AgnnCfg<BWD>;
+  constexpr int NB = C::NB, NI = C::NI;
+  constexpr float kLog2e = 1.4426950408889634f;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gw = blockIdx.x * C::WPC + wid;
+  const int g = lane >> 2, t = lane & 3;
+  unsigned char* wsm = smem + wid * C::WARP;
+  const uint32_t ring = smem_u32(wsm);
+  const uint32_t iring = ring + C::RING;
+  const unsigned char* iring_p = wsm + C::RING;
+  unsigned char* map = wsm + C::RING + C::IDX;
+  float* esc = reinterpret_cast<float*>(map + C::MAP);
+  float* rowm = esc + 256;   // [16] running max (fwd)
+  float* rowl = rowm + 16;   // [16] 1 / row sum (fwd)
+  float* rowrs = rowl + 16;  // [16] rs (bwd)
+
+  const int B0 = __ldg(a.boff + a.win_begin), B1 = __ldg(a.boff + a.win_end);
+  const int64_t TBr = B1 - B0;
+  const int lo_b = B0 + (int)(TBr * gw / a.nwarps);
+  const int hi_b = B0 + (int)(TBr * (gw + 1) / a.nwarps);
+  const int ws = warp_lower_bound(a.boff, a.win_begin, a.win_end, lo_b);
+  const int we = gw + 1 == a.nwarps ? a.win_end : warp_lower_bound(a.boff, ws, a.win_end, hi_b);
+  if (ws >= we) return;
+  const int gb0 = __ldg(a.boff + ws);
+
+  const char* xb = reinterpret_cast<const char*>(a.z + g * 4);
+  const uint64_t xrow = (uint64_t)a.ldz * 4;
+  const uint32_t so0 = agnn_off(t, g), so1 = agnn_off(t + 4, g);             // SpMM reads/writes
+  const int pr = (g >> 1) + 4 * (g & 1);                                      // SDDMM row
+  const uint32_t sd0 = agnn_off(pr, t), sd1 = agnn_off(pr, t + 4);
+  const uint32_t* csw = a.cs + 8 * (int64_t)gb0;
+  auto issue_idx = [&](int s) {
+    if (lane < 2) cp_async<16>(iring + (s & (NI - 1)) * 32 + lane * 16, csw + 8 * (int64_t)s + 4 * lane);
+  };
+  auto issue_x = [&](int s) {
+    const uint2 id = *reinterpret_cast<const uint2*>(iring_p + (s & (NI - 1)) * 32 + 8 * t);
+    const uint32_t sb = ring + (s & (NB - 1)) * 1024;
+    cp_async<16>(sb + so0, xb + id.x * xrow);
+    cp_async<16>(sb + so1, xb + id.y * xrow);
+  };
+  for (int s = 0; s < NB; ++s) issue_idx(s);
+  cp_commit();
+  cp_wait<0>();
+  __syncwarp();
+  for (int s = 0; s < NB; ++s) {
+    issue_x(s);
+    issue_idx(s + NB);
+    cp_commit();
+  }
+
+  auto ptr_of = [&](int w) { return (int64_t)__ldg(a.ptr + min((int64_t)w * 16, a.n)); };
+  auto blk_of = [&](int w) { return __ldg(a.boff + min(w, a.win_end)) - gb0; };
+  int cb0 = 0, cb1 = blk_of(ws + 1), nb2 = blk_of(ws + 2), nb3 = blk_of(ws + 3);
+  int64_t e0 = ptr_of(ws), e1 = ptr_of(ws + 1), e2 = ptr_of(ws + 2), e3 = ptr_of(ws + 3);
+  // own rows (A operand of the SDDMM) of the next window, prefetched raw:
+  // lane (g,t): rows g, g+8; features 4t..4t+3 and 4(t+4)..4(t+4)+3
+  float4 own[4], ownn[4], yfn[4];
+  auto load_own = [&](int w, float4 (&o)[4], float4 (&yv)[4]) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int64_t r = (int64_t)w * 16 + g + 8 * (h & 1);
+      const int f = 4 * (t + 4 * (h >> 1));
+      const bool ok = w < a.win_end && r < a.n;
+      o[h] = ok ? __ldg(reinterpret_cast<const float4*>(a.za + r * a.lda + f)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if constexpr (BWD)
+        yv[h] = ok ? __ldg(reinterpret_cast<const float4*>(a.yf + r * a.ldyf + f)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  uint32_t pf[kEPL];
+  float pp[kEPL];
+  auto prefetch = [&](int64_t lo, int64_t hi) {
+#pragma unroll
+    for (int k = 0; k < kEPL; ++k) {
+      const int64_t e = lo + lane + 32 * k;
+      const bool ok = e < hi;
+      pf[k] = ok ? __ldg(a.efrag + e) : 0xffffffffu;
+      if constexpr (BWD) pp[k] = ok ? __ldg(a.pin + e) : 0.f;
+    }
+  };
+  float4 yv[4];
+  load_own(ws, ownn, yfn);
+  prefetch(e0, e1);
+  const uint32_t* map32 = reinterpret_cast<const uint32_t*>(map);
+
+  int s = 0;
+  for (int w = ws; w < we; ++w) {
+    const int nbw = cb1 - cb0;
+    const int ne = (int)(e1 - e0);
+    // ---- InitSparse: slot map (local edge + 1), per-edge P (bwd) ----
+    __syncwarp();
+    for (int q = lane; q < kMapB * 8; q += 32) reinterpret_cast<uint4*>(map)[q] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kEPL; ++k) {
+      if (pf[k] < (uint32_t)(kMapB * 128)) map[pf[k]] = (unsigned char)(lane + 32 * k + 1);
+      if constexpr (BWD)
+        if (lane + 32 * k < ne) esc[lane + 32 * k] = pp[k];
+    }
+    for (int j = 32 * kEPL + lane; j < ne; j += 32) {
+      const uint32_t f = __ldg(a.efrag + e0 + j);
+      if (f < (uint32_t)(kMapB * 128)) map[f] = (unsigned char)(j + 1);
+      if constexpr (BWD) esc[j] = __ldg(a.pin + e0 + j);
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h) own[h] = ownn[h];
+    if constexpr (BWD) {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) yv[h] = yfn[h];
+    }
+    load_own(w + 1, ownn, yfn);
+    prefetch(e1, e2);
+    __syncwarp();
+    // SDDMM A operand (tf32) for this window: a[h][j]: h = (row g/g+8) x (k t/t+4)
+    uint32_t ao[4][4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int hs = (h & 1) | ((h >> 1) << 1);  // own[] index: bit0 row-half, bit1 k-half
+      ao[h][0] = tf32_rn(own[hs].x), ao[h][1] = tf32_rn(own[hs].y);
+      ao[h][2] = tf32_rn(own[hs].z), ao[h][3] = tf32_rn(own[hs].w);
+    }
+    // per-row state: rows g (index 0) and g+8 (index 1)
+    float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f}, rs[2] = {0.f, 0.f};
+    if constexpr (BWD) {
+      // rs_i = <G_i, Y_i> over the lane's 8 features, then over the quad
+#pragma unroll
+      for (int rh = 0; rh < 2; ++rh) {
+        float d = 0.f;
+#pragma unroll
+        for (int kh = 0; kh < 2; ++kh) {
+          const float4 gv = own[rh | (kh << 1)], fv = yv[rh | (kh << 1)];
+          d += gv.x * fv.x + gv.y * fv.y + gv.z * fv.z + gv.w * fv.w;
+        }
+        d += __shfl_xor_sync(0xffffffffu, d, 1);
+        d += __shfl_xor_sync(0xffffffffu, d, 2);
+        rs[rh] = d;
+      }
+    }
+    float acc[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+    for (int lb = 0; lb < nbw; ++lb, ++s) {
+      cp_wait<NB - 1>();
+      __syncwarp();
+      const uint32_t sb = ring + (s & (NB - 1)) * 1024;
+      // SDDMM: sc = scores in SpMM-A layout (slot order: (g,t), (g+8,t), (g,t+4), (g+8,t+4))
+      float sc[4] = {0.f, 0.f, 0.f, 0.f};
+      {
+        float b0[4], b1[4];
+        lds_slice<4>(b0, sb + sd0);
+        lds_slice<4>(b1, sb + sd1);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          mma_tf32(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], tf32_rn(b0[j]), tf32_rn(b1[j]));
+      }
+      // C (g, 2t) <-> A (g, t); C (g, 2t+1) <-> A (g, t+4): A slots are
+      // (0: (g,t), 1: (g+8,t), 2: (g,t+4), 3: (g+8,t+4)); C regs are
+      // (0: (g,2t), 1: (g,2t+1), 2: (g+8,2t), 3: (g+8,2t+1))
+      const float v[4] = {sc[0], sc[2], sc[1], sc[3]};
+      const uint32_t mw = lb < kMapB ? map32[lb * 32 + lane] : 0u;
+      float av[4];
+      if constexpr (!BWD) {
+        float bm[2];
+        bm[0] = fmaxf((mw & 0xffu) ? v[0] : -INFINITY, (mw & 0xff0000u) ? v[2] : -INFINITY);
+        bm[1] = fmaxf((mw & 0xff00u) ? v[1] : -INFINITY, (mw & 0xff000000u) ? v[3] : -INFINITY);
+#pragma unroll
+        for (int rh = 0; rh < 2; ++rh) {
+          bm[rh] = fmaxf(bm[rh], __shfl_xor_sync(0xffffffffu, bm[rh], 1));
+          bm[rh] = fmaxf(bm[rh], __shfl_xor_sync(0xffffffffu, bm[rh], 2));
+          const float mn = fmaxf(mrow[rh], bm[rh]);
+          const float sf = mn == -INFINITY ? 1.f : exp2f((mrow[rh] - mn) * kLog2e);
+          mrow[rh] = mn;
+          lrow[rh] *= sf;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[j][2 * rh] *= sf, acc[j][2 * rh + 1] *= sf;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t ej = (mw >> (8 * q)) & 0xffu;
+          av[q] = ej ? exp2f((v[q] - mrow[q & 1]) * kLog2e) : 0.f;
+          lrow[q & 1] += av[q];
+          if (ej) esc[ej - 1] = v[q];
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t ej = (mw >> (8 * q)) & 0xffu;
+          float d = 0.f;
+          if (ej) {
+            const float pv = esc[ej - 1];
+            d = pv * (v[q] - rs[q & 1]);
+            a.eout[e0 + ej - 1] = d;
+          }
+          av[q] = d;
+        }
+      }
+      // SpMM: acc += A_av * Zc
+      {
+        float x0[4], x1[4];
+        lds_slice<4>(x0, sb + so0);
+        lds_slice<4>(x1, sb + so1);
+        const uint32_t a0 = tf32_rn(av[0]), a1 = tf32_rn(av[1]), a2 = tf32_rn(av[2]), a3 = tf32_rn(av[3]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mma_tf32(acc[j], a0, a1, a2, a3, tf32_rn(x0[j]), tf32_rn(x1[j]));
+      }
+      __syncwarp();
+      issue_x(s + NB);
+      issue_idx(s + 2 * NB);
+      cp_commit();
+    }
+    // ---- window epilogue ----
+    float inv[2] = {1.f, 1.f};
+    if constexpr (!BWD) {
+#pragma unroll
+      for (int rh = 0; rh < 2; ++rh) {
+        float l = lrow[rh];
+        l += __shfl_xor_sync(0xffffffffu, l, 1);
+        l += __shfl_xor_sync(0xffffffffu, l, 2);
+        inv[rh] = l > 0.f ? 1.f / l : 0.f;
+      }
+      __syncwarp();
+      if (t == 0) {
+        rowm[g] = mrow[0], rowm[g + 8] = mrow[1];
+        rowl[g] = inv[0], rowl[g + 8] = inv[1];
+      }
+      __syncwarp();
+      // P_e = exp(S_e - m_i) / l_i, two lanes per row
+      const int r = lane >> 1, sub = lane & 1;
+      const int64_t rg = (int64_t)w * 16 + r;
+      if (rg < a.n) {
+        const int64_t rb = __ldg(a.ptr + rg) - e0, re = __ldg(a.ptr + rg + 1) - e0;
+        const float m = rowm[r], il = rowl[r];
+        for (int64_t j = rb + sub; j < re; j += 2) a.eout[e0 + j] = exp2f((esc[j] - m) * kLog2e) * il;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t r = (int64_t)w * 16 + g + 8 * h;
+      if (r >= a.n) continue;
+      float4* yr = reinterpret_cast<float4*>(a.y + (r - a.y_row0) * a.ldy + 8 * t);
+      yr[0] = make_float4(acc[0][2 * h] * inv[h], acc[1][2 * h] * inv[h], acc[2][2 * h] * inv[h],
+                          acc[3][2 * h] * inv[h]);
+      yr[1] = make_float4(acc[0][2 * h + 1] * inv[h], acc[1][2 * h + 1] * inv[h],
+                          acc[2][2 * h + 1] * inv[h], acc[3][2 * h + 1] * inv[h]);
+    }
+    cb0 = cb1, cb1 = nb2, nb2 = nb3, nb3 = blk_of(w + 4);
+    e0 = e1, e1 = e2, e2 = e3, e3 = ptr_of(w + 4);
+  }
+  cp_wait<0>();
+}
+
+template <bool BWD>
+int launch_agnn(AgnnArgs& a, cudaStream_t s) {
+  using C = AgnnCfg<BWD>;
+  auto kern = agnn_stream<BWD>;
+  static int configured = -1;
+  int dev = 0;
+  TCG_CUDA(cudaGetDevice(&dev), "agnn_stream device");
+  if (configured != dev) {
+    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
+             "agnn_stream attr");
+    configured = dev;
+  }
+  int per_sm = 1;
+  TCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPC * 32, C::SMEM),
+           "agnn_stream occupancy");
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ctas = (int64_t)num_sms() * per_sm;
+  a.nwarps = (int)(ctas * C::WPC);
+  kern<<<(unsigned)ctas, C::WPC * 32, C::SMEM, s>>>(a);
+  TCG_LAUNCHED(BWD ? "agnn_stream_bwd" : "agnn_stream_fwd");
+  return TCG_OK;
+}
+
 // ---- tiling preprocessing ---------------------------------------------------
 
 // block_offsets[w] = sum of win_partition[0..w) (single CTA; once per tiling)
@@ -466,6 +802,28 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
     rc = dual ? stream::launch_t<1, true>(a, 1, s) : stream::launch_t<1, false>(a, 1, s);
   }
   return rc;
+}
+
+// Fused AGNN forward / backward on the block stream; TCG_E_UNSUPPORTED when
+// the shape does not fit (D != 32, misaligned, windows wider than the slot map).
+int stream_agnn(const tcg_tiling* t, bool bwd, const float* z, int64_t ldz, const float* za,
+                int64_t lda, const float* yf, int64_t ldyf, const float* pin, float* eout,
+                float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
+                cudaStream_t s) {
+  if (!t->block_offsets || !t->col_stream || !t->edge_frag) return TCG_E_UNSUPPORTED;
+  if (t->max_window_edges <= 0 || t->max_window_edges > stream::kMaxE ||
+      t->max_window_unique > 8 * stream::kMapB)
+    return TCG_E_UNSUPPORTED;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al(z) || !al(za) || !al(y) || ldz % 4 || lda % 4 || ldy % 4) return TCG_E_UNSUPPORTED;
+  if (bwd && (!yf || !al(yf) || ldyf % 4 || !pin)) return TCG_E_UNSUPPORTED;
+  stream::AgnnArgs a{};
+  a.ptr = t->node_ptr, a.efrag = t->edge_frag, a.boff = t->block_offsets, a.cs = t->col_stream;
+  a.n = t->num_nodes;
+  a.win_begin = (int)win_begin, a.win_end = (int)win_end;
+  a.z = z, a.ldz = ldz, a.za = za, a.lda = lda, a.yf = yf, a.ldyf = ldyf, a.pin = pin;
+  a.eout = eout, a.y = y, a.ldy = ldy, a.y_row0 = y_row0;
+  return bwd ? stream::launch_agnn<true>(a, s) : stream::launch_agnn<false>(a, s);
 }
 
 }  // namespace tcg

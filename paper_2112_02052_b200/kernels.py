@@ -302,9 +302,11 @@ def agnn_forward_device(t: TiledGraph, z, *, p=None, out=None, win_range=None, y
 
 
 def agnn_backward_device(t: TiledGraph, z, gy, p, *, ds=None, out=None, win_range=None,
-                         y_row0=0):
+                         y_row0=0, y_fwd=None):
     """A-side half of the AGNN backward (tcg_agnn_backward): returns (dZ_A, dS)
-    with dS = P (dP - rowsum(P dP)), dP = <G_i, Z_j>, dZ_A = A_dS Z."""
+    with dS = P (dP - rowsum(P dP)), dP = <G_i, Z_j>, dZ_A = A_dS Z. With the
+    forward output `y_fwd` the one-pass form (tcg_agnn_backward_fused,
+    rowsum(P dP)_i = <G_i, Y_i>) runs."""
     import torch
 
     lib = _lib.load()
@@ -314,6 +316,12 @@ def agnn_backward_device(t: TiledGraph, z, gy, p, *, ds=None, out=None, win_rang
     if out is None:
         out = torch.empty((t.num_nodes, z.shape[1]), dtype=torch.float32, device=z.device)
         y_row0 = 0
+    if y_fwd is not None:
+        _lib.check(lib.tcg_agnn_backward_fused(
+            C.byref(t.abi()), z.data_ptr(), z.stride(0), gy.data_ptr(), gy.stride(0),
+            y_fwd.data_ptr(), y_fwd.stride(0), z.shape[1], p.data_ptr(), ds.data_ptr(),
+            out.data_ptr(), out.stride(0), y_row0, wb, we, _stream()), "tcg_agnn_backward_fused")
+        return out, ds
     _lib.check(lib.tcg_agnn_backward(C.byref(t.abi()), z.data_ptr(), z.stride(0), gy.data_ptr(),
                                      gy.stride(0), z.shape[1], p.data_ptr(), ds.data_ptr(),
                                      out.data_ptr(), out.stride(0), y_row0, wb, we, _stream()),

@@ -109,13 +109,14 @@ class AgnnAggregate(torch.autograd.Function):
             loc = torch.zeros(shard.edges_max, dtype=torch.float32, device=z.device)
             loc[: e1 - e0] = p[e0:e1]
             p = allgather_edges(loc, shard)
-        ctx.save_for_backward(z, p)
+        y = _finish_rows(out, shard)
+        ctx.save_for_backward(z, p, y if mode == "tf32" else None)
         ctx.t, ctx.mode, ctx.shard = t, mode, shard
-        return _finish_rows(out, shard)
+        return y
 
     @staticmethod
     def backward(ctx, g):
-        z, p = ctx.saved_tensors
+        z, p, y_fwd = ctx.saved_tensors
         t, mode, shard = ctx.t, ctx.mode, ctx.shard
         g = g.contiguous()
         m = t.num_edges
@@ -126,7 +127,8 @@ class AgnnAggregate(torch.autograd.Function):
         ds = torch.empty(m, dtype=torch.float32, device=z.device)
         if mode == "tf32":
             # dS and A_dS Z from one gather of Z's neighbour rows
-            agnn_backward_device(t, z, g, p, ds=ds, out=out, win_range=wr, y_row0=r0)
+            agnn_backward_device(t, z, g, p, ds=ds, out=out, win_range=wr, y_row0=r0,
+                                 y_fwd=y_fwd)
         else:
             sddmm_device(t, g, z, mode=mode, epilogue=_lib.EPI_SOFTMAX_BWD, aux=p, out=ds,
                          win_range=wr)

@@ -1,0 +1,169 @@
+"""Block-stream engine (csrc/stream.cu) against the oracle.
+
+The stream engine takes every TF32 SpMM whose feature chunks are multiples of
+8 (NT = 4 / 2 / 1 launches), the dual A^T form of the AGNN backward, and the
+fused AGNN forward / one-pass backward at D = 32. These cases pin it: chunk
+splits (8 ... 128 features), bias / accumulate / shard row offsets, graphs
+with hub windows (> 16 blocks: the fragment re-load path; > 255 edges: the
+fused kernels hand over to the window engine), empty windows, the block
+stream arrays themselves, and the arxiv shape against the exact-f32 path.
+Tolerance: TF32 rel-L2 5e-3 (tests/conftest.py).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import TF32_REL_L2, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    import paper_2112_02052_b200 as tcg
+    from paper_2112_02052_b200 import kernels, layers
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return tcg, kernels, layers, torch
+
+
+def _graph(tcg, kind, n, deg, seed):
+    if kind == "uniform":
+        return tcg.synth.gen_uniform(n, deg, seed)
+    if kind == "powerlaw":
+        return tcg.synth.gen_powerlaw(n, deg, seed)
+    # hub rows: a few rows with hundreds of neighbours plus empty windows
+    rng = np.random.default_rng(seed)
+    src = np.concatenate([rng.integers(0, n, n * deg), np.repeat(np.arange(3), 300),
+                          np.full(400, n // 2)])
+    dst = np.concatenate([rng.integers(0, n, n * deg), rng.integers(0, n, 900),
+                          rng.integers(0, n, 400)])
+    keep = (src < 64) | (src >= 96)  # rows 64..95: two empty windows
+    return tcg.CsrGraph.from_edges(src[keep], dst[keep], n)
+
+
+def test_block_stream_arrays(env, oracle):
+    tcg, _, _, torch = env
+    g = tcg.synth.gen_uniform(777, 5, 3)
+    t = tcg.translate(g, tcg.BlockConfig())
+    t.abi()
+    bo = t.dev["block_offsets"].cpu().numpy()
+    assert np.array_equal(bo, t.block_offsets())
+    cs = t.dev["col_stream"].cpu().numpy().view(np.uint32)
+    tb = int(bo[-1])
+    for w in range(t.num_row_windows):
+        nodes = t.window_nodes(w)
+        for b in range(bo[w], bo[w + 1]):
+            for i in range(8):
+                c = (b - bo[w]) * 8 + (i >> 1) + 4 * (i & 1)
+                want = nodes[c] if c < len(nodes) else nodes[0]
+                assert cs[8 * b + i] == want
+    assert cs.size == 8 * (tb + 16)
+
+
+@pytest.mark.parametrize("dim", [8, 16, 24, 32, 40, 64, 128])
+@pytest.mark.parametrize("kind", ["uniform", "hub"])
+def test_stream_spmm_dims(env, oracle, dim, kind):
+    tcg, kernels, _, torch = env
+    g = _graph(tcg, kind, 3000, 6, 5)
+    t = tcg.translate(g, tcg.BlockConfig())
+    rng = np.random.default_rng(dim)
+    x = rng.standard_normal((g.num_nodes, dim)).astype(np.float32)
+    w = rng.random(g.num_edges).astype(np.float32)
+    y = kernels.spmm_device(t, torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda())
+    ref = oracle.spmm(g.node_pointer, g.edge_list, x, f=w)
+    assert rel_l2(y.cpu().numpy(), ref) <= TF32_REL_L2
+
+
+def test_stream_spmm_bias_accumulate_shard(env, oracle):
+    tcg, kernels, _, torch = env
+    g = tcg.synth.gen_uniform(2500, 7, 9)
+    t = tcg.translate(g, tcg.BlockConfig())
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((2500, 32)).astype(np.float32)
+    b = rng.standard_normal(32).astype(np.float32)
+    y0 = rng.standard_normal((2500, 32)).astype(np.float32)
+    ref = oracle.spmm(g.node_pointer, g.edge_list, x) + b + y0
+    xt, bt = torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda()
+    # full range, accumulate + bias
+    out = torch.from_numpy(y0.copy()).cuda()
+    kernels.spmm_device(t, xt, out=out, bias=bt, accumulate=True)
+    assert rel_l2(out.cpu().numpy(), ref) <= TF32_REL_L2
+    # two shards writing into row slabs at their own row offsets
+    W = t.num_row_windows
+    for wb, we in ((0, W // 3), (W // 3, W)):
+        r0, r1 = wb * 16, min(we * 16, 2500)
+        slab = torch.from_numpy(y0[r0:r1].copy()).cuda()
+        kernels.spmm_device(t, xt, out=slab, bias=bt, accumulate=True, win_range=(wb, we),
+                            y_row0=r0)
+        assert rel_l2(slab.cpu().numpy(), ref[r0:r1]) <= TF32_REL_L2
+
+
+def test_stream_dual_spmm(env, oracle):
+    tcg, kernels, _, torch = env
+    g = tcg.synth.gen_uniform(3000, 6, 13)
+    t = tcg.translate(g, tcg.BlockConfig())
+    rng = np.random.default_rng(4)
+    x1 = rng.standard_normal((3000, 32)).astype(np.float32)
+    x2 = rng.standard_normal((3000, 32)).astype(np.float32)
+    w1 = rng.random(g.num_edges).astype(np.float32)
+    w2 = rng.standard_normal(g.num_edges).astype(np.float32)
+    y = kernels.spmm_device(t, torch.from_numpy(x1).cuda(), torch.from_numpy(w1).cuda(),
+                            x2=torch.from_numpy(x2).cuda(), weights2=torch.from_numpy(w2).cuda())
+    ref = (oracle.spmm(g.node_pointer, g.edge_list, x1, f=w1)
+           + oracle.spmm(g.node_pointer, g.edge_list, x2, f=w2))
+    assert rel_l2(y.cpu().numpy(), ref) <= TF32_REL_L2
+
+
+@pytest.mark.parametrize("kind", ["uniform", "powerlaw", "hub"])
+def test_stream_agnn_forward_backward(env, oracle, kind):
+    tcg, kernels, layers, torch = env
+    g = _graph(tcg, kind, 4000, 7, 21)
+    t = tcg.translate(g, tcg.BlockConfig())
+    rng = np.random.default_rng(6)
+    z = rng.standard_normal((g.num_nodes, 32)).astype(np.float32)
+    gy = rng.standard_normal((g.num_nodes, 32)).astype(np.float32)
+    zt = torch.from_numpy(z).cuda()
+    y, p = kernels.agnn_forward_device(t, zt)
+    ptr, cols = g.node_pointer, g.edge_list
+    p_ref = oracle.segment_softmax(oracle.sddmm(ptr, cols, z), ptr)
+    y_ref = oracle.spmm(ptr, cols, z, f=p_ref)
+    assert rel_l2(p.cpu().numpy()[: g.num_edges], p_ref) <= TF32_REL_L2
+    assert rel_l2(y.cpu().numpy(), y_ref) <= TF32_REL_L2
+    # one-pass backward (rs = <G, Y>) against the restated gradient
+    gyt = torch.from_numpy(gy).cuda()
+    dz_a, ds = kernels.agnn_backward_device(t, zt, gyt, p, y_fwd=y)
+    dp = oracle.sddmm(ptr, cols, gy, z)
+    ds_ref = oracle.softmax_backward(p_ref, dp, ptr)
+    assert rel_l2(ds.cpu().numpy()[: g.num_edges], ds_ref) <= TF32_REL_L2
+    assert rel_l2(dz_a.cpu().numpy(), oracle.spmm(ptr, cols, z, f=ds_ref)) <= TF32_REL_L2
+    zt.requires_grad_(True)
+    out = layers.AgnnAggregate.apply(zt, t, "tf32", None)
+    out.backward(gyt)
+    dz_ref = oracle.agnn_backward(ptr, cols, z, p_ref, gy)
+    assert rel_l2(zt.grad.cpu().numpy(), dz_ref) <= TF32_REL_L2
+
+
+def test_stream_arxiv_against_exact(env):
+    """Full arxiv shape: the TF32 stream SpMM / fused AGNN against the exact-f32
+    CUDA-core path (itself bitwise = the reference f32 fold on small cases)."""
+    tcg, kernels, _, torch = env
+    g = tcg.synth.shaped_graph("arxiv")
+    t = tcg.translate(g, tcg.BlockConfig())
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    z = torch.randn(g.num_nodes, 32, device="cuda", generator=gen)
+    w = torch.rand(g.num_edges, device="cuda", generator=gen)
+    y_tc = kernels.spmm_device(t, z, w)
+    y_ex = kernels.spmm_device(t, z, w, mode="f32")
+    assert rel_l2(y_tc.cpu().numpy(), y_ex.cpu().numpy()) <= TF32_REL_L2
+    y_f, p_f = kernels.agnn_forward_device(t, z)
+    from paper_2112_02052_b200 import _lib
+
+    p_ex = kernels.sddmm_device(t, z, mode="f32", epilogue=_lib.EPI_SOFTMAX)
+    y_ex = kernels.spmm_device(t, z, p_ex, mode="f32")
+    assert rel_l2(p_f.cpu().numpy(), p_ex.cpu().numpy()) <= TF32_REL_L2
+    assert rel_l2(y_f.cpu().numpy(), y_ex.cpu().numpy()) <= TF32_REL_L2
