@@ -159,36 +159,45 @@ __global__ void __launch_bounds__(256) sum_slabs(const float* __restrict__ part,
 }
 
 // One warp per row: log-softmax, NLL, dlogits; per-CTA loss partials.
+// 8 lanes per row (32 rows per CTA); the 8 row losses of each lpart entry are
+// summed in row order, so the mean stays a fixed-order reduction.
 __global__ void __launch_bounds__(256)
     softmax_xent(const float* __restrict__ logits, int64_t ld, const int64_t* __restrict__ labels,
-                 int64_t n, int c, float* __restrict__ dlogits, float* __restrict__ lpart) {
-  __shared__ float wsum[8];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 8 + warp;
+                 int64_t n, int c, float* __restrict__ dlogits, float* __restrict__ lpart,
+                 int64_t parts) {
+  __shared__ float rowc[32];
+  const int sub = threadIdx.x & 7, lr_ = threadIdx.x >> 3;
+  const int64_t row = (int64_t)blockIdx.x * 32 + lr_;
+  const unsigned gm = 0xffu << (threadIdx.x & 24);
   float contrib = 0.f;
   if (row < n) {
     const float* lr = logits + row * ld;
     float mx = -INFINITY;
-    for (int j = lane; j < c; j += 32) mx = fmaxf(mx, lr[j]);
-    mx = warp_max(mx);
-    float s = 0.f;
-    for (int j = lane; j < c; j += 32) s += expf(lr[j] - mx);
-    s = warp_sum(s);
-    const float lse = mx + logf(s);
+    for (int j = sub; j < c; j += 8) mx = fmaxf(mx, __ldg(lr + j));
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(gm, mx, o));
+    float sm = 0.f;
+    for (int j = sub; j < c; j += 8) sm += expf(__ldg(lr + j) - mx);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) sm += __shfl_xor_sync(gm, sm, o);
+    const float lse = mx + logf(sm);
     const int64_t lab = labels[row];
     const float inv_n = 1.f / (float)n;
-    for (int j = lane; j < c; j += 32) {
-      const float pj = expf(lr[j] - lse);
+    for (int j = sub; j < c; j += 8) {
+      const float pj = expf(__ldg(lr + j) - lse);
       dlogits[row * c + j] = (pj - (j == lab ? 1.f : 0.f)) * inv_n;
     }
-    if (lane == 0) contrib = lse - lr[lab];
+    contrib = lse - lr[lab];
   }
-  if (lane == 0) wsum[warp] = contrib;
+  if (sub == 0) rowc[lr_] = contrib;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float s = 0.f;
-    for (int w = 0; w < 8; ++w) s += wsum[w];
-    lpart[blockIdx.x] = s;
+  if (threadIdx.x < 4) {
+    const int64_t part = (int64_t)blockIdx.x * 4 + threadIdx.x;
+    if (part < parts) {
+      float acc = 0.f;
+      for (int r = 0; r < 8; ++r) acc += rowc[threadIdx.x * 8 + r];
+      lpart[part] = acc;
+    }
   }
 }
 
@@ -457,7 +466,8 @@ extern "C" int tcg_softmax_xent(const float* logits, int64_t ld, const int64_t* 
   cudaStream_t s = as_stream(stream);
   const int64_t parts = (n + 7) / 8;
   float* lpart = static_cast<float*>(workspace);
-  softmax_xent<<<(unsigned)parts, 256, 0, s>>>(logits, ld, labels, n, (int)c, dlogits, lpart);
+  softmax_xent<<<(unsigned)((n + 31) / 32), 256, 0, s>>>(logits, ld, labels, n, (int)c, dlogits,
+                                                          lpart, parts);
   TCG_LAUNCHED("softmax_xent");
   final_loss<<<1, 256, 0, s>>>(lpart, parts, n, loss);
   TCG_LAUNCHED("final_loss");

@@ -108,7 +108,6 @@ struct Args {
   int accumulate;
 };
 
-constexpr int kMaxB = 16;  // A-fragment blocks resident per warp (8 KB per operand)
 constexpr int kEPL = 5;    // edges per lane prefetched for the next window (160)
 
 template <int NT, bool DUAL>
@@ -117,11 +116,12 @@ struct Cfg {
   static constexpr int NI = 2 * NB;                // column-id ring
   static constexpr int SLOT = 8 * 32 * NT;         // bytes of one operand's block
   static constexpr int OPS = DUAL ? 2 : 1;
+  static constexpr int MB = DUAL ? 8 : 16;         // A-fragment blocks resident (one round)
   static constexpr int RING = NB * SLOT * OPS;
   static constexpr int IDX = NI * 32;
-  static constexpr int AFR = kMaxB * 512 * OPS;
+  static constexpr int AFR = MB * 512 * OPS;
   static constexpr int WARP = RING + IDX + AFR;
-  static constexpr int WPC = 8;                    // warps per CTA
+  static constexpr int WPC = DUAL ? 4 : 8;         // warps per CTA
   static constexpr int SMEM = WPC * WARP;
 };
 
@@ -145,9 +145,10 @@ __device__ __forceinline__ int warp_lower_bound(const int32_t* __restrict__ a, i
 }
 
 template <int NT, bool DUAL>
-__global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32, 1) spmm_stream(const Args a) {
+__global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Args a) {
   using C = Cfg<NT, DUAL>;
-  constexpr int NB = C::NB, NI = C::NI, SLOT = C::SLOT;
+  constexpr int NB = C::NB, NI = C::NI, SLOT = C::SLOT, MB = C::MB;
+  constexpr uint32_t RS = MB * 128;  // fragment slots of one round
   constexpr int CP = 4 * NT;  // bytes per lane per staged row
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32, 1) spmm_stream(const 
   const uint32_t iring = ring + C::RING;
   const unsigned char* iring_p = wsm + C::RING;
   uint32_t* afr = reinterpret_cast<uint32_t*>(wsm + C::RING + C::IDX);
-  uint32_t* afr2 = afr + kMaxB * 128;
+  uint32_t* afr2 = afr + MB * 128;
 
   // ---- this warp's slice of the block stream ----
   const int B0 = __ldg(a.boff + a.win_begin), B1 = __ldg(a.boff + a.win_end);
@@ -205,8 +206,9 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32, 1) spmm_stream(const 
   auto blk_of = [&](int w) { return __ldg(a.boff + min(w, a.win_end)) - gb0; };
   int cb0 = 0, cb1 = blk_of(ws + 1), nb2 = blk_of(ws + 2), nb3 = blk_of(ws + 3);
   int64_t e0 = ptr_of(ws), e1 = ptr_of(ws + 1), e2 = ptr_of(ws + 2), e3 = ptr_of(ws + 3);
+  // next window's edges (pf/pw) and the current window's (of/ow), in registers
   uint32_t pf[kEPL], of[kEPL];
-  float pw[kEPL], pw2[kEPL];
+  float pw[kEPL], pw2[kEPL], ow[kEPL], ow2[kEPL];
   auto weight = [&](const float* w, const uint32_t* widx, int64_t e) {
     return w ? (widx ? __ldg(w + __ldg(widx + e)) : __ldg(w + e)) : 1.f;
   };
@@ -220,31 +222,39 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32, 1) spmm_stream(const 
       if constexpr (DUAL) pw2[k] = ok ? weight(a.w2, a.widx2, e) : 0.f;
     }
   };
-  for (int q = lane; q < kMaxB * 32 * C::OPS; q += 32)
-    reinterpret_cast<uint4*>(afr)[q] = make_uint4(0, 0, 0, 0);
-#pragma unroll
-  for (int k = 0; k < kEPL; ++k) of[k] = 0xffffffffu;
-  prefetch(e0, e1);
-
-  const uint32_t as = smem_u32(afr) + lane * 16;
-  float acc[NT][4];
   auto clear_frags = [&]() {
     __syncwarp();
-    for (int q = lane; q < kMaxB * 32 * C::OPS; q += 32)
-      reinterpret_cast<uint4*>(afr)[q] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int q = 0; q < MB * C::OPS; ++q) reinterpret_cast<uint4*>(afr)[q * 32 + lane] = make_uint4(0, 0, 0, 0);
     __syncwarp();
   };
-  auto hub_load = [&](int r0) {  // windows with > kMaxB blocks or > 32*kEPL edges
+  // InitSparse for round [lo, lo + RS) of the current window's slots from registers
+  auto put_round = [&](uint32_t lo, bool zero) {
+#pragma unroll
+    for (int k = 0; k < kEPL; ++k) {
+      const uint32_t f = of[k] - lo;
+      if (f < RS) {
+        afr[f] = zero ? 0u : tf32_rn(ow[k]);
+        if constexpr (DUAL) afr2[f] = zero ? 0u : tf32_rn(ow2[k]);
+      }
+    }
+  };
+  auto hub_load = [&](int r0) {  // windows with more than 32*kEPL edges
     clear_frags();
     for (int64_t e = e0 + lane; e < e1; e += 32) {
       const uint32_t f = __ldg(a.efrag + e) - (uint32_t)(r0 * 128);
-      if (f < (uint32_t)(kMaxB * 128)) {
+      if (f < RS) {
         afr[f] = tf32_rn(weight(a.w, a.widx, e));
         if constexpr (DUAL) afr2[f] = tf32_rn(weight(a.w2, a.widx2, e));
       }
     }
     __syncwarp();
   };
+  clear_frags();
+  prefetch(e0, e1);
+
+  const uint32_t as = smem_u32(afr) + lane * 16;
+  float acc[NT][4];
   auto store = [&](int wv) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -255,9 +265,9 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32, 1) spmm_stream(const 
       for (int j = 0; j < NT; ++j) o[j] = acc[j][2 * h] + 0.f, o[NT + j] = acc[j][2 * h + 1] + 0.f;
       const int fo = d0 + 2 * t * NT;
       float* yr = a.y + (r - a.y_row0) * a.ldy + fo;
+      if (a.bias) {
 #pragma unroll
-      for (int q = 0; q < 2 * NT; ++q) {
-        if (a.bias) o[q] += __ldg(a.bias + fo + q);
+        for (int q = 0; q < 2 * NT; ++q) o[q] += __ldg(a.bias + fo + q);
       }
       if (a.accumulate) {
 #pragma unroll
@@ -277,18 +287,15 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32, 1) spmm_stream(const 
   int s = 0;
   for (int w = ws; w < we; ++w) {
     const int nbw = cb1 - cb0;
-    const bool hub = nbw > kMaxB || e1 - e0 > 32 * kEPL;
-    // InitSparse
+    const bool hub = e1 - e0 > 32 * kEPL;
+#pragma unroll
+    for (int k = 0; k < kEPL; ++k) {
+      of[k] = pf[k], ow[k] = pw[k];
+      if constexpr (DUAL) ow2[k] = pw2[k];
+    }
     __syncwarp();
     if (!hub) {
-#pragma unroll
-      for (int k = 0; k < kEPL; ++k)
-        if (pf[k] < (uint32_t)(kMaxB * 128)) {
-          afr[pf[k]] = tf32_rn(pw[k]);
-          if constexpr (DUAL) afr2[pf[k]] = tf32_rn(pw2[k]);
-        }
-#pragma unroll
-      for (int k = 0; k < kEPL; ++k) of[k] = pf[k];
+      put_round(0, false);
       __syncwarp();
     } else {
       hub_load(0);
@@ -297,11 +304,21 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32, 1) spmm_stream(const 
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
     for (int lb = 0; lb < nbw; ++lb, ++s) {
-      if (lb >= kMaxB && (lb & (kMaxB - 1)) == 0) hub_load(lb);
+      if (lb >= MB && (lb & (MB - 1)) == 0) {  // next round of fragment blocks
+        if (!hub) {
+          __syncwarp();
+          put_round((uint32_t)(lb - MB) * 128, true);
+          __syncwarp();
+          put_round((uint32_t)lb * 128, false);
+          __syncwarp();
+        } else {
+          hub_load(lb);
+        }
+      }
       cp_wait<NB - 1>();
       __syncwarp();
       const uint32_t sb = ring + (s & (NB - 1)) * SLOT * C::OPS;
-      const uint32_t fa = as + (lb & (kMaxB - 1)) * 512;
+      const uint32_t fa = as + (lb & (MB - 1)) * 512;
       {
         float x0[NT], x1[NT];
         lds_slice<NT>(x0, sb + so0);
@@ -315,7 +332,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32, 1) spmm_stream(const 
         float x0[NT], x1[NT];
         lds_slice<NT>(x0, sb + SLOT + so0);
         lds_slice<NT>(x1, sb + SLOT + so1);
-        const uint4 af = lds_frag(fa + kMaxB * 512);
+        const uint4 af = lds_frag(fa + MB * 512);
 #pragma unroll
         for (int j = 0; j < NT; ++j)
           mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
@@ -326,15 +343,10 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32, 1) spmm_stream(const 
       cp_commit();
     }
     store(w);
-    // un-scatter this window's fragment slots
+    // un-scatter this window's last round
     __syncwarp();
     if (!hub) {
-#pragma unroll
-      for (int k = 0; k < kEPL; ++k)
-        if (of[k] < (uint32_t)(kMaxB * 128)) {
-          afr[of[k]] = 0u;
-          if constexpr (DUAL) afr2[of[k]] = 0u;
-        }
+      put_round((uint32_t)(nbw > 0 ? ((nbw - 1) & ~(MB - 1)) : 0) * 128, true);
     } else {
       clear_frags();
     }
@@ -381,6 +393,15 @@ struct AgnnArgs {
   int64_t ldy, y_row0;
 };
 
+constexpr float kTau = 8.f;  // lazy-rescale threshold of the online softmax (natural log)
+
+// 2^x (MUFU.EX2, ~2 ulp; ftz). exp(-inf) = 0.
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 constexpr int kMapB = 24;   // blocks per window covered by the slot map (192 columns)
 constexpr int kMaxE = 255;  // edges per window (u8 slot map)
 
@@ -405,7 +426,7 @@ __device__ __forceinline__ uint32_t agnn_off(int r, int c) {
 }
 
 template <bool BWD>
-__global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 1) agnn_stream(const AgnnArgs a) {
+__global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 2) agnn_stream(const AgnnArgs a) {
   using C = AgnnCfg<BWD>;
   constexpr int NB = C::NB, NI = C::NI;
   constexpr float kLog2e = 1.4426950408889634f;
@@ -529,6 +550,7 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 1) agnn_stream(const A
     }
     // per-row state: rows g (index 0) and g+8 (index 1)
     float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f}, rs[2] = {0.f, 0.f};
+    float ml2[2] = {-INFINITY, -INFINITY};
     if constexpr (BWD) {
       // rs_i = <G_i, Y_i> over the lane's 8 features, then over the quad
 #pragma unroll
@@ -568,6 +590,7 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 1) agnn_stream(const A
       const uint32_t mw = lb < kMapB ? map32[lb * 32 + lane] : 0u;
       float av[4];
       if constexpr (!BWD) {
+        // block row maxima (rows g, g+8) over the quad
         float bm[2];
         bm[0] = fmaxf((mw & 0xffu) ? v[0] : -INFINITY, (mw & 0xff0000u) ? v[2] : -INFINITY);
         bm[1] = fmaxf((mw & 0xff00u) ? v[1] : -INFINITY, (mw & 0xff000000u) ? v[3] : -INFINITY);
@@ -575,17 +598,27 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 1) agnn_stream(const A
         for (int rh = 0; rh < 2; ++rh) {
           bm[rh] = fmaxf(bm[rh], __shfl_xor_sync(0xffffffffu, bm[rh], 1));
           bm[rh] = fmaxf(bm[rh], __shfl_xor_sync(0xffffffffu, bm[rh], 2));
-          const float mn = fmaxf(mrow[rh], bm[rh]);
-          const float sf = mn == -INFINITY ? 1.f : exp2f((mrow[rh] - mn) * kLog2e);
-          mrow[rh] = mn;
-          lrow[rh] *= sf;
+        }
+        // lazy rescale: the running max only moves when a score exceeds it by
+        // kTau (exp(s - m) stays <= e^kTau); P uses the same stale max, so the
+        // result is unchanged
+        if (__any_sync(0xffffffffu, bm[0] > mrow[0] + kTau || bm[1] > mrow[1] + kTau)) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[j][2 * rh] *= sf, acc[j][2 * rh + 1] *= sf;
+          for (int rh = 0; rh < 2; ++rh) {
+            const bool up = bm[rh] > mrow[rh] + kTau;
+            const float mn = up ? bm[rh] : mrow[rh];
+            const float sf = up ? ex2_approx((mrow[rh] - mn) * kLog2e) : 1.f;
+            mrow[rh] = mn;
+            ml2[rh] = mn * kLog2e;
+            lrow[rh] *= sf;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j][2 * rh] *= sf, acc[j][2 * rh + 1] *= sf;
+          }
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const uint32_t ej = (mw >> (8 * q)) & 0xffu;
-          av[q] = ej ? exp2f((v[q] - mrow[q & 1]) * kLog2e) : 0.f;
+          av[q] = ej ? ex2_approx(fmaf(v[q], kLog2e, -ml2[q & 1])) : 0.f;
           lrow[q & 1] += av[q];
           if (ej) esc[ej - 1] = v[q];
         }
@@ -638,7 +671,7 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 1) agnn_stream(const A
       if (rg < a.n) {
         const int64_t rb = __ldg(a.ptr + rg) - e0, re = __ldg(a.ptr + rg + 1) - e0;
         const float m = rowm[r], il = rowl[r];
-        for (int64_t j = rb + sub; j < re; j += 2) a.eout[e0 + j] = exp2f((esc[j] - m) * kLog2e) * il;
+        for (int64_t j = rb + sub; j < re; j += 2) a.eout[e0 + j] = ex2_approx((esc[j] - m) * kLog2e) * il;
       }
     }
 #pragma unroll

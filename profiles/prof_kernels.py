@@ -45,7 +45,7 @@ def main():
                     out=out, accumulate=True)
         spmm_device(t, z, p, mode="f32", out=out)
         agnn_forward_device(t, z, p=p, out=out)
-        agnn_backward_device(t, z, gy, p, ds=ds, out=out)
+        agnn_backward_device(t, z, gy, p, ds=ds, out=out, y_fwd=out)
     torch.cuda.synchronize()
 
 
