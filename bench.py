@@ -292,12 +292,12 @@ def run_ours(args):
         net = layers.AGNN(feats, hidden, classes, layers=nlayers, mode="tf32").to(dev)
     else:
         net = layers.GCN(feats, hidden, classes, mode="tf32").to(dev)
-    opt = torch.optim.Adam(net.parameters(), lr=0.01, capturable=True)
+    opt = torch.optim.Adam(net.parameters(), lr=0.01, capturable=True, fused=True)
     x_dev = torch.from_numpy(x_np).to(dev)
     y_dev = torch.from_numpy(labels_np).to(dev)
 
     def train_step():
-        opt.zero_grad(set_to_none=False)
+        opt.zero_grad(set_to_none=True)
         loss = layers.cross_entropy(net(x_dev, t, shard), y_dev)
         loss.backward()
         opt.step()
@@ -459,10 +459,10 @@ def run_ours(args):
         if model_kind == "agnn" and world == 1:
             # the GCN-2 epoch on the same graph (second half of the metric)
             gnet = layers.GCN(feats, 16, classes, mode="tf32").to(dev)
-            gopt = torch.optim.Adam(gnet.parameters(), lr=0.01, capturable=True)
+            gopt = torch.optim.Adam(gnet.parameters(), lr=0.01, capturable=True, fused=True)
 
             def gstep():
-                gopt.zero_grad(set_to_none=False)
+                gopt.zero_grad(set_to_none=True)
                 lo = layers.cross_entropy(gnet(x_dev, t), y_dev)
                 lo.backward()
                 gopt.step()

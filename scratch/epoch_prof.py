@@ -11,9 +11,9 @@ t = tcg.translate(g, tcg.BlockConfig(), device="cuda")
 t.transpose()
 x = torch.from_numpy(x_np).cuda(); y = torch.from_numpy(lab_np).cuda()
 net = (layers.AGNN(128, 32, 40, layers=4) if kind == "agnn" else layers.GCN(128, 16, 40)).cuda()
-opt = torch.optim.Adam(net.parameters(), lr=0.01, capturable=True)
+opt = torch.optim.Adam(net.parameters(), lr=0.01, capturable=True, fused=True)
 def step():
-    opt.zero_grad(set_to_none=False)
+    opt.zero_grad(set_to_none=True)
     lo = layers.cross_entropy(net(x, t), y); lo.backward(); opt.step()
 for _ in range(3): step()
 torch.cuda.synchronize()
