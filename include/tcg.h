@@ -77,6 +77,36 @@ int64_t tcg_launch_count(void);
 /* Multiprocessor count / L2 bytes of the current device (0 if unavailable). */
 int tcg_device_info(int64_t* num_sms, int64_t* l2_bytes);
 
+/* ---- graph normalisation / invariants ---------- */
+/* Reference CsrGraph.from_edges (graph.py:55-89) on the device: sort the
+ * (src, dst) pairs by (row, column) with one stable radix sort, collapse
+ * duplicates, sum duplicate values (nullable) in input order in float64 and
+ * build node_ptr[N+1]. edge_list / edge_values need capacity num_edges; the
+ * surviving count is node_ptr[N]. Ids must lie in [0, N) for src and
+ * [0, 2^32) for dst; bad_ids (device i64) receives the number of pairs that
+ * do not (outputs are then unspecified). */
+size_t tcg_from_edges_workspace_bytes(int64_t num_edges);
+int tcg_from_edges(const int64_t* src, const int64_t* dst, const float* values,
+                   int64_t num_edges, int64_t num_nodes, int64_t* node_ptr,
+                   uint32_t* edge_list, float* edge_values, int64_t* bad_ids,
+                   void* workspace, size_t workspace_bytes, void* stream);
+/* Reference validate() (graph.py:92-142) counts on the device: report[6]
+ * (device u64) = first non-monotone row, #such rows, first out-of-range
+ * column, #such edges, first unsorted/duplicate column, #such edges (first =
+ * 2^64-1 when none). The caller formats the reference messages. Workspace:
+ * 48 bytes. */
+int tcg_validate(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_nodes,
+                 int64_t num_edges, int64_t* report, void* workspace, size_t workspace_bytes,
+                 void* stream);
+
+/* ---- tile accounting ---------------------------- */
+/* Reference structure_blocks_before (sgt.py:199-217), equal to
+ * count_blocks_before (sgt.py:140-157) on the same graph: per window the
+ * distinct col_to_node // tile_width buckets (per_window i64[W]) and their
+ * total (device i64). */
+int tcg_structure_blocks(const tcg_tiling* t, int64_t tile_width, int64_t* per_window,
+                         int64_t* total, void* stream);
+
 /* ---- SGT: reference sgt.translate (sgt.py:101-137) ---------------------- */
 /* Workspace bytes tcg_sgt needs for this graph size. */
 size_t tcg_sgt_workspace_bytes(int64_t num_nodes, int64_t num_edges, int32_t blk_h);

@@ -57,6 +57,10 @@ SIGNATURES = {
     "tcg_version": (C.c_char_p, []),
     "tcg_launch_count": (_I64, []),
     "tcg_device_info": (C.c_int, [C.POINTER(_I64), C.POINTER(_I64)]),
+    "tcg_from_edges_workspace_bytes": (_SZ, [_I64]),
+    "tcg_from_edges": (C.c_int, [_P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
+    "tcg_validate": (C.c_int, [_P, _P, _I64, _I64, _P, _P, _SZ, _P]),
+    "tcg_structure_blocks": (C.c_int, [C.POINTER(TcgTiling), _I64, _P, _P, _P]),
     "tcg_sgt_workspace_bytes": (_SZ, [_I64, _I64, _I32]),
     "tcg_sgt": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
     "tcg_edge_frag": (C.c_int, [C.POINTER(TcgTiling), _P, _P]),

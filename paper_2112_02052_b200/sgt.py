@@ -83,7 +83,9 @@ class TiledGraph:
 
     @property
     def num_unique(self) -> int:
-        return int(self.dev["num_unique"])
+        if "num_unique" in self.dev:
+            return int(self.dev["num_unique"])
+        return int(self.col_offsets[-1]) if self.num_row_windows else 0
 
     def unique_count(self, window: int) -> int:
         return int(self.col_offsets[window + 1] - self.col_offsets[window])
@@ -303,8 +305,13 @@ class _DeviceCsr(CsrGraph):
 # ---- tile accounting (sgt.py:140-217; reporting, host-side) -----------------
 
 
-def count_blocks_before(g: CsrGraph, cfg: BlockConfig) -> tuple[int, np.ndarray]:
-    """Occupied blk_w-wide original-column buckets per window (sgt.py:140-157)."""
+def count_blocks_before(g: CsrGraph, cfg: BlockConfig, device=None) -> tuple[int, np.ndarray]:
+    """Occupied blk_w-wide original-column buckets per window (sgt.py:140-157).
+    With `device` it is the GPU structure count on the (GPU) SGT of g — the
+    condensed columns keep each window's distinct neighbour set."""
+    if device is not None:
+        t = translate(g, cfg, device)
+        return structure_blocks_device(t, cfg.blk_w)
     n, bh, bw = g.num_nodes, cfg.blk_h, cfg.blk_w
     W = -(-n // bh)
     if g.num_edges == 0:
@@ -313,6 +320,43 @@ def count_blocks_before(g: CsrGraph, cfg: BlockConfig) -> tuple[int, np.ndarray]
     nb = -(-n // bw)
     uniq = np.unique(win * nb + g.edge_list.astype(np.int64) // bw)
     return int(uniq.shape[0]), np.bincount(uniq // nb, minlength=W)
+
+
+def structure_blocks_device(t: TiledGraph, tile_width: int) -> tuple[int, np.ndarray]:
+    """(total, per-window) distinct col_to_node // tile_width buckets on the
+    GPU (tcg_structure_blocks)."""
+    import torch
+
+    if tile_width < 1:
+        raise ValueError("tile_width must be >= 1")
+    W = t.num_row_windows
+    dev = t.dev["col_offsets"].device
+    per = torch.zeros(max(W, 1), dtype=torch.int64, device=dev)
+    tot = torch.zeros(1, dtype=torch.int64, device=dev)
+    s = _lib.TcgTiling(t.num_nodes, t.num_edges, W, t.num_unique, t.config.blk_h, t.config.blk_w,
+                       None, None, None, t.dev["col_offsets"].data_ptr(),
+                       t.dev["col_to_node"].data_ptr() if t.num_unique else None,
+                       None, None, 0, 0, None, None)
+    _lib.check(_lib.load().tcg_structure_blocks(C.byref(s), int(tile_width), per.data_ptr(),
+                                                tot.data_ptr(), _stream_ptr()),
+               "tcg_structure_blocks")
+    return int(tot.item()), per[:W].cpu().numpy()
+
+
+def structure_blocks_before(t: TiledGraph, tile_width: int) -> int:
+    """Occupied original-column buckets per window from the tiling structure
+    alone (sgt.py:199-217); equals count_blocks_before on the source graph.
+    Device-resident tilings count on the GPU."""
+    if tile_width < 1:
+        raise ValueError("tile_width must be >= 1")
+    if t.dev:
+        return structure_blocks_device(t, tile_width)[0]
+    c2n = t.col_to_node
+    if c2n.size == 0:
+        return 0
+    win = np.repeat(np.arange(t.num_row_windows, dtype=np.int64), np.diff(t.col_offsets))
+    nb = -(-t.num_nodes // tile_width)
+    return int(np.unique(win * nb + c2n.astype(np.int64) // tile_width).shape[0])
 
 
 def count_blocks_after(t: TiledGraph) -> int:
