@@ -178,6 +178,20 @@ def cpu_epoch_runner(wl):
     return step, workers, g
 
 
+def arm_config(workload: str, world: int, n: int, m: int) -> dict:
+    """The workload description both arms print (same dict for the same N)."""
+    shape, model_kind, feats, hidden, classes, nlayers = WORKLOADS[workload]
+    return {
+        "workload": f"{workload}: {model_kind.upper()}-{nlayers} hidden {hidden} "
+                    f"full-batch train epoch (fwd+bwd+Adam), TF32 sparse ops, fp32 GEMMs",
+        "graph": f"synthetic {shape}-shaped", "nodes": n, "edges": m,
+        "features": feats, "classes": classes, "blk": "16x8",
+        "parallelism": f"row-window shards x{world}" if world > 1 else "single GPU",
+        "l2": "flushed between timed steps (write of 2x L2)",
+        "cuda_graph": world == 1,
+    }
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -207,8 +221,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms/epoch",
         "n_gpus": args.gpus, "steps": len(times), "warmup": 1, "ms_per_step": round(ms, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "tf32",
-        "data": "synthetic", "config": {"workload": args.workload, "graph": f"gen_uniform {shape}",
-                                         "nodes": g.num_nodes, "edges": g.num_edges},
+        "data": "synthetic (gen_uniform seed 1, N(0,1) features seed 2)",
+        "config": arm_config(args.workload, args.gpus, g.num_nodes, g.num_edges),
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms/epoch", "cores": workers,
                          "kind": "port", "sample": sample},
         "e2e": {"value": round(ms, 3), "unit": "ms/epoch", "h2d_bytes_per_step": 0,
@@ -445,7 +459,32 @@ def run_ours(args):
                     "peak_kind": peak_kind, "kernel": f"spmm_tc weighted D={d} ({shape})",
                     "algorithmic_bytes": b_spmm, "launch_us": round(t_spmm * 1e3, 2),
                     "l2": "cold (flushed before each launch)"}
+        # 8(f) rows: graph normalisation / invariant check / tile accounting on the device
+        gen = torch.Generator(device=dev).manual_seed(1)
+        src_r = torch.randint(0, n, (m,), device=dev, generator=gen)
+        dst_r = torch.randint(0, n, (m,), device=dev, generator=gen)
+
+        def timed(fn, reps=5):
+            ts = []
+            for _ in range(reps):
+                torch.cuda.synchronize()
+                s, e = ev(), ev()
+                s.record()
+                fn()
+                e.record()
+                e.synchronize()
+                ts.append(s.elapsed_time(e))
+            return statistics.median(ts[1:])
+
+        t_fe = timed(lambda: tcg.CsrGraph.from_edges(src_r, dst_r, n))
+        g_dev = tcg.CsrGraph.from_edges(src_r, dst_r, n)
+        t_val = timed(lambda: tcg.validate(g_dev))
+        t_blk = timed(lambda: tcg.structure_blocks_before(t, 8))
+        del src_r, dst_r, g_dev
         extras = {
+            "from_edges_ms": round(t_fe, 3),
+            "validate_ms": round(t_val, 3),
+            "structure_blocks_ms": round(t_blk, 3),
             "sgt_ms": round(sgt_ms, 4),
             "sgt_gbs": round(b_sgt / (sgt_ms * 1e-3) / 1e9, 1),
             "spmm_tc_us_cold": round(t_spmm * 1e3, 2),
@@ -499,17 +538,9 @@ def run_ours(args):
             "metric": METRIC, "value": round(ms_per_step, 4), "unit": "ms/epoch",
             "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
             "ms_per_step": round(ms_per_step, 4), "higher_is_better": False,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "scaling": "strong", "vs_baseline": None,
             "dtype": "tf32", "data": "synthetic (gen_uniform seed 1, N(0,1) features seed 2)",
-            "config": {
-                "workload": f"{args.workload}: {model_kind.upper()}-{nlayers} hidden {hidden} "
-                            f"full-batch train epoch (fwd+bwd+Adam), TF32 sparse ops, fp32 GEMMs",
-                "graph": f"synthetic {shape}-shaped", "nodes": n, "edges": m,
-                "features": feats, "classes": classes, "blk": "16x8",
-                "parallelism": f"row-window shards x{world}" if world > 1 else "single GPU",
-                "l2": "flushed between timed steps (write of 2x L2)",
-                "cuda_graph": bool(graph is not None),
-            },
+            "config": arm_config(args.workload, world, n, m),
             "clocks": clocks.summary(t_wall0, t_wall1),
             "e2e": {"value": round(e2e_ms_step, 4), "unit": "ms/epoch",
                     "h2d_bytes_per_step": int(x_np.nbytes + labels_np.astype(np.int64).nbytes),
