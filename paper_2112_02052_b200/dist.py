@@ -78,16 +78,28 @@ def make_shard_plan(node_pointer: np.ndarray, num_nodes: int, blk_h: int, wp_a: 
     return ShardPlan(rank, world, wins, rows, edges, blk_h)
 
 
+def _all_gather(buf, local, group):
+    """all_gather_into_tensor over NCCL; other backends (gloo, used by the
+    1-GPU functional tests) stage device tensors through the host."""
+    import torch.distributed as dist
+
+    if local.is_cuda and dist.get_backend(group) != "nccl":
+        hb = buf.cpu()
+        dist.all_gather_into_tensor(hb, local.cpu(), group=group)
+        buf.copy_(hb)
+    else:
+        dist.all_gather_into_tensor(buf, local, group=group)
+
+
 def allgather_rows(local_slab, plan: ShardPlan, group=None):
     """local_slab: [rows_max, D] (rank's rows at the top). Returns the full
     [N, D] matrix assembled from every rank's slab."""
     import torch
-    import torch.distributed as dist
 
     D = local_slab.shape[1]
     buf = torch.empty((plan.world * plan.rows_max, D), dtype=local_slab.dtype,
                       device=local_slab.device)
-    dist.all_gather_into_tensor(buf, local_slab.contiguous(), group=group)
+    _all_gather(buf, local_slab.contiguous(), group)
     parts = [buf[r * plan.rows_max: r * plan.rows_max + (r1 - r0)]
              for r, (r0, r1) in enumerate(plan.rows)]
     return torch.cat(parts, 0)
@@ -96,10 +108,9 @@ def allgather_rows(local_slab, plan: ShardPlan, group=None):
 def allgather_edges(local_vec, plan: ShardPlan, group=None):
     """local_vec: [edges_max] (rank's edges first). Returns the full [M]."""
     import torch
-    import torch.distributed as dist
 
     buf = torch.empty(plan.world * plan.edges_max, dtype=local_vec.dtype, device=local_vec.device)
-    dist.all_gather_into_tensor(buf, local_vec.contiguous(), group=group)
+    _all_gather(buf, local_vec.contiguous(), group)
     parts = [buf[r * plan.edges_max: r * plan.edges_max + (e1 - e0)]
              for r, (e0, e1) in enumerate(plan.edges)]
     return torch.cat(parts, 0)
