@@ -118,7 +118,7 @@ struct Cfg {
   static constexpr int OPS = DUAL ? 2 : 1;
   static constexpr int MB = DUAL ? 8 : 16;         // A-fragment blocks resident (one round)
   static constexpr int RING = NB * SLOT * OPS;
-  static constexpr int IDX = NI * 32;
+  static constexpr int IDX = NI * 256;             // per-lane copies of the column ids
   static constexpr int AFR = MB * 512 * OPS;
   static constexpr int WARP = RING + IDX + AFR;
   static constexpr int WPC = DUAL ? 4 : 8;         // warps per CTA
@@ -174,32 +174,35 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Arg
   const int d0 = a.d0 + blockIdx.y * 8 * NT;
   const char* xb = reinterpret_cast<const char*>(a.x + d0 + g * NT);
   const char* xb2 = DUAL ? reinterpret_cast<const char*>(a.x2 + d0 + g * NT) : nullptr;
-  const uint64_t xrow = (uint64_t)a.ldx * 4, xrow2 = (uint64_t)a.ldx2 * 4;
-  const uint32_t so0 = slot_off<NT>(t, g), so1 = slot_off<NT>(t + 4, g);
-  const uint32_t* csw = a.cs + 8 * (int64_t)gb0;
-
-  auto issue_idx = [&](int s) {
-    if (lane < 2) cp_async<16>(iring + (s & (NI - 1)) * 32 + lane * 16, csw + 8 * (int64_t)s + 4 * lane);
-  };
-  auto issue_x = [&](int s) {
-    const uint2 id = *reinterpret_cast<const uint2*>(iring_p + (s & (NI - 1)) * 32 + 8 * t);
-    const uint32_t sb = ring + (s & (NB - 1)) * SLOT * C::OPS;
-    cp_async<CP>(sb + so0, xb + id.x * xrow);
-    cp_async<CP>(sb + so1, xb + id.y * xrow);
+  const uint32_t xrow = (uint32_t)a.ldx * 4u, xrow2 = (uint32_t)a.ldx2 * 4u;
+  // per-lane ring addresses: X slot s at xs + (s % NB) * SLOT * OPS (rows t / t+4 at
+  // +0 / +d1), this lane's column-id pair of block s at is + (s % NI) * 256
+  const uint32_t xs = ring + slot_off<NT>(t, g);
+  const uint32_t d1 = slot_off<NT>(t + 4, g) - slot_off<NT>(t, g);
+  const uint32_t is = iring + lane * 8;
+  // each lane copies its own (c_t, c_t+4) pair of every block: no cross-lane
+  // visibility, so the stream loop needs no warp barrier
+  const char* csl = reinterpret_cast<const char*>(a.cs + 8 * (int64_t)gb0 + 2 * t);
+  auto issue_x = [&](uint32_t xo, uint32_t io) {
+    const uint2 id = *reinterpret_cast<const uint2*>(iring_p + lane * 8 + io);
+    cp_async<CP>(xs + xo, xb + (uint64_t)id.x * xrow);
+    cp_async<CP>(xs + xo + d1, xb + (uint64_t)id.y * xrow);
     if constexpr (DUAL) {
-      cp_async<CP>(sb + SLOT + so0, xb2 + id.x * xrow2);
-      cp_async<CP>(sb + SLOT + so1, xb2 + id.y * xrow2);
+      cp_async<CP>(xs + xo + SLOT, xb2 + (uint64_t)id.x * xrow2);
+      cp_async<CP>(xs + xo + SLOT + d1, xb2 + (uint64_t)id.y * xrow2);
     }
   };
-  for (int s = 0; s < NB; ++s) issue_idx(s);
+  for (int s = 0; s < NB; ++s) cp_async<8>(is + s * 256, csl + 32 * s);
   cp_commit();
   cp_wait<0>();
-  __syncwarp();
   for (int s = 0; s < NB; ++s) {
-    issue_x(s);
-    issue_idx(s + NB);
+    issue_x(s * SLOT * C::OPS, s * 256);
+    cp_async<8>(is + (s + NB) * 256, csl + 32 * (s + NB));
     cp_commit();
   }
+  // ring cursors of the consumed block s: X slot, id slot of s + NB, id slot of s + 2NB
+  uint32_t xo = 0, io = NB * 256, iw = 0;
+  const char* cnext = csl + 32 * 2 * NB;
 
   // ---- window metadata, rolled 3 windows ahead ----
   auto ptr_of = [&](int w) { return (int64_t)__ldg(a.ptr + min((int64_t)w * 16, a.n)); };
@@ -284,7 +287,6 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Arg
     }
   };
 
-  int s = 0;
   for (int w = ws; w < we; ++w) {
     const int nbw = cb1 - cb0;
     const bool hub = e1 - e0 > 32 * kEPL;
@@ -303,44 +305,49 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Arg
     prefetch(e1, e2);
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-    for (int lb = 0; lb < nbw; ++lb, ++s) {
-      if (lb >= MB && (lb & (MB - 1)) == 0) {  // next round of fragment blocks
+    for (int r0 = 0; r0 < nbw; r0 += MB) {
+      if (r0 > 0) {  // next round of fragment blocks
         if (!hub) {
           __syncwarp();
-          put_round((uint32_t)(lb - MB) * 128, true);
+          put_round((uint32_t)(r0 - MB) * 128, true);
           __syncwarp();
-          put_round((uint32_t)lb * 128, false);
+          put_round((uint32_t)r0 * 128, false);
           __syncwarp();
         } else {
-          hub_load(lb);
+          hub_load(r0);
         }
       }
-      cp_wait<NB - 1>();
-      __syncwarp();
-      const uint32_t sb = ring + (s & (NB - 1)) * SLOT * C::OPS;
-      const uint32_t fa = as + (lb & (MB - 1)) * 512;
-      {
-        float x0[NT], x1[NT];
-        lds_slice<NT>(x0, sb + so0);
-        lds_slice<NT>(x1, sb + so1);
-        const uint4 af = lds_frag(fa);
+      const int rend = min(nbw, r0 + MB);
+      uint32_t fa = as;
+      for (int lb = r0; lb < rend; ++lb, fa += 512) {
+        cp_wait<NB - 1>();
+        {
+          float x0[NT], x1[NT];
+          lds_slice<NT>(x0, xs + xo);
+          lds_slice<NT>(x1, xs + xo + d1);
+          const uint4 af = lds_frag(fa);
 #pragma unroll
-        for (int j = 0; j < NT; ++j)
-          mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
-      }
-      if constexpr (DUAL) {
-        float x0[NT], x1[NT];
-        lds_slice<NT>(x0, sb + SLOT + so0);
-        lds_slice<NT>(x1, sb + SLOT + so1);
-        const uint4 af = lds_frag(fa + MB * 512);
+          for (int j = 0; j < NT; ++j)
+            mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
+        }
+        if constexpr (DUAL) {
+          float x0[NT], x1[NT];
+          lds_slice<NT>(x0, xs + xo + SLOT);
+          lds_slice<NT>(x1, xs + xo + SLOT + d1);
+          const uint4 af = lds_frag(fa + MB * 512);
 #pragma unroll
-        for (int j = 0; j < NT; ++j)
-          mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
+          for (int j = 0; j < NT; ++j)
+            mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
+        }
+        // refill: X of block s + NB into this slot, ids of block s + 2NB
+        issue_x(xo, io);
+        cp_async<8>(is + iw, cnext);
+        cp_commit();
+        cnext += 32;
+        xo = (xo + SLOT * C::OPS) & (NB * SLOT * C::OPS - 1);
+        io = (io + 256) & (NI * 256 - 1);
+        iw = (iw + 256) & (NI * 256 - 1);
       }
-      __syncwarp();
-      issue_x(s + NB);
-      issue_idx(s + 2 * NB);
-      cp_commit();
     }
     store(w);
     // un-scatter this window's last round
