@@ -69,6 +69,20 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// Same mma with the B operands rounded in the same asm block (cvt.rn.tf32 of
+// two fp32 values straight into the HMMA register pair: no operand moves).
+__device__ __forceinline__ void mma_tf32_rb(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                            uint32_t a3, float b0, float b1) {
+  asm volatile(
+      "{\n.reg .b32 tb0, tb1;\n"
+      "cvt.rn.tf32.f32 tb0, %8;\n"
+      "cvt.rn.tf32.f32 tb1, %9;\n"
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {tb0,tb1}, {%0,%1,%2,%3};\n}\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "f"(b0), "f"(b1));
+}
+
 template <typename T>
 __device__ __forceinline__ T ldg_stream(const T* p) {
   return __ldg(p);

@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Arg
           const uint4 af = lds_frag(fa);
 #pragma unroll
           for (int j = 0; j < NT; ++j)
-            mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
+            mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
         }
         if constexpr (DUAL) {
           float x0[NT], x1[NT];
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Arg
           const uint4 af = lds_frag(fa + MB * 512);
 #pragma unroll
           for (int j = 0; j < NT; ++j)
-            mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
+            mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
         }
         // refill: X of block s + NB into this slot, ids of block s + 2NB
         issue_x(xo, io);
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 2) agnn_stream(const A
         lds_slice<4>(b1, sb + sd1);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          mma_tf32(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], tf32_rn(b0[j]), tf32_rn(b1[j]));
+          mma_tf32_rb(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], b0[j], b1[j]);
       }
       // C (g, 2t) <-> A (g, t); C (g, 2t+1) <-> A (g, t+4): A slots are
       // (0: (g,t), 1: (g+8,t), 2: (g,t+4), 3: (g+8,t+4)); C regs are
@@ -606,9 +606,17 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 2) agnn_stream(const A
           bm[rh] = fmaxf(bm[rh], __shfl_xor_sync(0xffffffffu, bm[rh], 1));
           bm[rh] = fmaxf(bm[rh], __shfl_xor_sync(0xffffffffu, bm[rh], 2));
         }
-        // lazy rescale: the running max only moves when a score exceeds it by
-        // kTau (exp(s - m) stays <= e^kTau); P uses the same stale max, so the
-        // result is unchanged
+        // first scores of a row just set its max (acc and l are still zero);
+        // after that the running max only moves when a score exceeds it by kTau
+        // (lazy rescale: exp(s - m) stays <= e^kTau, and P uses the same stale
+        // max, so the result is unchanged)
+#pragma unroll
+        for (int rh = 0; rh < 2; ++rh) {
+          if (mrow[rh] == -INFINITY) {
+            mrow[rh] = bm[rh];
+            ml2[rh] = bm[rh] * kLog2e;
+          }
+        }
         if (__any_sync(0xffffffffu, bm[0] > mrow[0] + kTau || bm[1] > mrow[1] + kTau)) {
 #pragma unroll
           for (int rh = 0; rh < 2; ++rh) {
@@ -649,7 +657,7 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 2) agnn_stream(const A
         lds_slice<4>(x1, sb + so1);
         const uint32_t a0 = tf32_rn(av[0]), a1 = tf32_rn(av[1]), a2 = tf32_rn(av[2]), a3 = tf32_rn(av[3]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) mma_tf32(acc[j], a0, a1, a2, a3, tf32_rn(x0[j]), tf32_rn(x1[j]));
+        for (int j = 0; j < 4; ++j) mma_tf32_rb(acc[j], a0, a1, a2, a3, x0[j], x1[j]);
       }
       __syncwarp();
       issue_x(s + NB);
