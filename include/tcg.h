@@ -138,6 +138,10 @@ int tcg_block_stream(const tcg_tiling* t, int32_t* block_offsets, uint32_t* col_
  * A^T edge order once per backward, so the A^T SpMM reads them coalesced. */
 int tcg_permute_f32(const float* src, const uint32_t* idx, float* dst, int64_t n, void* stream);
 
+/* dst[idx[k]] = src[k] (the inverse move of tcg_permute_f32). */
+int tcg_scatter_f32(const float* src, const uint32_t* idx, float* dst, int64_t n, void* stream);
+/* inv[perm[k]] = k: for A^T's perm, inv[e] is the A^T position of A's edge e. */
+int tcg_invert_perm(const uint32_t* perm, int64_t n, uint32_t* inv, void* stream);
 /* ---- CSR transpose (backward support; no reference counterpart — the
  * reference has no backward. SURVEY.md Appendix B restates it as
  * CsrGraph.from_edges(dst, src), graph.py:55-89) ------------------------ */
@@ -210,8 +214,17 @@ int tcg_agnn_backward(const tcg_tiling* t, const float* z, int64_t ldz, const fl
  * tcg_agnn_backward where the block-stream engine does not apply. */
 int tcg_agnn_backward_fused(const tcg_tiling* t, const float* z, int64_t ldz, const float* gy,
                             int64_t ldg, const float* y_fwd, int64_t ld_yfwd, int64_t dim,
-                            const float* p, float* ds, float* dz, int64_t lddz, int64_t dz_row0,
-                            int64_t win_begin, int64_t win_end, void* stream);
+                            const float* p, float* ds, float* ds_t, const uint32_t* inv_perm,
+                            float* dz, int64_t lddz, int64_t dz_row0, int64_t win_begin,
+                            int64_t win_end, void* stream);
+/* tcg_agnn_forward followed by P in A^T edge order (p_t[inv_perm[e]] = p[e];
+ * inv_perm from tcg_invert_perm of the transpose's perm), for the backward's
+ * A^T SpMM. tcg_agnn_backward_fused does the same for dS when ds_t is given.
+ * (Writing the A^T copy from the kernel epilogue was measured slower than
+ * this separate coalesced-read scatter.) */
+int tcg_agnn_forward_t(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim, float* p,
+                       float* p_t, const uint32_t* inv_perm, float* y, int64_t ldy,
+                       int64_t y_row0, int64_t win_begin, int64_t win_end, void* stream);
 /* ---- dense companions of the layers (fp32; no reference counterpart beyond
  * gcn_layer's `agg @ w + b`, kernels.py:577-582) ---------------------------- */
 /* y[n x co] = act((x .* [mask > 0]) . M + bias) (mask: [n x ci]); M is [ci x co]

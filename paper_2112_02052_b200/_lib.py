@@ -79,7 +79,11 @@ SIGNATURES = {
     "tcg_agnn_backward": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _P, _I64, _I64, _P, _P,
                                     _P, _I64, _I64, _I64, _I64, _P]),
     "tcg_agnn_backward_fused": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _P, _I64, _P, _I64,
-                                          _I64, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
+                                          _I64, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
+    "tcg_agnn_forward_t": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _I64, _P, _P, _P, _P, _I64,
+                                     _I64, _I64, _I64, _P]),
+    "tcg_scatter_f32": (C.c_int, [_P, _P, _P, _I64, _P]),
+    "tcg_invert_perm": (C.c_int, [_P, _I64, _P, _P]),
     "tcg_quantize_tf32": (C.c_int, [_P, _P, _I64, _P]),
     "tcg_dense": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _I32, _P, _I32, _P, _I64, _P, _I64,
                             _P]),

@@ -207,6 +207,29 @@ extern "C" int tcg_permute_f32(const float* src, const uint32_t* idx, float* dst
   return TCG_OK;
 }
 
+namespace tcg {
+namespace {
+__global__ void scatter_f32(const float* __restrict__ src, const uint32_t* __restrict__ idx,
+                            float* __restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[idx[i]] = src[i];
+}
+}  // namespace
+}  // namespace tcg
+
+extern "C" int tcg_scatter_f32(const float* src, const uint32_t* idx, float* dst, int64_t n,
+                               void* stream) {
+  TCG_REQUIRE(n >= 0, "tcg_scatter_f32: negative size");
+  if (n == 0) return TCG_OK;
+  TCG_REQUIRE(src && idx && dst, "tcg_scatter_f32: null pointer");
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  tcg::scatter_f32<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(src, idx, dst, n);
+  TCG_LAUNCHED("scatter_f32");
+  return TCG_OK;
+}
+
 extern "C" size_t tcg_csr_transpose_workspace_bytes(int64_t num_nodes, int64_t num_edges) {
   if (num_nodes < 0 || num_edges < 0) return 0;
   return tr_layout(num_nodes, num_edges).total;

@@ -221,9 +221,19 @@ extern "C" int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz
   return win::launch(win::MODE_AGNN_FWD, nt, q, as_stream(stream));
 }
 
+extern "C" int tcg_agnn_forward_t(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim,
+                                  float* p, float* p_t, const uint32_t* inv_perm, float* y,
+                                  int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
+                                  void* stream) {
+  const int rc = tcg_agnn_forward(t, z, ldz, dim, p, y, ldy, y_row0, win_begin, win_end, stream);
+  if (rc != TCG_OK || !p_t || !inv_perm || !t || t->num_edges == 0) return rc;
+  return tcg_scatter_f32(p, inv_perm, p_t, t->num_edges, stream);
+}
+
 extern "C" int tcg_agnn_backward_fused(const tcg_tiling* t, const float* z, int64_t ldz,
                                        const float* gy, int64_t ldg, const float* y_fwd,
                                        int64_t ld_yfwd, int64_t dim, const float* p, float* ds,
+                                       float* ds_t, const uint32_t* inv_perm,
                                        float* dz, int64_t lddz, int64_t dz_row0,
                                        int64_t win_begin, int64_t win_end, void* stream) {
   TCG_REQUIRE(t != nullptr && dim >= 1 && ldz >= dim && ldg >= dim && lddz >= dim &&
@@ -239,10 +249,15 @@ extern "C" int tcg_agnn_backward_fused(const tcg_tiling* t, const float* z, int6
     TCG_REQUIRE(z && gy && y_fwd && p && ds && dz, "tcg_agnn_backward_fused: null pointer");
     const int rc = stream_agnn(t, true, z, ldz, gy, ldg, y_fwd, ld_yfwd, p, ds, dz, lddz, dz_row0,
                                win_begin, win_end, as_stream(stream));
-    if (rc != TCG_E_UNSUPPORTED) return rc;
+    if (rc != TCG_E_UNSUPPORTED) {
+      if (rc != TCG_OK || !ds_t || !inv_perm) return rc;
+      return tcg_scatter_f32(ds, inv_perm, ds_t, t->num_edges, stream);
+    }
   }
-  return tcg_agnn_backward(t, z, ldz, gy, ldg, dim, p, ds, dz, lddz, dz_row0, win_begin, win_end,
-                           stream);
+  const int rc = tcg_agnn_backward(t, z, ldz, gy, ldg, dim, p, ds, dz, lddz, dz_row0, win_begin,
+                                   win_end, stream);
+  if (rc != TCG_OK || !ds_t || !inv_perm || t->num_edges == 0) return rc;
+  return tcg_scatter_f32(ds, inv_perm, ds_t, t->num_edges, stream);
 }
 
 extern "C" int tcg_agnn_backward(const tcg_tiling* t, const float* z, int64_t ldz,

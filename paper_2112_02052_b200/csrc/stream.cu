@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Arg
           const uint4 af = lds_frag(fa);
 #pragma unroll
           for (int j = 0; j < NT; ++j)
-            mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
+            mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
         }
         if constexpr (DUAL) {
           float x0[NT], x1[NT];
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Arg
           const uint4 af = lds_frag(fa + MB * 512);
 #pragma unroll
           for (int j = 0; j < NT; ++j)
-            mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
+            mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
         }
         // refill: X of block s + NB into this slot, ids of block s + 2NB
         issue_x(xo, io);
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 2) agnn_stream(const A
         lds_slice<4>(b1, sb + sd1);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          mma_tf32_rb(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], b0[j], b1[j]);
+          mma_tf32(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], tf32_rn(b0[j]), tf32_rn(b1[j]));
       }
       // C (g, 2t) <-> A (g, t); C (g, 2t+1) <-> A (g, t+4): A slots are
       // (0: (g,t), 1: (g+8,t), 2: (g,t+4), 3: (g+8,t+4)); C regs are
@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 2) agnn_stream(const A
         lds_slice<4>(x1, sb + so1);
         const uint32_t a0 = tf32_rn(av[0]), a1 = tf32_rn(av[1]), a2 = tf32_rn(av[2]), a3 = tf32_rn(av[3]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) mma_tf32_rb(acc[j], a0, a1, a2, a3, x0[j], x1[j]);
+        for (int j = 0; j < 4; ++j) mma_tf32(acc[j], a0, a1, a2, a3, tf32_rn(x0[j]), tf32_rn(x1[j]));
       }
       __syncwarp();
       issue_x(s + NB);
@@ -877,6 +877,24 @@ int stream_agnn(const tcg_tiling* t, bool bwd, const float* z, int64_t ldz, cons
 }  // namespace tcg
 
 using namespace tcg;
+
+namespace tcg {
+namespace {
+__global__ void invert_perm_kernel(const uint32_t* __restrict__ perm, int64_t m, uint32_t* inv) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < m) inv[perm[k]] = (uint32_t)k;
+}
+}  // namespace
+}  // namespace tcg
+
+extern "C" int tcg_invert_perm(const uint32_t* perm, int64_t n, uint32_t* inv, void* stream) {
+  TCG_REQUIRE(n >= 0, "tcg_invert_perm: negative size");
+  if (n == 0) return TCG_OK;
+  TCG_REQUIRE(perm && inv, "tcg_invert_perm: null pointer");
+  tcg::invert_perm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(perm, n, inv);
+  TCG_LAUNCHED("invert_perm");
+  return TCG_OK;
+}
 
 extern "C" int tcg_block_stream(const tcg_tiling* t, int32_t* block_offsets,
                                 uint32_t* col_stream, void* stream) {

@@ -272,6 +272,16 @@ def sddmm_device(t: TiledGraph, xa, xb=None, *, mode="tf32", epilogue=_lib.EPI_N
     return out
 
 
+def invert_perm_device(perm):
+    """inv[perm[k]] = k (tcg_invert_perm)."""
+    import torch
+
+    inv = torch.empty_like(perm)
+    _lib.check(_lib.load().tcg_invert_perm(perm.data_ptr(), perm.shape[0], inv.data_ptr(),
+                                           _stream()), "tcg_invert_perm")
+    return inv
+
+
 def permute_device(src, idx, out=None):
     """out[k] = src[idx[k]] (tcg_permute_f32)."""
     import torch
@@ -284,8 +294,10 @@ def permute_device(src, idx, out=None):
     return out
 
 
-def agnn_forward_device(t: TiledGraph, z, *, p=None, out=None, win_range=None, y_row0=0):
-    """Fused TF32 AGNN aggregation (tcg_agnn_forward): returns (Y, P)."""
+def agnn_forward_device(t: TiledGraph, z, *, p=None, out=None, win_range=None, y_row0=0,
+                        p_t=None, inv_perm=None):
+    """Fused TF32 AGNN aggregation (tcg_agnn_forward): returns (Y, P). With
+    `p_t` / `inv_perm` P is also written in A^T edge order (tcg_agnn_forward_t)."""
     import torch
 
     lib = _lib.load()
@@ -295,6 +307,12 @@ def agnn_forward_device(t: TiledGraph, z, *, p=None, out=None, win_range=None, y
     if out is None:
         out = torch.empty((t.num_nodes, z.shape[1]), dtype=torch.float32, device=z.device)
         y_row0 = 0
+    if p_t is not None:
+        _lib.check(lib.tcg_agnn_forward_t(C.byref(t.abi()), z.data_ptr(), z.stride(0), z.shape[1],
+                                          p.data_ptr(), p_t.data_ptr(), inv_perm.data_ptr(),
+                                          out.data_ptr(), out.stride(0), y_row0, wb, we,
+                                          _stream()), "tcg_agnn_forward_t")
+        return out, p
     _lib.check(lib.tcg_agnn_forward(C.byref(t.abi()), z.data_ptr(), z.stride(0), z.shape[1],
                                     p.data_ptr(), out.data_ptr(), out.stride(0), y_row0, wb, we,
                                     _stream()), "tcg_agnn_forward")
@@ -302,7 +320,7 @@ def agnn_forward_device(t: TiledGraph, z, *, p=None, out=None, win_range=None, y
 
 
 def agnn_backward_device(t: TiledGraph, z, gy, p, *, ds=None, out=None, win_range=None,
-                         y_row0=0, y_fwd=None):
+                         y_row0=0, y_fwd=None, ds_t=None, inv_perm=None):
     """A-side half of the AGNN backward (tcg_agnn_backward): returns (dZ_A, dS)
     with dS = P (dP - rowsum(P dP)), dP = <G_i, Z_j>, dZ_A = A_dS Z. With the
     forward output `y_fwd` the one-pass form (tcg_agnn_backward_fused,
@@ -320,6 +338,8 @@ def agnn_backward_device(t: TiledGraph, z, gy, p, *, ds=None, out=None, win_rang
         _lib.check(lib.tcg_agnn_backward_fused(
             C.byref(t.abi()), z.data_ptr(), z.stride(0), gy.data_ptr(), gy.stride(0),
             y_fwd.data_ptr(), y_fwd.stride(0), z.shape[1], p.data_ptr(), ds.data_ptr(),
+            ds_t.data_ptr() if ds_t is not None else None,
+            inv_perm.data_ptr() if ds_t is not None else None,
             out.data_ptr(), out.stride(0), y_row0, wb, we, _stream()), "tcg_agnn_backward_fused")
         return out, ds
     _lib.check(lib.tcg_agnn_backward(C.byref(t.abi()), z.data_ptr(), z.stride(0), gy.data_ptr(),

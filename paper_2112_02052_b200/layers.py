@@ -35,6 +35,7 @@ from .dense import DenseFn, Linear, cross_entropy  # noqa: F401  (re-exported)
 from .kernels import (
     agnn_backward_device,
     agnn_forward_device,
+    invert_perm_device,
     permute_device,
     sddmm_device,
     spmm_device,
@@ -95,6 +96,22 @@ class GcnAggregate(torch.autograd.Function):
 _PERMUTE_WEIGHTS = os.environ.get("TCG_GATHER_WEIGHTS") is None
 
 
+# P / dS in A^T edge order: by default a gather (tcg_permute_f32) in the
+# backward; TCG_FUSED_PT=1 switches to scatters right after the producing
+# kernels (tcg_agnn_forward_t / ds_t). Writing them from the kernel epilogues
+# was measured slower (1.22 vs 1.15 ms / epoch) and is not offered.
+_FUSED_PT = os.environ.get("TCG_FUSED_PT") is not None
+
+
+def _inv_perm(t: TiledGraph):
+    """A^T position of every A edge (cached per tiling)."""
+    inv = t._aux.get("inv_perm")
+    if inv is None:
+        inv = invert_perm_device(t.transpose().perm)
+        t._aux["inv_perm"] = inv
+    return inv
+
+
 class AgnnAggregate(torch.autograd.Function):
     """Y = spmm(A, P; Z), P = rowsoftmax(sddmm(Z, Z))."""
 
@@ -104,7 +121,12 @@ class AgnnAggregate(torch.autograd.Function):
         m = t.num_edges
         p = torch.empty(max(m, 1), dtype=torch.float32, device=z.device)
         out, r0, wr = _rows_out(t, z.shape[1], z, shard)
-        if mode == "tf32":
+        p_t = None
+        if mode == "tf32" and shard is None and m and _FUSED_PT:
+            # P also written in A^T edge order by the same epilogue (no permute pass)
+            p_t = torch.empty(m, dtype=torch.float32, device=z.device)
+            agnn_forward_device(t, z, p=p, out=out, p_t=p_t, inv_perm=_inv_perm(t))
+        elif mode == "tf32":
             agnn_forward_device(t, z, p=p, out=out, win_range=wr, y_row0=r0)
         else:
             if m:
@@ -116,13 +138,13 @@ class AgnnAggregate(torch.autograd.Function):
             loc[: e1 - e0] = p[e0:e1]
             p = allgather_edges(loc, shard)
         y = _finish_rows(out, shard)
-        ctx.save_for_backward(z, p, y if mode == "tf32" else None)
+        ctx.save_for_backward(z, p, y if mode == "tf32" else None, p_t)
         ctx.t, ctx.mode, ctx.shard = t, mode, shard
         return y
 
     @staticmethod
     def backward(ctx, g):
-        z, p, y_fwd = ctx.saved_tensors
+        z, p, y_fwd, p_t = ctx.saved_tensors
         t, mode, shard = ctx.t, ctx.mode, ctx.shard
         g = g.contiguous()
         m = t.num_edges
@@ -131,10 +153,12 @@ class AgnnAggregate(torch.autograd.Function):
             out.zero_()
             return _finish_rows(out, shard), None, None, None
         ds = torch.empty(m, dtype=torch.float32, device=z.device)
+        ds_t = torch.empty(m, dtype=torch.float32, device=z.device) if p_t is not None else None
         if mode == "tf32":
-            # dS and A_dS Z from one gather of Z's neighbour rows
+            # dS and A_dS Z from one gather of Z's neighbour rows (dS also in A^T order)
             agnn_backward_device(t, z, g, p, ds=ds, out=out, win_range=wr, y_row0=r0,
-                                 y_fwd=y_fwd)
+                                 y_fwd=y_fwd, ds_t=ds_t,
+                                 inv_perm=_inv_perm(t) if ds_t is not None else None)
         else:
             sddmm_device(t, g, z, mode=mode, epilogue=_lib.EPI_SOFTMAX_BWD, aux=p, out=ds,
                          win_range=wr)
@@ -148,7 +172,10 @@ class AgnnAggregate(torch.autograd.Function):
         tt = t.transpose()
         # one dual SpMM on A^T reading P and dS through the edge permutation
         # (A^T edge k = A edge perm[k]; gathered a window ahead in the kernel)
-        if mode == "tf32" and not _PERMUTE_WEIGHTS:
+        if p_t is not None:
+            spmm_device(tt.tiled, g, p_t, x2=z, weights2=ds_t, mode=mode, out=out,
+                        accumulate=True, win_range=wr, y_row0=r0)
+        elif mode == "tf32" and not _PERMUTE_WEIGHTS:
             spmm_device(tt.tiled, g, p, weight_idx=tt.perm, x2=z, weights2=ds,
                         weight_idx2=tt.perm, mode=mode, out=out, accumulate=True, win_range=wr,
                         y_row0=r0)
