@@ -157,6 +157,13 @@ extern "C" int tcg_sddmm(const tcg_tiling* t, const float* xa, int64_t lda, cons
   TCG_REQUIRE(t->blk_h == 16 && t->blk_w == 8,
               "tf32 mode requires the 16x8 tile shape, got %dx%d", t->blk_h, t->blk_w);
   TCG_REQUIRE(t->edge_frag, "tcg_sddmm: tf32 needs edge_frag (tcg_edge_frag)");
+  {
+    static const bool no_stream = std::getenv("TCG_NO_STREAM") != nullptr;
+    if (!no_stream && dim == 32) {
+      const int rc = stream_sddmm(t, xa, lda, xb, ldb, aux, out, epilogue, win_begin, win_end, s);
+      if (rc != TCG_E_UNSUPPORTED) return rc;
+    }
+  }
   win::Params q = base_params(t, win_begin, win_end);
   const int nt = win::nt_for(dim);
   const int kw = 8 * nt;  // features per launch (<= 64)

@@ -398,6 +398,7 @@ struct AgnnArgs {
   float* eout;       // fwd: P, bwd: dS
   float* y;          // fwd: Y, bwd: dZ (A-side)
   int64_t ldy, y_row0;
+  int epi;           // SDDMM-only launches: TCG_EPI_*
 };
 
 constexpr float kTau = 8.f;  // lazy-rescale threshold of the online softmax (natural log)
@@ -412,7 +413,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 constexpr int kMapB = 24;   // blocks per window covered by the slot map (192 columns)
 constexpr int kMaxE = 255;  // edges per window (u8 slot map)
 
-template <bool BWD>
+template <int KIND>
 struct AgnnCfg {
   static constexpr int NB = 4, NI = 8;
   static constexpr int RING = NB * 1024;
@@ -432,9 +433,10 @@ __device__ __forceinline__ uint32_t agnn_off(int r, int c) {
   return r * 128 + ((c ^ h) & 7) * 16;
 }
 
-template <bool BWD>
-__global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 2) agnn_stream(const AgnnArgs a) {
-  using C = AgnnCfg<BWD>;
+template <int KIND>
+__global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const AgnnArgs a) {
+  using C = AgnnCfg<KIND>;
+  constexpr bool BWD = KIND == 1;   // 0: forward, 1: backward A-side, 2: SDDMM only
   constexpr int NB = C::NB, NI = C::NI;
   constexpr float kLog2e = 1.4426950408889634f;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -596,7 +598,14 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 2) agnn_stream(const A
       const float v[4] = {sc[0], sc[2], sc[1], sc[3]};
       const uint32_t mw = lb < kMapB ? map32[lb * 32 + lane] : 0u;
       float av[4];
-      if constexpr (!BWD) {
+      if constexpr (KIND == 2) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t ej = (mw >> (8 * q)) & 0xffu;
+          if (ej) esc[ej - 1] = v[q];
+        }
+        (void)av;
+      } else if constexpr (KIND == 0) {
         // block row maxima (rows g, g+8) over the quad
         float bm[2];
         bm[0] = fmaxf((mw & 0xffu) ? v[0] : -INFINITY, (mw & 0xff0000u) ? v[2] : -INFINITY);
@@ -651,7 +660,7 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 2) agnn_stream(const A
         }
       }
       // SpMM: acc += A_av * Zc
-      {
+      if constexpr (KIND != 2) {
         float x0[4], x1[4];
         lds_slice<4>(x0, sb + so0);
         lds_slice<4>(x1, sb + so1);
@@ -666,7 +675,33 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 2) agnn_stream(const A
     }
     // ---- window epilogue ----
     float inv[2] = {1.f, 1.f};
-    if constexpr (!BWD) {
+    if constexpr (KIND == 2) {
+      // StoreSparse + the fused row epilogue, two lanes per row (rows never
+      // straddle windows): raw scores, row softmax, or softmax backward
+      __syncwarp();
+      const int r = lane >> 1, sub = lane & 1;
+      const int64_t rg = (int64_t)w * 16 + r;
+      const bool live = rg < a.n;  // every lane runs the same shuffles
+      const int64_t rb = live ? __ldg(a.ptr + rg) - e0 : 0;
+      const int64_t re = live ? __ldg(a.ptr + rg + 1) - e0 : 0;
+      if (a.epi == TCG_EPI_NONE) {
+        for (int64_t j = rb + sub; j < re; j += 2) a.eout[e0 + j] = esc[j];
+      } else if (a.epi == TCG_EPI_SOFTMAX) {
+        float mx = -INFINITY;
+        for (int64_t j = rb + sub; j < re; j += 2) mx = fmaxf(mx, esc[j]);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        float sm = 0.f;
+        for (int64_t j = rb + sub; j < re; j += 2) sm += expf(esc[j] - mx);
+        sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+        for (int64_t j = rb + sub; j < re; j += 2) a.eout[e0 + j] = expf(esc[j] - mx) / sm;
+      } else {
+        float rsum = 0.f;
+        for (int64_t j = rb + sub; j < re; j += 2) rsum += __ldg(a.pin + e0 + j) * esc[j];
+        rsum += __shfl_xor_sync(0xffffffffu, rsum, 1);
+        for (int64_t j = rb + sub; j < re; j += 2)
+          a.eout[e0 + j] = __ldg(a.pin + e0 + j) * (esc[j] - rsum);
+      }
+    } else if constexpr (KIND == 0) {
 #pragma unroll
       for (int rh = 0; rh < 2; ++rh) {
         float l = lrow[rh];
@@ -691,6 +726,7 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 2) agnn_stream(const A
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
+      if constexpr (KIND == 2) break;
       const int64_t r = (int64_t)w * 16 + g + 8 * h;
       if (r >= a.n) continue;
       float4* yr = reinterpret_cast<float4*>(a.y + (r - a.y_row0) * a.ldy + 8 * t);
@@ -705,10 +741,10 @@ __global__ void __launch_bounds__(AgnnCfg<BWD>::WPC * 32, 2) agnn_stream(const A
   cp_wait<0>();
 }
 
-template <bool BWD>
+template <int KIND>
 int launch_agnn(AgnnArgs& a, cudaStream_t s) {
-  using C = AgnnCfg<BWD>;
-  auto kern = agnn_stream<BWD>;
+  using C = AgnnCfg<KIND>;
+  auto kern = agnn_stream<KIND>;
   static int configured = -1;
   int dev = 0;
   TCG_CUDA(cudaGetDevice(&dev), "agnn_stream device");
@@ -724,7 +760,7 @@ int launch_agnn(AgnnArgs& a, cudaStream_t s) {
   const int64_t ctas = (int64_t)num_sms() * per_sm;
   a.nwarps = (int)(ctas * C::WPC);
   kern<<<(unsigned)ctas, C::WPC * 32, C::SMEM, s>>>(a);
-  TCG_LAUNCHED(BWD ? "agnn_stream_bwd" : "agnn_stream_fwd");
+  TCG_LAUNCHED(KIND == 1 ? "agnn_stream_bwd" : KIND == 0 ? "agnn_stream_fwd" : "sddmm_stream");
   return TCG_OK;
 }
 
@@ -871,7 +907,26 @@ int stream_agnn(const tcg_tiling* t, bool bwd, const float* z, int64_t ldz, cons
   a.win_begin = (int)win_begin, a.win_end = (int)win_end;
   a.z = z, a.ldz = ldz, a.za = za, a.lda = lda, a.yf = yf, a.ldyf = ldyf, a.pin = pin;
   a.eout = eout, a.y = y, a.ldy = ldy, a.y_row0 = y_row0;
-  return bwd ? stream::launch_agnn<true>(a, s) : stream::launch_agnn<false>(a, s);
+  return bwd ? stream::launch_agnn<1>(a, s) : stream::launch_agnn<0>(a, s);
+}
+
+// SDDMM (+ softmax / softmax-backward row epilogue) on the block stream, D = 32
+int stream_sddmm(const tcg_tiling* t, const float* xa, int64_t lda, const float* xb, int64_t ldb,
+                 const float* aux, float* out, int epi, int64_t win_begin, int64_t win_end,
+                 cudaStream_t s) {
+  if (!t->block_offsets || !t->col_stream || !t->edge_frag) return TCG_E_UNSUPPORTED;
+  if (t->max_window_edges <= 0 || t->max_window_edges > stream::kMaxE ||
+      t->max_window_unique > 8 * stream::kMapB)
+    return TCG_E_UNSUPPORTED;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al(xa) || !al(xb) || lda % 4 || ldb % 4) return TCG_E_UNSUPPORTED;
+  if (epi == TCG_EPI_SOFTMAX_BWD && !aux) return TCG_E_UNSUPPORTED;
+  stream::AgnnArgs a{};
+  a.ptr = t->node_ptr, a.efrag = t->edge_frag, a.boff = t->block_offsets, a.cs = t->col_stream;
+  a.n = t->num_nodes;
+  a.win_begin = (int)win_begin, a.win_end = (int)win_end;
+  a.z = xb, a.ldz = ldb, a.za = xa, a.lda = lda, a.pin = aux, a.eout = out, a.epi = epi;
+  return stream::launch_agnn<2>(a, s);
 }
 
 }  // namespace tcg

@@ -167,3 +167,27 @@ def test_stream_arxiv_against_exact(env):
     y_ex = kernels.spmm_device(t, z, p_ex, mode="f32")
     assert rel_l2(p_f.cpu().numpy(), p_ex.cpu().numpy()) <= TF32_REL_L2
     assert rel_l2(y_f.cpu().numpy(), y_ex.cpu().numpy()) <= TF32_REL_L2
+
+
+@pytest.mark.parametrize("kind", ["uniform", "powerlaw", "hub"])
+def test_stream_sddmm_epilogues(env, oracle, kind):
+    tcg, kernels, _, torch = env
+    from paper_2112_02052_b200 import _lib
+
+    g = _graph(tcg, kind, 3000, 7, 8)
+    t = tcg.translate(g, tcg.BlockConfig())
+    rng = np.random.default_rng(9)
+    xa = rng.standard_normal((g.num_nodes, 32)).astype(np.float32)
+    xb = rng.standard_normal((g.num_nodes, 32)).astype(np.float32)
+    ptr, cols = g.node_pointer, g.edge_list
+    xat, xbt = torch.from_numpy(xa).cuda(), torch.from_numpy(xb).cuda()
+    s = kernels.sddmm_device(t, xat, xbt)
+    s_ref = oracle.sddmm(ptr, cols, xa, xb)
+    assert rel_l2(s.cpu().numpy(), s_ref) <= TF32_REL_L2
+    p = kernels.sddmm_device(t, xat, epilogue=_lib.EPI_SOFTMAX)
+    p_ref = oracle.segment_softmax(oracle.sddmm(ptr, cols, xa), ptr)
+    assert rel_l2(p.cpu().numpy(), p_ref) <= TF32_REL_L2
+    ds = kernels.sddmm_device(t, xat, xbt, epilogue=_lib.EPI_SOFTMAX_BWD,
+                              aux=torch.from_numpy(p_ref).cuda())
+    ds_ref = oracle.softmax_backward(p_ref, s_ref, ptr)
+    assert rel_l2(ds.cpu().numpy(), ds_ref) <= TF32_REL_L2
