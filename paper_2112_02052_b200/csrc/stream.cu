@@ -110,7 +110,7 @@ struct Args {
 
 constexpr int kEPL = 5;    // edges per lane prefetched for the next window (160)
 
-template <int NT, bool DUAL>
+template <int NT, bool DUAL, bool BIG = false>
 struct Cfg {
   static constexpr int NB = 4;                     // ring depth (blocks)
   static constexpr int NI = 2 * NB;                // column-id ring
@@ -120,8 +120,12 @@ struct Cfg {
   static constexpr int RING = NB * SLOT * OPS;
   static constexpr int IDX = NI * 256;             // per-lane copies of the column ids
   static constexpr int AFR = MB * 512 * OPS;
-  static constexpr int WARP = RING + IDX + AFR;
-  static constexpr int WPC = DUAL ? 4 : 8;         // warps per CTA
+  // BIG: windows with more edges than the register prefetch holds (products:
+  // ~400) stage the next window's edge slots and weights in shared memory
+  static constexpr int EMAX = BIG ? 768 : 0;
+  static constexpr int EDGE = 2 * EMAX * 4 * (1 + OPS);
+  static constexpr int WARP = RING + IDX + AFR + EDGE;
+  static constexpr int WPC = (DUAL || BIG) ? 4 : 8;  // warps per CTA
   static constexpr int SMEM = WPC * WARP;
 };
 
@@ -144,9 +148,9 @@ __device__ __forceinline__ int warp_lower_bound(const int32_t* __restrict__ a, i
   return lo + __popc(__ballot_sync(0xffffffffu, pr));
 }
 
-template <int NT, bool DUAL>
-__global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Args a) {
-  using C = Cfg<NT, DUAL>;
+template <int NT, bool DUAL, bool BIG>
+__global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(const Args a) {
+  using C = Cfg<NT, DUAL, BIG>;
   constexpr int NB = C::NB, NI = C::NI, SLOT = C::SLOT, MB = C::MB;
   constexpr uint32_t RS = MB * 128;  // fragment slots of one round
   constexpr int CP = 4 * NT;  // bytes per lane per staged row
@@ -160,6 +164,8 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Arg
   const unsigned char* iring_p = wsm + C::RING;
   uint32_t* afr = reinterpret_cast<uint32_t*>(wsm + C::RING + C::IDX);
   uint32_t* afr2 = afr + MB * 128;
+  // BIG: edge staging, 2 slots x {frag u32[EMAX], w f32[EMAX] (, w2 f32[EMAX])}
+  unsigned char* ebuf = wsm + C::RING + C::IDX + C::AFR;
 
   // ---- this warp's slice of the block stream ----
   const int B0 = __ldg(a.boff + a.win_begin), B1 = __ldg(a.boff + a.win_end);
@@ -242,6 +248,37 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Arg
       }
     }
   };
+  // BIG: copy the edges of [lo, hi) into staging slot `slot` (cp.async, own group);
+  // returns false when they do not fit (the window then reads global memory)
+  auto stage_edges = [&](int64_t lo, int64_t hi, int slot) -> bool {
+    if constexpr (BIG) {
+      const int64_t ne = hi - lo;
+      if (ne > C::EMAX || a.widx || (DUAL && a.widx2)) return false;
+      const uint32_t sb = smem_u32(ebuf) + slot * C::EMAX * 4 * (1 + C::OPS);
+      for (int j = lane; j < ne; j += 32) {
+        cp_async<4>(sb + 4 * j, a.efrag + lo + j);
+        if (a.w) cp_async<4>(sb + 4 * (C::EMAX + j), a.w + lo + j);
+        if constexpr (DUAL)
+          if (a.w2) cp_async<4>(sb + 4 * (2 * C::EMAX + j), a.w2 + lo + j);
+      }
+      cp_commit();
+      return true;
+    }
+    return false;
+  };
+  auto round_from_stage = [&](int r0, int slot, int ne) {
+    clear_frags();
+    const uint32_t* ef = reinterpret_cast<const uint32_t*>(ebuf + slot * C::EMAX * 4 * (1 + C::OPS));
+    const float* ew = reinterpret_cast<const float*>(ef + C::EMAX);
+    for (int j = lane; j < ne; j += 32) {
+      const uint32_t f = ef[j] - (uint32_t)(r0 * 128);
+      if (f < RS) {
+        afr[f] = tf32_rn(a.w ? ew[j] : 1.f);
+        if constexpr (DUAL) afr2[f] = tf32_rn(a.w2 ? ew[C::EMAX + j] : 1.f);
+      }
+    }
+    __syncwarp();
+  };
   auto hub_load = [&](int r0) {  // windows with more than 32*kEPL edges
     clear_frags();
     for (int64_t e = e0 + lane; e < e1; e += 32) {
@@ -255,6 +292,8 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Arg
   };
   clear_frags();
   prefetch(e0, e1);
+  int eslot = 0;
+  bool staged = BIG ? stage_edges(e0, e1, 0) : false;
 
   const uint32_t as = smem_u32(afr) + lane * 16;
   float acc[NT][4];
@@ -290,6 +329,8 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Arg
   for (int w = ws; w < we; ++w) {
     const int nbw = cb1 - cb0;
     const bool hub = e1 - e0 > 32 * kEPL;
+    const bool from_stage = BIG && hub && staged;
+    const int cur_slot = eslot;
 #pragma unroll
     for (int k = 0; k < kEPL; ++k) {
       of[k] = pf[k], ow[k] = pw[k];
@@ -299,10 +340,18 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Arg
     if (!hub) {
       put_round(0, false);
       __syncwarp();
+    } else if (from_stage) {
+      cp_wait<0>();
+      __syncwarp();
+      round_from_stage(0, cur_slot, (int)(e1 - e0));
     } else {
       hub_load(0);
     }
     prefetch(e1, e2);
+    if constexpr (BIG) {
+      eslot ^= 1;
+      staged = (e2 - e1 > 32 * kEPL) ? stage_edges(e1, e2, eslot) : false;
+    }
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
     for (int r0 = 0; r0 < nbw; r0 += MB) {
@@ -313,6 +362,8 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL>::WPC * 32) spmm_stream(const Arg
           __syncwarp();
           put_round((uint32_t)r0 * 128, false);
           __syncwarp();
+        } else if (from_stage) {
+          round_from_stage(r0, cur_slot, (int)(e1 - e0));
         } else {
           hub_load(r0);
         }
@@ -809,10 +860,10 @@ __global__ void stream_pad_kernel(const int32_t* __restrict__ boff, int64_t W, u
   for (int q = threadIdx.x; q < 8 * TCG_STREAM_PAD; q += blockDim.x) cs[8 * tb + q] = fill;
 }
 
-template <int NT, bool DUAL>
+template <int NT, bool DUAL, bool BIG>
 int launch_t(Args& a, int nchunks, cudaStream_t s) {
-  using C = Cfg<NT, DUAL>;
-  auto kern = spmm_stream<NT, DUAL>;
+  using C = Cfg<NT, DUAL, BIG>;
+  auto kern = spmm_stream<NT, DUAL, BIG>;
   static int configured = -1;
   int dev = 0;
   TCG_CUDA(cudaGetDevice(&dev), "spmm_stream device");
@@ -867,23 +918,30 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
   a.ldx = (int)q.ldx, a.ldx2 = (int)q.ldx2;
   a.x = q.x, a.x2 = q.x2, a.w = q.w, a.widx = q.widx, a.w2 = q.w2, a.widx2 = q.widx2;
   a.bias = q.bias, a.y = q.y, a.ldy = q.ldy, a.y_row0 = q.y_row0, a.accumulate = q.accumulate;
+  // big windows (products: ~400 edges each) stage their edges in shared memory
+  const bool big = t->num_windows > 0 && t->num_edges > 128 * t->num_windows;
   int rc = TCG_OK;
   int d = 0;
   if (full > 0) {
     a.d0 = 0;
-    rc = dual ? stream::launch_t<4, true>(a, full, s) : stream::launch_t<4, false>(a, full, s);
+    rc = big ? (dual ? stream::launch_t<4, true, true>(a, full, s)
+                     : stream::launch_t<4, false, true>(a, full, s))
+             : (dual ? stream::launch_t<4, true, false>(a, full, s)
+                     : stream::launch_t<4, false, false>(a, full, s));
     if (rc != TCG_OK) return rc;
     d = 32 * full;
   }
   if (rem >= 16) {
     a.d0 = d;
-    rc = dual ? stream::launch_t<2, true>(a, 1, s) : stream::launch_t<2, false>(a, 1, s);
+    rc = big ? (dual ? stream::launch_t<2, true, true>(a, 1, s) : stream::launch_t<2, false, true>(a, 1, s))
+             : (dual ? stream::launch_t<2, true, false>(a, 1, s) : stream::launch_t<2, false, false>(a, 1, s));
     if (rc != TCG_OK) return rc;
     d += 16;
   }
   if (d < dim) {
     a.d0 = d;
-    rc = dual ? stream::launch_t<1, true>(a, 1, s) : stream::launch_t<1, false>(a, 1, s);
+    rc = big ? (dual ? stream::launch_t<1, true, true>(a, 1, s) : stream::launch_t<1, false, true>(a, 1, s))
+             : (dual ? stream::launch_t<1, true, false>(a, 1, s) : stream::launch_t<1, false, false>(a, 1, s));
   }
   return rc;
 }

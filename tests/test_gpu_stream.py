@@ -191,3 +191,30 @@ def test_stream_sddmm_epilogues(env, oracle, kind):
                               aux=torch.from_numpy(p_ref).cuda())
     ds_ref = oracle.softmax_backward(p_ref, s_ref, ptr)
     assert rel_l2(ds.cpu().numpy(), ds_ref) <= TF32_REL_L2
+
+
+@pytest.mark.parametrize("dim", [16, 32, 40])
+def test_stream_spmm_big_windows(env, oracle, dim):
+    """Products-like windows (~480 edges): the shared-memory edge-staging variant,
+    including windows past its 768-edge staging capacity (global fallback)."""
+    tcg, kernels, _, torch = env
+    rng = np.random.default_rng(dim)
+    n = 2000
+    src = np.concatenate([rng.integers(0, n, n * 30), np.repeat(np.arange(16), 80)])
+    dst = np.concatenate([rng.integers(0, n, n * 30), rng.integers(0, n, 16 * 80)])
+    g = tcg.CsrGraph.from_edges(src, dst, n)
+    t = tcg.translate(g, tcg.BlockConfig())
+    assert g.num_edges > 128 * t.num_row_windows
+    x = rng.standard_normal((n, dim)).astype(np.float32)
+    x2 = rng.standard_normal((n, dim)).astype(np.float32)
+    w = rng.random(g.num_edges).astype(np.float32)
+    w2 = rng.standard_normal(g.num_edges).astype(np.float32)
+    ptr, cols = g.node_pointer, g.edge_list
+    y = kernels.spmm_device(t, torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda())
+    assert rel_l2(y.cpu().numpy(), oracle.spmm(ptr, cols, x, f=w)) <= TF32_REL_L2
+    y1 = kernels.spmm_device(t, torch.from_numpy(x).cuda())
+    assert rel_l2(y1.cpu().numpy(), oracle.spmm(ptr, cols, x)) <= TF32_REL_L2
+    yd = kernels.spmm_device(t, torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(),
+                             x2=torch.from_numpy(x2).cuda(), weights2=torch.from_numpy(w2).cuda())
+    ref = oracle.spmm(ptr, cols, x, f=w) + oracle.spmm(ptr, cols, x2, f=w2)
+    assert rel_l2(yd.cpu().numpy(), ref) <= TF32_REL_L2
