@@ -49,6 +49,17 @@ __device__ __forceinline__ void cp_async(uint32_t s, const void* g) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(g), "n"(BYTES)
                  : "memory");
 }
+// copy `src_bytes` (<= BYTES) and zero-fill the rest of the BYTES-wide slot
+template <int BYTES>
+__device__ __forceinline__ void cp_async_n(uint32_t s, const void* g, int src_bytes) {
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(g), "r"(src_bytes)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(g), "n"(BYTES),
+                 "r"(src_bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -96,6 +107,7 @@ struct Args {
   int win_begin, win_end;
   int nwarps;            // warps per feature chunk
   int d0, ldx, ldx2;     // first feature of chunk 0 (chunk y adds y * 8 * NT)
+  int dv;                // valid features of the (single) chunk when masked, else 8 * NT
   const float* x;
   const float* x2;
   const float* w;
@@ -106,6 +118,7 @@ struct Args {
   float* y;
   int64_t ldy, y_row0;
   int accumulate;
+  int vec_out;           // 16-B aligned output rows
 };
 
 constexpr int kEPL = 5;    // edges per lane prefetched for the next window (160)
@@ -148,7 +161,7 @@ __device__ __forceinline__ int warp_lower_bound(const int32_t* __restrict__ a, i
   return lo + __popc(__ballot_sync(0xffffffffu, pr));
 }
 
-template <int NT, bool DUAL, bool BIG>
+template <int NT, bool DUAL, bool BIG, bool MASK>
 __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(const Args a) {
   using C = Cfg<NT, DUAL, BIG>;
   constexpr int NB = C::NB, NI = C::NI, SLOT = C::SLOT, MB = C::MB;
@@ -189,8 +202,22 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(cons
   // each lane copies its own (c_t, c_t+4) pair of every block: no cross-lane
   // visibility, so the stream loop needs no warp barrier
   const char* csl = reinterpret_cast<const char*>(a.cs + 8 * (int64_t)gb0 + 2 * t);
+  // masked tail chunk: this lane's slice holds min(NT, dv - g NT) real features
+  const int vb = MASK ? max(0, min(CP, (a.dv - g * NT) * 4)) : CP;
+  constexpr bool masked = MASK;
   auto issue_x = [&](uint32_t xo, uint32_t io) {
     const uint2 id = *reinterpret_cast<const uint2*>(iring_p + lane * 8 + io);
+    if constexpr (masked) {
+      const void* z1 = a.x;  // any valid address when nothing is copied
+      cp_async_n<CP>(xs + xo, vb ? (const void*)(xb + (uint64_t)id.x * xrow) : z1, vb);
+      cp_async_n<CP>(xs + xo + d1, vb ? (const void*)(xb + (uint64_t)id.y * xrow) : z1, vb);
+      if constexpr (DUAL) {
+        cp_async_n<CP>(xs + xo + SLOT, vb ? (const void*)(xb2 + (uint64_t)id.x * xrow2) : z1, vb);
+        cp_async_n<CP>(xs + xo + SLOT + d1, vb ? (const void*)(xb2 + (uint64_t)id.y * xrow2) : z1,
+                       vb);
+      }
+      return;
+    }
     cp_async<CP>(xs + xo, xb + (uint64_t)id.x * xrow);
     cp_async<CP>(xs + xo + d1, xb + (uint64_t)id.y * xrow);
     if constexpr (DUAL) {
@@ -309,13 +336,20 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(cons
       float* yr = a.y + (r - a.y_row0) * a.ldy + fo;
       if (a.bias) {
 #pragma unroll
-        for (int q = 0; q < 2 * NT; ++q) o[q] += __ldg(a.bias + fo + q);
+        for (int q = 0; q < 2 * NT; ++q)
+          if (!MASK || 2 * t * NT + q < a.dv) o[q] += __ldg(a.bias + fo + q);
       }
       if (a.accumulate) {
 #pragma unroll
-        for (int q = 0; q < 2 * NT; ++q) o[q] += yr[q];
+        for (int q = 0; q < 2 * NT; ++q)
+          if (!MASK || 2 * t * NT + q < a.dv) o[q] += yr[q];
       }
-      if constexpr (NT == 4) {
+      if (MASK || !a.vec_out) {
+        // lane t holds chunk features 2t NT .. 2t NT + 2NT
+#pragma unroll
+        for (int q = 0; q < 2 * NT; ++q)
+          if (!MASK || 2 * t * NT + q < a.dv) yr[q] = o[q];
+      } else if constexpr (NT == 4) {
         reinterpret_cast<float4*>(yr)[0] = make_float4(o[0], o[1], o[2], o[3]);
         reinterpret_cast<float4*>(yr)[1] = make_float4(o[4], o[5], o[6], o[7]);
       } else if constexpr (NT == 2) {
@@ -860,10 +894,10 @@ __global__ void stream_pad_kernel(const int32_t* __restrict__ boff, int64_t W, u
   for (int q = threadIdx.x; q < 8 * TCG_STREAM_PAD; q += blockDim.x) cs[8 * tb + q] = fill;
 }
 
-template <int NT, bool DUAL, bool BIG>
+template <int NT, bool DUAL, bool BIG, bool MASK>
 int launch_t(Args& a, int nchunks, cudaStream_t s) {
   using C = Cfg<NT, DUAL, BIG>;
-  auto kern = spmm_stream<NT, DUAL, BIG>;
+  auto kern = spmm_stream<NT, DUAL, BIG, MASK>;
   static int configured = -1;
   int dev = 0;
   TCG_CUDA(cudaGetDevice(&dev), "spmm_stream device");
@@ -895,18 +929,14 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
   if (!t->block_offsets || !t->col_stream) return TCG_E_UNSUPPORTED;
   const int dim = q.dim;
   const bool dual = q.x2 != nullptr;
-  if (dim % 8 != 0 || !q.vec_out || q.nwin <= 0) return TCG_E_UNSUPPORTED;
+  if (q.nwin <= 0) return TCG_E_UNSUPPORTED;
   auto al = [](const void* p, int b) { return (reinterpret_cast<uintptr_t>(p) % b) == 0; };
-  // each chunk width must keep per-lane slices aligned
-  const int full = dim / 32, rem = dim % 32;
-  auto ok_for = [&](int nt) {
+  // a chunk of 8*nt features starting at feature d needs 4*nt-byte aligned slices
+  auto ok_at = [&](int nt, int d) {
     const int b = 4 * nt;
-    return al(q.x, b) && (q.ldx * 4) % b == 0 &&
-           (!dual || (al(q.x2, b) && (q.ldx2 * 4) % b == 0));
+    return al(q.x + d, b) && (q.ldx * 4) % b == 0 &&
+           (!dual || (al(q.x2 + d, b) && (q.ldx2 * 4) % b == 0));
   };
-  if (full > 0 && !ok_for(4)) return TCG_E_UNSUPPORTED;
-  if (rem >= 16 && !ok_for(2)) return TCG_E_UNSUPPORTED;
-  if (rem % 16 == 8 && !ok_for(1)) return TCG_E_UNSUPPORTED;
   stream::Args a{};
   a.ptr = t->node_ptr;
   a.efrag = t->edge_frag;
@@ -920,30 +950,47 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
   a.bias = q.bias, a.y = q.y, a.ldy = q.ldy, a.y_row0 = q.y_row0, a.accumulate = q.accumulate;
   // big windows (products: ~400 edges each) stage their edges in shared memory
   const bool big = t->num_windows > 0 && t->num_edges > 128 * t->num_windows;
-  int rc = TCG_OK;
+  auto launch = [&](int nt, int nchunks) -> int {
+    a.vec_out = (a.dv == 8 * nt) && q.vec_out &&
+                ((a.d0 % 4) == 0);  // float4 / float2 row stores need aligned slices
+    const bool mk = a.dv < 8 * nt;
+#define TCG_SL(NTV, MK)                                                                   \
+  if (nt == NTV && mk == MK)                                                              \
+    return big ? (dual ? stream::launch_t<NTV, true, true, MK>(a, nchunks, s)             \
+                       : stream::launch_t<NTV, false, true, MK>(a, nchunks, s))           \
+               : (dual ? stream::launch_t<NTV, true, false, MK>(a, nchunks, s)            \
+                       : stream::launch_t<NTV, false, false, MK>(a, nchunks, s));
+    TCG_SL(4, false)
+    TCG_SL(2, false)
+    TCG_SL(2, true)
+    TCG_SL(1, false)
+    TCG_SL(1, true)
+#undef TCG_SL
+    return TCG_E_UNSUPPORTED;
+  };
+  // plan: 32-wide chunks (one launch), then 16, then 8-wide, then one masked tail.
+  // Rows whose stride breaks 16-B alignment would need one 8-wide pass per 8
+  // features: past two such passes the single-pass window engine is faster.
+  if (!ok_at(2, 0) && dim > 16) return TCG_E_UNSUPPORTED;
   int d = 0;
-  if (full > 0) {
-    a.d0 = 0;
-    rc = big ? (dual ? stream::launch_t<4, true, true>(a, full, s)
-                     : stream::launch_t<4, false, true>(a, full, s))
-             : (dual ? stream::launch_t<4, true, false>(a, full, s)
-                     : stream::launch_t<4, false, false>(a, full, s));
+  const int full = dim / 32;
+  if (full > 0 && ok_at(4, 0)) {
+    a.d0 = 0, a.dv = 32;
+    const int rc = launch(4, full);
     if (rc != TCG_OK) return rc;
     d = 32 * full;
   }
-  if (rem >= 16) {
+  while (d < dim) {
+    const int rem = dim - d;
+    const int nt = (rem >= 16 && ok_at(2, d)) ? 2 : 1;
+    if (nt == 1 && !ok_at(1, d)) return d == 0 ? TCG_E_UNSUPPORTED : TCG_E_INVALID;
     a.d0 = d;
-    rc = big ? (dual ? stream::launch_t<2, true, true>(a, 1, s) : stream::launch_t<2, false, true>(a, 1, s))
-             : (dual ? stream::launch_t<2, true, false>(a, 1, s) : stream::launch_t<2, false, false>(a, 1, s));
+    a.dv = rem < 8 * nt ? rem : 8 * nt;
+    const int rc = launch(nt, 1);
     if (rc != TCG_OK) return rc;
-    d += 16;
+    d += a.dv;
   }
-  if (d < dim) {
-    a.d0 = d;
-    rc = big ? (dual ? stream::launch_t<1, true, true>(a, 1, s) : stream::launch_t<1, false, true>(a, 1, s))
-             : (dual ? stream::launch_t<1, true, false>(a, 1, s) : stream::launch_t<1, false, false>(a, 1, s));
-  }
-  return rc;
+  return TCG_OK;
 }
 
 // Fused AGNN forward / backward on the block stream; TCG_E_UNSUPPORTED when

@@ -60,12 +60,26 @@ def _finish_rows(slab, shard):
     return slab if shard is None else allgather_rows(slab, shard)
 
 
+def _rows16(x):
+    """x with 16-B aligned rows: the TF32 engine stages rows in 16/8-byte slices,
+    so an odd width (GCN class counts, e.g. products' 47) is copied once into a
+    padded-stride buffer instead of falling back to 4-byte slices."""
+    x = x.contiguous()
+    d = x.shape[1]
+    if d <= 16 or d % 4 == 0:
+        return x
+    buf = torch.empty((x.shape[0], (d + 3) // 4 * 4), dtype=x.dtype, device=x.device)
+    v = buf[:, :d]
+    v.copy_(x)
+    return v
+
+
 class GcnAggregate(torch.autograd.Function):
     """Y = A_w H + b, w = stored edge values (or 1)."""
 
     @staticmethod
     def forward(ctx, h, bias, t: TiledGraph, mode: str, shard: ShardPlan | None):
-        h = h.contiguous()
+        h = _rows16(h) if mode == "tf32" else h.contiguous()
         out, r0, wr = _rows_out(t, h.shape[1], h, shard)
         spmm_device(t, h, _edge_weights(t), mode=mode, out=out, bias=bias, win_range=wr,
                     y_row0=r0)
@@ -76,7 +90,7 @@ class GcnAggregate(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g):
         t, shard = ctx.t, ctx.shard
-        g = g.contiguous()
+        g = _rows16(g) if ctx.mode == "tf32" else g.contiguous()
         tt = t.transpose()
         out, r0, wr = _rows_out(t, g.shape[1], g, shard)
         wt = _edge_weights(t)

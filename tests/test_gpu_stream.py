@@ -65,7 +65,7 @@ def test_block_stream_arrays(env, oracle):
     assert cs.size == 8 * (tb + 16)
 
 
-@pytest.mark.parametrize("dim", [8, 16, 24, 32, 40, 64, 128])
+@pytest.mark.parametrize("dim", [3, 7, 8, 16, 22, 24, 32, 40, 47, 64, 100, 128])
 @pytest.mark.parametrize("kind", ["uniform", "hub"])
 def test_stream_spmm_dims(env, oracle, dim, kind):
     tcg, kernels, _, torch = env
@@ -77,6 +77,31 @@ def test_stream_spmm_dims(env, oracle, dim, kind):
     y = kernels.spmm_device(t, torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda())
     ref = oracle.spmm(g.node_pointer, g.edge_list, x, f=w)
     assert rel_l2(y.cpu().numpy(), ref) <= TF32_REL_L2
+
+
+@pytest.mark.parametrize("dim", [7, 47])
+def test_stream_spmm_masked_tail_bias_accumulate(env, oracle, dim):
+    """Odd widths (GCN class counts): unaligned rows, masked last chunk, bias,
+    accumulate and a shard row offset."""
+    tcg, kernels, _, torch = env
+    g = tcg.synth.gen_uniform(1500, 6, 2)
+    t = tcg.translate(g, tcg.BlockConfig())
+    rng = np.random.default_rng(dim)
+    x = rng.standard_normal((1500, dim)).astype(np.float32)
+    b = rng.standard_normal(dim).astype(np.float32)
+    y0 = rng.standard_normal((1500, dim)).astype(np.float32)
+    ref = oracle.spmm(g.node_pointer, g.edge_list, x) + b + y0
+    out = torch.from_numpy(y0.copy()).cuda()
+    kernels.spmm_device(t, torch.from_numpy(x).cuda(), out=out, bias=torch.from_numpy(b).cuda(),
+                        accumulate=True)
+    assert rel_l2(out.cpu().numpy(), ref) <= TF32_REL_L2
+    W = t.num_row_windows
+    wb, we = W // 2, W
+    r0, r1 = wb * 16, 1500
+    slab = torch.from_numpy(y0[r0:r1].copy()).cuda()
+    kernels.spmm_device(t, torch.from_numpy(x).cuda(), out=slab, bias=torch.from_numpy(b).cuda(),
+                        accumulate=True, win_range=(wb, we), y_row0=r0)
+    assert rel_l2(slab.cpu().numpy(), ref[r0:r1]) <= TF32_REL_L2
 
 
 def test_stream_spmm_bias_accumulate_shard(env, oracle):
@@ -193,7 +218,7 @@ def test_stream_sddmm_epilogues(env, oracle, kind):
     assert rel_l2(ds.cpu().numpy(), ds_ref) <= TF32_REL_L2
 
 
-@pytest.mark.parametrize("dim", [16, 32, 40])
+@pytest.mark.parametrize("dim", [16, 32, 40, 47])
 def test_stream_spmm_big_windows(env, oracle, dim):
     """Products-like windows (~480 edges): the shared-memory edge-staging variant,
     including windows past its 768-edge staging capacity (global fallback)."""
