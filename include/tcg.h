@@ -138,6 +138,9 @@ int tcg_block_stream(const tcg_tiling* t, int32_t* block_offsets, uint32_t* col_
  * A^T edge order once per backward, so the A^T SpMM reads them coalesced. */
 int tcg_permute_f32(const float* src, const uint32_t* idx, float* dst, int64_t n, void* stream);
 
+/* Both arrays through the same permutation in one pass (P and dS). */
+int tcg_permute2_f32(const float* src_a, const float* src_b, const uint32_t* idx, float* dst_a,
+                     float* dst_b, int64_t n, void* stream);
 /* dst[idx[k]] = src[k] (the inverse move of tcg_permute_f32). */
 int tcg_scatter_f32(const float* src, const uint32_t* idx, float* dst, int64_t n, void* stream);
 /* inv[perm[k]] = k: for A^T's perm, inv[e] is the A^T position of A's edge e. */

@@ -66,6 +66,7 @@ SIGNATURES = {
     "tcg_edge_frag": (C.c_int, [C.POINTER(TcgTiling), _P, _P]),
     "tcg_block_stream": (C.c_int, [C.POINTER(TcgTiling), _P, _P, _P]),
     "tcg_permute_f32": (C.c_int, [_P, _P, _I64, _P, _P]),
+    "tcg_permute2_f32": (C.c_int, [_P, _P, _P, _P, _P, _I64, _P]),
     "tcg_csr_transpose_workspace_bytes": (_SZ, [_I64, _I64]),
     "tcg_csr_transpose": (C.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P, _SZ, _P]),
     "tcg_spmm": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P,

@@ -142,13 +142,23 @@ __global__ void __launch_bounds__(256)
 // then the 8 partial sums are combined in a fixed order (deterministic).
 __global__ void __launch_bounds__(256) sum_slabs(const float* __restrict__ part, int slabs,
                                                  int64_t len, float* __restrict__ out) {
+  // 32 outputs x 8 slab groups per CTA; each thread keeps 4 independent
+  // partial sums (loads in flight), combined in a fixed order (deterministic)
   __shared__ float sh[8][33];
   const int o = threadIdx.x & 31, j = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * 32 + o;
-  float s = 0.f;
-  if (i < len)
-    for (int q = j; q < slabs; q += 8) s += part[(int64_t)q * len + i];
-  sh[j][o] = s;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (i < len) {
+    int q = j;
+    for (; q + 24 < slabs; q += 32) {
+      s0 += part[(int64_t)q * len + i];
+      s1 += part[(int64_t)(q + 8) * len + i];
+      s2 += part[(int64_t)(q + 16) * len + i];
+      s3 += part[(int64_t)(q + 24) * len + i];
+    }
+    for (; q < slabs; q += 8) s0 += part[(int64_t)q * len + i];
+  }
+  sh[j][o] = (s0 + s1) + (s2 + s3);
   __syncthreads();
   if (j == 0 && i < len) {
     float tot = 0.f;

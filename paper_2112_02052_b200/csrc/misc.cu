@@ -192,8 +192,32 @@ __global__ void permute_f32(const float* __restrict__ src, const uint32_t* __res
        k += (int64_t)gridDim.x * blockDim.x)
     dst[k] = __ldg(src + __ldg(idx + k));
 }
+
+// two arrays through the same permutation (P and dS of the AGNN backward)
+__global__ void permute2_f32(const float* __restrict__ a, const float* __restrict__ b,
+                             const uint32_t* __restrict__ idx, float* __restrict__ da,
+                             float* __restrict__ db, int64_t n) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t j = __ldg(idx + k);
+    da[k] = __ldg(a + j);
+    db[k] = __ldg(b + j);
+  }
+}
 }  // namespace
 }  // namespace tcg
+
+extern "C" int tcg_permute2_f32(const float* src_a, const float* src_b, const uint32_t* idx,
+                                float* dst_a, float* dst_b, int64_t n, void* stream) {
+  TCG_REQUIRE(n >= 0, "tcg_permute2_f32: negative size");
+  if (n == 0) return TCG_OK;
+  TCG_REQUIRE(src_a && src_b && idx && dst_a && dst_b, "tcg_permute2_f32: null pointer");
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  permute2_f32<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(src_a, src_b, idx, dst_a, dst_b, n);
+  TCG_LAUNCHED("permute2_f32");
+  return TCG_OK;
+}
 
 extern "C" int tcg_permute_f32(const float* src, const uint32_t* idx, float* dst, int64_t n,
                                void* stream) {

@@ -282,6 +282,19 @@ def invert_perm_device(perm):
     return inv
 
 
+def permute2_device(a, b, idx):
+    """(a[idx], b[idx]) in one pass (tcg_permute2_f32)."""
+    import torch
+
+    n = idx.shape[0]
+    da = torch.empty(n, dtype=torch.float32, device=a.device)
+    db = torch.empty(n, dtype=torch.float32, device=a.device)
+    _lib.check(_lib.load().tcg_permute2_f32(a.data_ptr(), b.data_ptr(), idx.data_ptr(),
+                                            da.data_ptr(), db.data_ptr(), n, _stream()),
+               "tcg_permute2_f32")
+    return da, db
+
+
 def permute_device(src, idx, out=None):
     """out[k] = src[idx[k]] (tcg_permute_f32)."""
     import torch

@@ -36,6 +36,7 @@ from .kernels import (
     agnn_backward_device,
     agnn_forward_device,
     invert_perm_device,
+    permute2_device,
     permute_device,
     sddmm_device,
     spmm_device,
@@ -194,8 +195,7 @@ class AgnnAggregate(torch.autograd.Function):
                         weight_idx2=tt.perm, mode=mode, out=out, accumulate=True, win_range=wr,
                         y_row0=r0)
         else:
-            pt = permute_device(p, tt.perm)
-            dst = permute_device(ds, tt.perm)
+            pt, dst = permute2_device(p, ds, tt.perm)
             spmm_device(tt.tiled, g, pt, x2=z, weights2=dst, mode=mode, out=out,
                         accumulate=True, win_range=wr, y_row0=r0)
         return _finish_rows(out, shard), None, None, None
