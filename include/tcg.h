@@ -119,6 +119,11 @@ int tcg_sgt(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_node
             uint32_t* edge_to_col, int64_t* col_offsets, uint32_t* col_to_node,
             void* workspace, size_t workspace_bytes, void* stream);
 
+/* edgeToRow of the TC-GNN preprocessing: the row of each edge inside its
+ * row window (reference TiledGraph.window_edge_rows, sgt.py:84-90, for all
+ * windows at once); edge_to_row u32[M]. */
+int tcg_edge_to_row(const int64_t* node_ptr, int64_t num_nodes, int32_t blk_h,
+                    uint32_t* edge_to_row, void* stream);
 /* Per-edge fragment slot for the TF32 kernels (16x8 tilings): edge e of row
  * r with condensed column c lands at (c/8)*128 + lane*4 + slot of its
  * window's A tiles, lane = (r%8)*4 + c%4, slot = r%16/8 + 2*(c%8/4). Derived

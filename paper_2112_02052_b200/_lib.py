@@ -64,6 +64,7 @@ SIGNATURES = {
     "tcg_sgt_workspace_bytes": (_SZ, [_I64, _I64, _I32]),
     "tcg_sgt": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
     "tcg_edge_frag": (C.c_int, [C.POINTER(TcgTiling), _P, _P]),
+    "tcg_edge_to_row": (C.c_int, [_P, _I64, _I32, _P, _P]),
     "tcg_block_stream": (C.c_int, [C.POINTER(TcgTiling), _P, _P, _P]),
     "tcg_permute_f32": (C.c_int, [_P, _P, _I64, _P, _P]),
     "tcg_permute2_f32": (C.c_int, [_P, _P, _P, _P, _P, _I64, _P]),

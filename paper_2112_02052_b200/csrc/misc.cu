@@ -207,6 +207,30 @@ __global__ void permute2_f32(const float* __restrict__ a, const float* __restric
 }  // namespace
 }  // namespace tcg
 
+namespace tcg {
+namespace {
+// edgeToRow: row of each edge inside its row window (one thread per row)
+__global__ void edge_to_row_kernel(const int64_t* __restrict__ ptr, int64_t n, int blk_h,
+                                   uint32_t* __restrict__ e2r) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const uint32_t rl = (uint32_t)(r % blk_h);
+  for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) e2r[e] = rl;
+}
+}  // namespace
+}  // namespace tcg
+
+extern "C" int tcg_edge_to_row(const int64_t* node_ptr, int64_t num_nodes, int32_t blk_h,
+                               uint32_t* edge_to_row, void* stream) {
+  TCG_REQUIRE(num_nodes >= 0 && blk_h >= 1, "tcg_edge_to_row: bad arguments");
+  if (num_nodes == 0) return TCG_OK;
+  TCG_REQUIRE(node_ptr && edge_to_row, "tcg_edge_to_row: null pointer");
+  tcg::edge_to_row_kernel<<<(unsigned)((num_nodes + 255) / 256), 256, 0, as_stream(stream)>>>(
+      node_ptr, num_nodes, blk_h, edge_to_row);
+  TCG_LAUNCHED("edge_to_row");
+  return TCG_OK;
+}
+
 extern "C" int tcg_permute2_f32(const float* src_a, const float* src_b, const uint32_t* idx,
                                 float* dst_a, float* dst_b, int64_t n, void* stream) {
   TCG_REQUIRE(n >= 0, "tcg_permute2_f32: negative size");

@@ -106,6 +106,24 @@ class TiledGraph:
         r0, r1 = min(window * bh, g.num_nodes), min((window + 1) * bh, g.num_nodes)
         return np.repeat(np.arange(r1 - r0, dtype=np.int64), np.diff(g.node_pointer[r0:r1 + 1]))
 
+    @property
+    def edge_to_row(self) -> np.ndarray:
+        """edgeToRow for every edge (the window_edge_rows of all windows,
+        concatenated), computed on the GPU (tcg_edge_to_row)."""
+        a = self._host.get("edge_to_row")
+        if a is None:
+            import torch
+
+            self._require_graph()
+            ptr = self.dev["node_ptr"]
+            e2r = torch.empty(max(self.num_edges, 1), dtype=torch.int32, device=ptr.device)
+            _lib.check(_lib.load().tcg_edge_to_row(ptr.data_ptr(), self.num_nodes,
+                                                   self.config.blk_h, e2r.data_ptr(),
+                                                   _stream_ptr()), "tcg_edge_to_row")
+            a = _to_np_u32(e2r[: self.num_edges])
+            self._host["edge_to_row"] = a
+        return a
+
     def _require_graph(self) -> CsrGraph:
         if self.graph is None:
             raise ValueError(

@@ -115,3 +115,12 @@ def test_tcgt_from_gpu_sgt(env, tmp_path):
     assert tcg.structure_blocks_before(t2, 8) == tcg.count_blocks_before(g, tcg.BlockConfig())[0]
     for k in ("win_partition", "edge_to_col", "col_offsets", "col_to_node"):
         assert np.array_equal(getattr(t2, k), getattr(t, k))
+
+
+def test_edge_to_row_device(env):
+    tcg, torch = env
+    for n, deg, bh in ((1000, 5, 16), (777, 9, 8), (50, 2, 32)):
+        g = tcg.synth.gen_uniform(n, deg, 3)
+        t = tcg.translate(g, tcg.BlockConfig(blk_h=bh, blk_w=8))
+        want = np.concatenate([t.window_edge_rows(w) for w in range(t.num_row_windows)])
+        assert np.array_equal(t.edge_to_row.astype(np.int64), want)
