@@ -6,11 +6,13 @@ import bench
 import paper_2112_02052_b200 as tcg
 from paper_2112_02052_b200 import layers
 kind = sys.argv[1] if len(sys.argv) > 1 else "agnn"
-g, x_np, lab_np = bench.make_inputs("arxiv", 128, 40)
+shape = sys.argv[2] if len(sys.argv) > 2 else "arxiv"
+feats, classes = {"arxiv": (128, 40), "products": (100, 47), "amazon0601": (96, 22)}[shape]
+g, x_np, lab_np = bench.make_inputs(shape, feats, classes)
 t = tcg.translate(g, tcg.BlockConfig(), device="cuda")
 t.transpose()
 x = torch.from_numpy(x_np).cuda(); y = torch.from_numpy(lab_np).cuda()
-net = (layers.AGNN(128, 32, 40, layers=4) if kind == "agnn" else layers.GCN(128, 16, 40)).cuda()
+net = (layers.AGNN(feats, 32, classes, layers=4) if kind == "agnn" else layers.GCN(feats, 16, classes)).cuda()
 opt = torch.optim.Adam(net.parameters(), lr=0.01, capturable=True, fused=True)
 def step():
     opt.zero_grad(set_to_none=True)
