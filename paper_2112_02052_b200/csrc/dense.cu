@@ -140,30 +140,29 @@ __global__ void __launch_bounds__(256)
 // Fixed-order sum of the slab partials.
 // 32 outputs per CTA x 8 summers: summer j adds slabs j, j+8, ... in order,
 // then the 8 partial sums are combined in a fixed order (deterministic).
-__global__ void __launch_bounds__(256) sum_slabs(const float* __restrict__ part, int slabs,
-                                                 int64_t len, float* __restrict__ out) {
-  // 32 outputs x 8 slab groups per CTA; each thread keeps 4 independent
-  // partial sums (loads in flight), combined in a fixed order (deterministic)
-  __shared__ float sh[8][33];
+__global__ void __launch_bounds__(1024) sum_slabs(const float* __restrict__ part, int slabs,
+                                                  int64_t len, float* __restrict__ out) {
+  // 32 outputs x 32 slab groups per CTA (the partial count is ~300-600, so
+  // every thread keeps ~10-20 independent loads in flight); the groups are
+  // combined in a fixed order (deterministic)
+  __shared__ float sh[32][33];
   const int o = threadIdx.x & 31, j = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * 32 + o;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  float s0 = 0.f, s1 = 0.f;
   if (i < len) {
     int q = j;
-    for (; q + 24 < slabs; q += 32) {
+    for (; q + 32 < slabs; q += 64) {
       s0 += part[(int64_t)q * len + i];
-      s1 += part[(int64_t)(q + 8) * len + i];
-      s2 += part[(int64_t)(q + 16) * len + i];
-      s3 += part[(int64_t)(q + 24) * len + i];
+      s1 += part[(int64_t)(q + 32) * len + i];
     }
-    for (; q < slabs; q += 8) s0 += part[(int64_t)q * len + i];
+    for (; q < slabs; q += 32) s0 += part[(int64_t)q * len + i];
   }
-  sh[j][o] = (s0 + s1) + (s2 + s3);
+  sh[j][o] = s0 + s1;
   __syncthreads();
   if (j == 0 && i < len) {
     float tot = 0.f;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) tot += sh[q][o];
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) tot += sh[q][o];
     out[i] = tot;
   }
 }
@@ -439,10 +438,10 @@ extern "C" int tcg_gemm_tn(const float* a, int64_t lda, const float* b, int64_t 
     const int rc = fast_gemm_tn(a, lda, b, ldb, mask, ldm, n, (int)k, (int)c, part,
                                 colsum ? colpart : nullptr, slabs, &used, s);
     if (rc == TCG_OK) {
-      sum_slabs<<<(unsigned)((k * c + 31) / 32), 256, 0, s>>>(part, (int)used, k * c, out);
+      sum_slabs<<<(unsigned)((k * c + 31) / 32), 1024, 0, s>>>(part, (int)used, k * c, out);
       TCG_LAUNCHED("sum_slabs");
       if (colsum) {
-        sum_slabs<<<(unsigned)((c + 31) / 32), 256, 0, s>>>(colpart, (int)used, c, colsum);
+        sum_slabs<<<(unsigned)((c + 31) / 32), 1024, 0, s>>>(colpart, (int)used, c, colsum);
         TCG_LAUNCHED("sum_slabs");
       }
       return TCG_OK;
@@ -453,10 +452,10 @@ extern "C" int tcg_gemm_tn(const float* a, int64_t lda, const float* b, int64_t 
   gemm_tn_partial<<<grid, 256, 0, s>>>(a, lda, b, ldb, mask, ldm, n, (int)k, (int)c, rows, part,
                                        colsum ? colpart : nullptr);
   TCG_LAUNCHED("gemm_tn_partial");
-  sum_slabs<<<(unsigned)((k * c + 31) / 32), 256, 0, s>>>(part, (int)slabs, k * c, out);
+  sum_slabs<<<(unsigned)((k * c + 31) / 32), 1024, 0, s>>>(part, (int)slabs, k * c, out);
   TCG_LAUNCHED("sum_slabs");
   if (colsum) {
-    sum_slabs<<<(unsigned)((c + 31) / 32), 256, 0, s>>>(colpart, (int)slabs, c, colsum);
+    sum_slabs<<<(unsigned)((c + 31) / 32), 1024, 0, s>>>(colpart, (int)slabs, c, colsum);
     TCG_LAUNCHED("sum_slabs");
   }
   return TCG_OK;
