@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(DenseCfg<CI, CO, MASK>::NT)
 
 template <int CI, int CO, bool MASK>
 struct GemmCfg {
-  static constexpr int OG = (CI / 4) * (CO / 4);         // 4x4 output blocks
+  static constexpr int PB = CI % 8 == 0 && CI >= 64 ? 8 : 4;  // product rows per thread
+  static constexpr int OG = (CI / PB) * (CO / 4);        // PB x 4 output blocks
   // row groups (a power of two dividing ROWS): ~256 threads per CTA
   static constexpr int RQ = OG >= 256 ? 1 : OG >= 128 ? 2 : OG >= 64 ? 4 : OG >= 32 ? 8 : 16;
   static constexpr int NT = OG * RQ;
@@ -182,8 +183,9 @@ __global__ void __launch_bounds__(GemmCfg<CI, CO, MASK>::NT)
   using C = GemmCfg<CI, CO, MASK>;
   extern __shared__ __align__(16) float sh[];
   const int tid = threadIdx.x;
+  constexpr int PB = C::PB;
   const int og = tid % C::OG, rq = tid / C::OG;
-  const int ib = og / (CO / 4), cb = og % (CO / 4);  // product rows 4ib.., cols 4cb..
+  const int ib = og / (CO / 4), cb = og % (CO / 4);  // product rows PB ib.., cols 4cb..
   const int64_t ntiles = (n + C::ROWS - 1) / C::ROWS;
   const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int cq = (co + 3) / 4;  // B quads holding real columns
@@ -213,9 +215,9 @@ __global__ void __launch_bounds__(GemmCfg<CI, CO, MASK>::NT)
 #pragma unroll
   for (int s = 0; s < C::STAGES - 1; ++s) issue(s);
 
-  float acc[4][4];
+  float acc[PB][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < PB; ++i)
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
   float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);  // colsum of cols 4cb.. (ib == 0 threads)
@@ -229,22 +231,26 @@ __global__ void __launch_bounds__(GemmCfg<CI, CO, MASK>::NT)
 #pragma unroll 4
     for (int rr = 0; rr < RPG; ++rr) {
       const int r = rq * RPG + rr;
-      const float4 av = *reinterpret_cast<const float4*>(at + r * C::AS + 4 * ib);
+      float ai[PB];
+#pragma unroll
+      for (int h = 0; h < PB / 4; ++h) {
+        const float4 av = *reinterpret_cast<const float4*>(at + r * C::AS + PB * ib + 4 * h);
+        ai[4 * h] = av.x, ai[4 * h + 1] = av.y, ai[4 * h + 2] = av.z, ai[4 * h + 3] = av.w;
+      }
       float4 bv = *reinterpret_cast<const float4*>(bt + r * C::BS + 4 * cb);
       if (MASK) {
         const float4 mk = *reinterpret_cast<const float4*>(bt + C::ROWS * C::BS + r * C::BS + 4 * cb);
         bv.x = mk.x > 0.f ? bv.x : 0.f, bv.y = mk.y > 0.f ? bv.y : 0.f;
         bv.z = mk.z > 0.f ? bv.z : 0.f, bv.w = mk.w > 0.f ? bv.w : 0.f;
       }
-      const float ai[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < PB; ++i) {
         acc[i][0] = fmaf(ai[i], bv.x, acc[i][0]);
         acc[i][1] = fmaf(ai[i], bv.y, acc[i][1]);
         acc[i][2] = fmaf(ai[i], bv.z, acc[i][2]);
         acc[i][3] = fmaf(ai[i], bv.w, acc[i][3]);
       }
-      cs.x += bv.x, cs.y += bv.y, cs.z += bv.z, cs.w += bv.w;
+      if (ib == 0) cs.x += bv.x, cs.y += bv.y, cs.z += bv.z, cs.w += bv.w;
     }
     __syncthreads();
   }
@@ -253,9 +259,9 @@ __global__ void __launch_bounds__(GemmCfg<CI, CO, MASK>::NT)
   // fixed-order reduction over the row groups through shared memory
   float* red = sh;  // [RQ][CI][CO] + [RQ][CO]
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < PB; ++i)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) red[(rq * CI + 4 * ib + i) * CO + 4 * cb + c] = acc[i][c];
+    for (int c = 0; c < 4; ++c) red[(rq * CI + PB * ib + i) * CO + 4 * cb + c] = acc[i][c];
   if (ib == 0) {
     float* rc = red + C::RQ * CI * CO + rq * CO + 4 * cb;
     rc[0] = cs.x, rc[1] = cs.y, rc[2] = cs.z, rc[3] = cs.w;
