@@ -1,0 +1,10 @@
+import sys; sys.path.insert(0, '.')
+import torch
+from paper_2112_02052_b200 import dense
+torch.backends.cuda.matmul.allow_tf32 = False
+n = 169343
+for ci, co in ((32, 32), (128, 32)):
+    x = torch.randn(n, ci, device='cuda'); w = torch.randn(ci, co, device='cuda'); g = torch.randn(n, co, device='cuda')
+    for _ in range(3):
+        dense.dense(x, w); dense.dense(g, w, transposed=True); dense.gemm_tn(x, g)
+torch.cuda.synchronize()
