@@ -131,7 +131,7 @@ struct Cfg {
   static constexpr int OPS = DUAL ? 2 : 1;
   static constexpr int MB = DUAL ? 8 : 16;         // A-fragment blocks resident (one round)
   static constexpr int RING = NB * SLOT * OPS;
-  static constexpr int IDX = NI * 256;             // per-lane copies of the column ids
+  static constexpr int IDX = NI * 32;              // column-id pairs of NI blocks
   static constexpr int AFR = MB * 512 * OPS;
   // BIG: windows with more edges than the register prefetch holds (products:
   // ~400) stage the next window's edge slots and weights in shared memory
@@ -198,15 +198,15 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(cons
   // +0 / +d1), this lane's column-id pair of block s at is + (s % NI) * 256
   const uint32_t xs = ring + slot_off<NT>(t, g);
   const uint32_t d1 = slot_off<NT>(t + 4, g) - slot_off<NT>(t, g);
-  const uint32_t is = iring + lane * 8;
+  const uint32_t is = iring + lane * 16;  // lanes 0-1 copy a block's 32 B of ids
   // each lane copies its own (c_t, c_t+4) pair of every block: no cross-lane
   // visibility, so the stream loop needs no warp barrier
-  const char* csl = reinterpret_cast<const char*>(a.cs + 8 * (int64_t)gb0 + 2 * t);
+  const char* csl = reinterpret_cast<const char*>(a.cs + 8 * (int64_t)gb0 + 4 * lane);
   // masked tail chunk: this lane's slice holds min(NT, dv - g NT) real features
   const int vb = MASK ? max(0, min(CP, (a.dv - g * NT) * 4)) : CP;
   constexpr bool masked = MASK;
   auto issue_x = [&](uint32_t xo, uint32_t io) {
-    const uint2 id = *reinterpret_cast<const uint2*>(iring_p + lane * 8 + io);
+    const uint2 id = *reinterpret_cast<const uint2*>(iring_p + 8 * t + io);
     if constexpr (masked) {
       const void* z1 = a.x;  // any valid address when nothing is copied
       cp_async_n<CP>(xs + xo, vb ? (const void*)(xb + (uint64_t)id.x * xrow) : z1, vb);
@@ -225,16 +225,18 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(cons
       cp_async<CP>(xs + xo + SLOT + d1, xb2 + (uint64_t)id.y * xrow2);
     }
   };
-  for (int s = 0; s < NB; ++s) cp_async<8>(is + s * 256, csl + 32 * s);
+  if (lane < 2)
+    for (int s = 0; s < NB; ++s) cp_async<16>(is + s * 32, csl + 32 * s);
   cp_commit();
   cp_wait<0>();
+  __syncwarp();
   for (int s = 0; s < NB; ++s) {
-    issue_x(s * SLOT * C::OPS, s * 256);
-    cp_async<8>(is + (s + NB) * 256, csl + 32 * (s + NB));
+    issue_x(s * SLOT * C::OPS, s * 32);
+    if (lane < 2) cp_async<16>(is + (s + NB) * 32, csl + 32 * (s + NB));
     cp_commit();
   }
   // ring cursors of the consumed block s: X slot, id slot of s + NB, id slot of s + 2NB
-  uint32_t xo = 0, io = NB * 256, iw = 0;
+  uint32_t xo = 0, io = NB * 32, iw = 0;
   const char* cnext = csl + 32 * 2 * NB;
 
   // ---- window metadata, rolled 3 windows ahead ----
@@ -406,6 +408,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(cons
       uint32_t fa = as;
       for (int lb = r0; lb < rend; ++lb, fa += 512) {
         cp_wait<NB - 1>();
+        __syncwarp();  // ids copied by lanes 0-1 visible to the warp
         {
           float x0[NT], x1[NT];
           lds_slice<NT>(x0, xs + xo);
@@ -426,12 +429,12 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(cons
         }
         // refill: X of block s + NB into this slot, ids of block s + 2NB
         issue_x(xo, io);
-        cp_async<8>(is + iw, cnext);
+        if (lane < 2) cp_async<16>(is + iw, cnext);
         cp_commit();
         cnext += 32;
         xo = (xo + SLOT * C::OPS) & (NB * SLOT * C::OPS - 1);
-        io = (io + 256) & (NI * 256 - 1);
-        iw = (iw + 256) & (NI * 256 - 1);
+        io = (io + 32) & (NI * 32 - 1);
+        iw = (iw + 32) & (NI * 32 - 1);
       }
     }
     store(w);
