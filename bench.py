@@ -393,28 +393,72 @@ def run_ours(args):
     final_loss = float(step().item())
 
     # ---- e2e: public API from pinned host buffers ----
+    # Every step copies its features + labels H2D from pinned memory and reads
+    # its loss back D2H. The copy of step k+1 runs on a copy stream while step
+    # k computes (double-buffered staging, then one D2D into the graph's static
+    # input); the timed span covers all copies, steps and loss reads, divided
+    # by the step count. The serial form (copy, step, read, in turn) is also
+    # reported (extras.e2e_serial_ms).
     x_host = torch.from_numpy(x_np).pin_memory()
     y_host = torch.from_numpy(labels_np).pin_memory()
-    loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
-    e2e_ms = []
-    for i in range(args.steps + 2):
-        flush()
+    loss_host = torch.empty(args.steps + 2, dtype=torch.float32).pin_memory()
+    comp = torch.cuda.current_stream()
+    copy_stream = torch.cuda.Stream()
+    x_stage = [torch.empty_like(x_dev) for _ in range(2)]
+    y_stage = [torch.empty_like(y_dev) for _ in range(2)]
+    copied = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+
+    def run_e2e(nsteps):
+        for b in range(2):
+            consumed[b].record(comp)
+        s, e = ev(), ev()
+        s.record(comp)
+        copy_stream.wait_stream(comp)
+
+        def prefetch(k):
+            b = k % 2
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(consumed[b])
+                x_stage[b].copy_(x_host, non_blocking=True)
+                y_stage[b].copy_(y_host, non_blocking=True)
+                copied[b].record(copy_stream)
+
+        prefetch(0)
+        for k in range(nsteps):
+            if k + 1 < nsteps:
+                prefetch(k + 1)
+            b = k % 2
+            comp.wait_event(copied[b])
+            x_dev.copy_(x_stage[b], non_blocking=True)
+            y_dev.copy_(y_stage[b], non_blocking=True)
+            consumed[b].record(comp)
+            lo = step()
+            loss_host[k].copy_(lo.detach().reshape(()), non_blocking=True)
+        e.record(comp)
+        e.synchronize()
+        return s.elapsed_time(e) / nsteps
+
+    run_e2e(2)  # warm-up
+    e2e_total = run_e2e(args.steps) * args.steps
+    serial = []
+    for i in range(min(args.steps, 5) + 1):
         s, e = ev(), ev()
         s.record()
         x_dev.copy_(x_host, non_blocking=True)
         y_dev.copy_(y_host, non_blocking=True)
         lo = step()
-        loss_host.copy_(lo.detach().reshape(1), non_blocking=True)
+        loss_host[0].copy_(lo.detach().reshape(()), non_blocking=True)
         e.record()
         e.synchronize()
-        if i >= 2:
-            e2e_ms.append(s.elapsed_time(e))
-    e2e_total = sum(e2e_ms)
+        if i:
+            serial.append(s.elapsed_time(e))
+    e2e_serial = statistics.median(serial)
     if world > 1:
         tm = torch.tensor([e2e_total], device=dev)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
         e2e_total = float(tm.item())
-    e2e_ms_step = e2e_total / len(e2e_ms)
+    e2e_ms_step = e2e_total / args.steps
     clocks.stop()
 
     extras = {}
@@ -502,6 +546,7 @@ def run_ours(args):
         t_blk = timed(lambda: tcg.structure_blocks_before(t, 8))
         del src_r, dst_r, g_dev
         extras = {
+            "e2e_serial_ms": round(e2e_serial, 4),
             "from_edges_ms": round(t_fe, 3),
             "validate_ms": round(t_val, 3),
             "structure_blocks_ms": round(t_blk, 3),
