@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(WPB * 32) g4(const __grid_constant__ CUtensorM
     __syncwarp();
     if (lane < IL) {
       const int i = c * rows_per + lane * 4;
-      const int4 r = make_int4(__ldg(idx + min(i, m - 1)), __ldg(idx + min(i + 1, m - 1)), __ldg(idx + min(i + 2, m - 1)), __ldg(idx + min(i + 3, m - 1)));
+      const int4 r = __ldg(reinterpret_cast<const int4*>(idx) + min(i, m - 4) / 4);
       asm volatile("cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
                    :: "r"(su(ring + s * STG + lane * 512)), "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w), "r"(su(bar + s)) : "memory");
     }
@@ -73,7 +73,7 @@ int main() {
   const int smem = WPB * (NS * STG + 1024);
   CK(cudaFuncSetAttribute(g4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int occ; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, g4, WPB * 32, smem);
-  for (int cps = 1; cps <= occ; cps *= 2) {
+  for (int cps = occ; cps >= 1 && cps >= occ / 2; --cps) {
     std::vector<float> c, w;
     for (int cold = 1; cold >= 0; --cold) {
       std::vector<float>& v = cold ? c : w;
