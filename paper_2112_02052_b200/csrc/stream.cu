@@ -129,13 +129,13 @@ struct Cfg {
   static constexpr int NI = 2 * NB;                // column-id ring
   static constexpr int SLOT = 8 * 32 * NT;         // bytes of one operand's block
   static constexpr int OPS = DUAL ? 2 : 1;
-  static constexpr int MB = DUAL ? 8 : 16;         // A-fragment blocks resident (one round)
+  static constexpr int MB = (DUAL || BIG) ? 8 : 16;  // A-fragment blocks resident (one round)
   static constexpr int RING = NB * SLOT * OPS;
   static constexpr int IDX = NI * 32;              // column-id pairs of NI blocks
   static constexpr int AFR = MB * 512 * OPS;
   // BIG: windows with more edges than the register prefetch holds (products:
   // ~400) stage the next window's edge slots and weights in shared memory
-  static constexpr int EMAX = BIG ? 768 : 0;
+  static constexpr int EMAX = BIG ? 512 : 0;
   static constexpr int EDGE = 2 * EMAX * 4 * (1 + OPS);
   static constexpr int WARP = RING + IDX + AFR + EDGE;
   static constexpr int WPC = (DUAL || BIG) ? 4 : 8;  // warps per CTA
@@ -323,6 +323,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(cons
   prefetch(e0, e1);
   int eslot = 0;
   bool staged = BIG ? stage_edges(e0, e1, 0) : false;
+  int stage_age = 0;  // block groups committed since the current staging group
 
   const uint32_t as = smem_u32(afr) + lane * 16;
   float acc[NT][4];
@@ -377,7 +378,9 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(cons
       put_round(0, false);
       __syncwarp();
     } else if (from_stage) {
-      cp_wait<0>();
+      // the staging group was committed before the previous window's nbw block
+      // groups; after >= NB of them the per-step wait has already retired it
+      if (stage_age < NB) cp_wait<0>();
       __syncwarp();
       round_from_stage(0, cur_slot, (int)(e1 - e0));
     } else {
@@ -387,6 +390,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(cons
     if constexpr (BIG) {
       eslot ^= 1;
       staged = (e2 - e1 > 32 * kEPL) ? stage_edges(e1, e2, eslot) : false;
+      stage_age = nbw;  // this window's block steps follow the new staging group
     }
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
