@@ -295,16 +295,30 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(cons
     }
     return false;
   };
-  auto round_from_stage = [&](int r0, int slot, int ne) {
+  // Staged windows are consumed round by round (MB blocks each). Within a row the
+  // edges are sorted by column, hence by block, so every row's edges of round k
+  // follow its edges of round k-1: two lanes per row walk their row with a
+  // cursor instead of rescanning the whole window each round.
+  int rc_cur = 0, rc_end = 0;  // this lane's cursor into its row's staged edges
+  auto rows_begin = [&](int64_t wbase_e, int w) {
+    const int row = lane >> 1;
+    const int64_t r = (int64_t)w * 16 + row;
+    const int64_t rb = r < a.n ? __ldg(a.ptr + r) : wbase_e;
+    const int64_t re = r < a.n ? __ldg(a.ptr + r + 1) : wbase_e;
+    rc_cur = (int)(rb - wbase_e) + (lane & 1);
+    rc_end = (int)(re - wbase_e);
+  };
+  auto round_from_stage = [&](int r0, int slot) {
     clear_frags();
     const uint32_t* ef = reinterpret_cast<const uint32_t*>(ebuf + slot * C::EMAX * 4 * (1 + C::OPS));
     const float* ew = reinterpret_cast<const float*>(ef + C::EMAX);
-    for (int j = lane; j < ne; j += 32) {
-      const uint32_t f = ef[j] - (uint32_t)(r0 * 128);
-      if (f < RS) {
-        afr[f] = tf32_rn(a.w ? ew[j] : 1.f);
-        if constexpr (DUAL) afr2[f] = tf32_rn(a.w2 ? ew[C::EMAX + j] : 1.f);
-      }
+    const uint32_t lo = (uint32_t)(r0 * 128);
+    while (rc_cur < rc_end) {
+      const uint32_t f = ef[rc_cur] - lo;
+      if (f >= RS) break;  // this row's next edges belong to a later round
+      afr[f] = tf32_rn(a.w ? ew[rc_cur] : 1.f);
+      if constexpr (DUAL) afr2[f] = tf32_rn(a.w2 ? ew[C::EMAX + rc_cur] : 1.f);
+      rc_cur += 2;
     }
     __syncwarp();
   };
@@ -382,7 +396,8 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(cons
       // groups; after >= NB of them the per-step wait has already retired it
       if (stage_age < NB) cp_wait<0>();
       __syncwarp();
-      round_from_stage(0, cur_slot, (int)(e1 - e0));
+      rows_begin(e0, w);
+      round_from_stage(0, cur_slot);
     } else {
       hub_load(0);
     }
@@ -403,7 +418,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(cons
           put_round((uint32_t)r0 * 128, false);
           __syncwarp();
         } else if (from_stage) {
-          round_from_stage(r0, cur_slot, (int)(e1 - e0));
+          round_from_stage(r0, cur_slot);
         } else {
           hub_load(r0);
         }
