@@ -110,7 +110,19 @@ int tcg_structure_blocks(const tcg_tiling* t, int64_t tile_width, int64_t* per_w
 /* ---- SGT: reference sgt.translate (sgt.py:101-137) ---------------------- */
 /* Workspace bytes tcg_sgt needs for this graph size. */
 size_t tcg_sgt_workspace_bytes(int64_t num_nodes, int64_t num_edges, int32_t blk_h);
-/* One stream-ordered call: per-window sort/dedup/rank on the GPU.
+/* Two-phase form. tcg_sgt_count writes edge_to_col[M]
+ * and col_offsets[W+1] (exclusive scan of the per-window unique counts, so
+ * U = col_offsets[W]); the caller reads U, allocates col_to_node[U] and calls
+ * tcg_sgt_fill, which writes col_to_node and win_partition[W]. Workspace as
+ * tcg_sgt_workspace_bytes (count only; fill needs none). */
+int tcg_sgt_count(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_nodes,
+                  int64_t num_edges, int32_t blk_h, int32_t blk_w, uint32_t* edge_to_col,
+                  int64_t* col_offsets, void* workspace, size_t workspace_bytes, void* stream);
+int tcg_sgt_fill(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_nodes,
+                 int64_t num_edges, int32_t blk_h, int32_t blk_w, const uint32_t* edge_to_col,
+                 const int64_t* col_offsets, uint32_t* win_partition, uint32_t* col_to_node,
+                 void* stream);
+/* One stream-ordered call (count + fill): per-window sort/dedup/rank on the GPU.
  * Writes win_partition[W], edge_to_col[M], col_offsets[W+1] and
  * col_to_node[0..U) where U = col_offsets[W] (col_to_node capacity must be
  * >= M). Bit-exact with the reference for any blk_h, blk_w >= 1. */
@@ -195,17 +207,26 @@ int tcg_segment_softmax(const int64_t* node_ptr, int64_t num_rows, const float* 
 /* dS = P * (dP - rowsum(P * dP)) (backward; no reference counterpart). */
 int tcg_segment_softmax_backward(const int64_t* node_ptr, int64_t num_rows, const float* p,
                                  const float* dp, float* ds, void* stream);
+/* The same pair under the SURVEY.md Appendix D names. */
+int tcg_softmax_fwd(const int64_t* node_ptr, int64_t num_rows, const float* values, float* out,
+                    void* stream);
+int tcg_softmax_bwd(const int64_t* node_ptr, int64_t num_rows, const float* p, const float* dp,
+                    float* ds, void* stream);
 
 /* ---- fused AGNN layer: reference kernels.agnn_layer (586-601) ----------- */
-/* One warp per window: the window's condensed neighbour rows of Z are
- * gathered once into shared memory and serve both the SDDMM (scores) and,
- * after the in-register row softmax, the weighted SpMM. Writes P[e]
- * (absolute edge ids; kept for the backward) and Y rows. Windows that do
- * not fit (max_window_edges > 256 or more condensed columns than one staged
- * round, or dim > 64) run the same two products unfused. TF32, 16x8 only. */
+/* SDDMM -> row softmax -> SpMM with one gather of Z's neighbour rows per
+ * 8-column block. With the block stream attached and dim == 32 this is
+ * agnn_stream<fwd> (scores straight from the SDDMM C fragment into the SpMM
+ * A fragment, online softmax); otherwise the window engine stages each
+ * window's rows once in shared memory, and shapes neither fits run the two
+ * products unfused. Writes P[e] (absolute edge ids; kept for the backward)
+ * and Y rows [win_begin, win_end) at y - y_row0. TF32, 16x8 only. */
 int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim, float* p,
                      float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
                      void* stream);
+/* SURVEY.md Appendix D form: the whole graph, Z dense with row stride dim. */
+int tcg_agnn_fused_fwd(const tcg_tiling* t, const float* z, int64_t dim, float* p, float* y,
+                       int64_t ldy, void* stream);
 /* AGNN backward, A-side half (no reference counterpart):
  * dS = P * (dP - rowsum(P dP)) with dP_e = <G_row, Z_col> (written to ds),
  * and dZ rows = A_dS Z (overwritten). The A^T half (A^T_P G + A^T_dS Z) is

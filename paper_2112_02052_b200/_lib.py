@@ -63,6 +63,8 @@ SIGNATURES = {
     "tcg_structure_blocks": (C.c_int, [C.POINTER(TcgTiling), _I64, _P, _P, _P]),
     "tcg_sgt_workspace_bytes": (_SZ, [_I64, _I64, _I32]),
     "tcg_sgt": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
+    "tcg_sgt_count": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _SZ, _P]),
+    "tcg_sgt_fill": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
     "tcg_edge_frag": (C.c_int, [C.POINTER(TcgTiling), _P, _P]),
     "tcg_edge_to_row": (C.c_int, [_P, _I64, _I32, _P, _P]),
     "tcg_block_stream": (C.c_int, [C.POINTER(TcgTiling), _P, _P, _P]),
@@ -76,6 +78,9 @@ SIGNATURES = {
                             _I32, _I32, _P]),
     "tcg_segment_softmax": (C.c_int, [_P, _I64, _P, _P, _P]),
     "tcg_segment_softmax_backward": (C.c_int, [_P, _I64, _P, _P, _P, _P]),
+    "tcg_softmax_fwd": (C.c_int, [_P, _I64, _P, _P, _P]),
+    "tcg_softmax_bwd": (C.c_int, [_P, _I64, _P, _P, _P, _P]),
+    "tcg_agnn_fused_fwd": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _P, _P, _I64, _P]),
     "tcg_agnn_forward": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _I64, _P, _P, _I64, _I64,
                                    _I64, _I64, _P]),
     "tcg_agnn_backward": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _P, _I64, _I64, _P, _P,

@@ -325,3 +325,14 @@ extern "C" int tcg_csr_transpose(const int64_t* node_ptr, const uint32_t* edge_l
   launch_counter().fetch_add(1, std::memory_order_relaxed);
   return TCG_OK;
 }
+
+// SURVEY.md Appendix D names of the segment-softmax pair.
+extern "C" int tcg_softmax_fwd(const int64_t* node_ptr, int64_t num_rows, const float* values,
+                               float* out, void* stream) {
+  return tcg_segment_softmax(node_ptr, num_rows, values, out, stream);
+}
+
+extern "C" int tcg_softmax_bwd(const int64_t* node_ptr, int64_t num_rows, const float* p,
+                               const float* dp, float* ds, void* stream) {
+  return tcg_segment_softmax_backward(node_ptr, num_rows, p, dp, ds, stream);
+}

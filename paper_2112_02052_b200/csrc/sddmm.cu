@@ -307,3 +307,10 @@ extern "C" int tcg_edge_frag(const tcg_tiling* t, uint32_t* edge_frag, void* str
   TCG_REQUIRE(t->node_ptr && t->edge_to_col && edge_frag, "tcg_edge_frag: null pointer");
   return win::edge_frag(t->node_ptr, t->edge_to_col, t->num_nodes, edge_frag, as_stream(stream));
 }
+
+// SURVEY.md Appendix D form of the fused AGNN forward: whole graph, dense Z.
+extern "C" int tcg_agnn_fused_fwd(const tcg_tiling* t, const float* z, int64_t dim, float* p,
+                                  float* y, int64_t ldy, void* stream) {
+  TCG_REQUIRE(t != nullptr, "tcg_agnn_fused_fwd: null tiling");
+  return tcg_agnn_forward(t, z, dim, dim, p, y, ldy, 0, 0, t->num_windows, stream);
+}

@@ -8,7 +8,7 @@
 // win_partition[w] = ceil(u_w / blk_w). Ranks are order-independent, so any
 // correct sort yields bit-exact reference output.
 //
-// Kernels (one stream-ordered tcg_sgt call):
+// Kernels (tcg_sgt = tcg_sgt_count + tcg_sgt_fill, stream-ordered):
 //   sgt_rank     one CTA per window: (col<<32 | local edge) keys -> smem
 //                bitonic sort -> head flags -> block scan -> edge_to_col,
 //                u_w. Windows with more than kSmemCap edges are queued.
@@ -197,10 +197,12 @@ extern "C" size_t tcg_sgt_workspace_bytes(int64_t num_nodes, int64_t num_edges, 
   return sgt_layout(num_nodes, W).total;
 }
 
-extern "C" int tcg_sgt(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_nodes,
-                       int64_t num_edges, int32_t blk_h, int32_t blk_w, uint32_t* win_partition,
-                       uint32_t* edge_to_col, int64_t* col_offsets, uint32_t* col_to_node,
-                       void* workspace, size_t workspace_bytes, void* stream) {
+// Phase 1 of SGT: ranks (edge_to_col), per-window unique counts and their
+// exclusive scan (col_offsets[W+1]; U = col_offsets[W]).
+extern "C" int tcg_sgt_count(const int64_t* node_ptr, const uint32_t* edge_list,
+                             int64_t num_nodes, int64_t num_edges, int32_t blk_h, int32_t blk_w,
+                             uint32_t* edge_to_col, int64_t* col_offsets, void* workspace,
+                             size_t workspace_bytes, void* stream) {
   TCG_REQUIRE(blk_h >= 1 && blk_w >= 1, "tcg_sgt: tile shape must be >= 1, got %dx%d", blk_h,
               blk_w);
   TCG_REQUIRE(num_nodes >= 0 && num_edges >= 0, "tcg_sgt: negative size");
@@ -216,11 +218,11 @@ extern "C" int tcg_sgt(const int64_t* node_ptr, const uint32_t* edge_list, int64
   int* big_count = reinterpret_cast<int*>(ws + L.big_count);
   int* big_list = reinterpret_cast<int*>(ws + L.big_list);
   if (W == 0) return TCG_OK;
-  TCG_REQUIRE(node_ptr && col_offsets && win_partition, "tcg_sgt: null pointer");
+  TCG_REQUIRE(node_ptr && col_offsets, "tcg_sgt: null pointer");
   TCG_CUDA(cudaMemsetAsync(ws + L.ucount, 0, sizeof(int64_t) * (W + 1), s), "tcg_sgt memset");
   TCG_CUDA(cudaMemsetAsync(big_count, 0, sizeof(int), s), "tcg_sgt memset");
   if (num_edges > 0) {
-    TCG_REQUIRE(edge_list && edge_to_col && col_to_node, "tcg_sgt: null pointer");
+    TCG_REQUIRE(edge_list && edge_to_col, "tcg_sgt: null pointer");
     const int64_t grid = W < 65535LL * 16 ? W : 65535LL * 16;
     sgt_rank<<<(unsigned)grid, kRankThreads, 0, s>>>(node_ptr, edge_list, num_nodes, W, blk_h,
                                                      edge_to_col, ucount, big_list, big_count);
@@ -235,11 +237,38 @@ extern "C" int tcg_sgt(const int64_t* node_ptr, const uint32_t* edge_list, int64
                                          (int)(W + 1), s),
            "tcg_sgt scan");
   launch_counter().fetch_add(1, std::memory_order_relaxed);
+  return TCG_OK;
+}
+
+// Phase 2: col_to_node[U] (caller-sized from col_offsets[W]) and win_partition.
+extern "C" int tcg_sgt_fill(const int64_t* node_ptr, const uint32_t* edge_list,
+                            int64_t num_nodes, int64_t num_edges, int32_t blk_h, int32_t blk_w,
+                            const uint32_t* edge_to_col, const int64_t* col_offsets,
+                            uint32_t* win_partition, uint32_t* col_to_node, void* stream) {
+  TCG_REQUIRE(blk_h >= 1 && blk_w >= 1, "tcg_sgt: tile shape must be >= 1, got %dx%d", blk_h,
+              blk_w);
+  TCG_REQUIRE(num_nodes >= 0 && num_edges >= 0, "tcg_sgt: negative size");
+  const int64_t W = (num_nodes + blk_h - 1) / blk_h;
+  if (W == 0) return TCG_OK;
+  TCG_REQUIRE(node_ptr && col_offsets && win_partition, "tcg_sgt: null pointer");
+  TCG_REQUIRE(num_edges == 0 || (edge_list && edge_to_col && col_to_node),
+              "tcg_sgt: null pointer");
   const int threads = 256;
   const int64_t blocks = (W * 32 + threads - 1) / threads;
-  sgt_fill<<<(unsigned)blocks, threads, 0, s>>>(node_ptr, edge_list, num_nodes, W, blk_h, blk_w,
-                                                edge_to_col, col_offsets, col_to_node,
-                                                win_partition);
+  sgt_fill<<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(
+      node_ptr, edge_list, num_nodes, W, blk_h, blk_w, edge_to_col, col_offsets, col_to_node,
+      win_partition);
   TCG_LAUNCHED("sgt_fill");
   return TCG_OK;
+}
+
+extern "C" int tcg_sgt(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_nodes,
+                       int64_t num_edges, int32_t blk_h, int32_t blk_w, uint32_t* win_partition,
+                       uint32_t* edge_to_col, int64_t* col_offsets, uint32_t* col_to_node,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  const int rc = tcg_sgt_count(node_ptr, edge_list, num_nodes, num_edges, blk_h, blk_w,
+                               edge_to_col, col_offsets, workspace, workspace_bytes, stream);
+  if (rc != TCG_OK) return rc;
+  return tcg_sgt_fill(node_ptr, edge_list, num_nodes, num_edges, blk_h, blk_w, edge_to_col,
+                      col_offsets, win_partition, col_to_node, stream);
 }

@@ -129,7 +129,10 @@ struct Cfg {
   static constexpr int NI = 2 * NB;                // column-id ring
   static constexpr int SLOT = 8 * 32 * NT;         // bytes of one operand's block
   static constexpr int OPS = DUAL ? 2 : 1;
-  static constexpr int MB = (DUAL || BIG) ? 8 : 16;  // A-fragment blocks resident (one round)
+#ifndef TCG_SPMM_MB
+#define TCG_SPMM_MB 16
+#endif
+  static constexpr int MB = (DUAL || BIG) ? 8 : TCG_SPMM_MB;  // A-fragment blocks resident (one round)
   static constexpr int RING = NB * SLOT * OPS;
   static constexpr int IDX = NI * 32;              // column-id pairs of NI blocks
   static constexpr int AFR = MB * 512 * OPS;
@@ -162,7 +165,11 @@ __device__ __forceinline__ int warp_lower_bound(const int32_t* __restrict__ a, i
 }
 
 template <int NT, bool DUAL, bool BIG, bool MASK>
-__global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32) spmm_stream(const Args a) {
+#ifndef TCG_SPMM_MINB
+#define TCG_SPMM_MINB 1
+#endif
+__global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32,
+                                  (DUAL || BIG) ? 1 : TCG_SPMM_MINB) spmm_stream(const Args a) {
   using C = Cfg<NT, DUAL, BIG>;
   constexpr int NB = C::NB, NI = C::NI, SLOT = C::SLOT, MB = C::MB;
   constexpr uint32_t RS = MB * 128;  // fragment slots of one round

@@ -239,13 +239,17 @@ def _sgt_device(ptr, cols, n: int, m: int, cfg: BlockConfig, graph) -> TiledGrap
     wp = torch.empty(max(W, 1), dtype=torch.int32, device=dev)
     e2c = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
     offs = torch.empty(W + 1, dtype=torch.int64, device=dev)
-    c2n = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
     wsb = int(lib.tcg_sgt_workspace_bytes(n, m, cfg.blk_h))
     ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
-    _lib.check(lib.tcg_sgt(ptr.data_ptr(), cols.data_ptr() if m else None, n, m, cfg.blk_h,
-                           cfg.blk_w, wp.data_ptr(), e2c.data_ptr(), offs.data_ptr(),
-                           c2n.data_ptr(), ws.data_ptr(), wsb, _stream_ptr()), "tcg_sgt")
+    cp = cols.data_ptr() if m else None
+    # two-phase: ranks + scanned counts, then col_to_node sized exactly U
+    _lib.check(lib.tcg_sgt_count(ptr.data_ptr(), cp, n, m, cfg.blk_h, cfg.blk_w, e2c.data_ptr(),
+                                 offs.data_ptr(), ws.data_ptr(), wsb, _stream_ptr()), "tcg_sgt")
     u = int(offs[-1].item()) if W else 0
+    c2n = torch.empty(max(u, 1), dtype=torch.int32, device=dev)
+    _lib.check(lib.tcg_sgt_fill(ptr.data_ptr(), cp, n, m, cfg.blk_h, cfg.blk_w, e2c.data_ptr(),
+                                offs.data_ptr(), wp.data_ptr(), c2n.data_ptr(), _stream_ptr()),
+               "tcg_sgt")
     t = TiledGraph(graph, cfg, n, m, W)
     t.dev.update(node_ptr=ptr, edge_list=cols, win_partition=wp[:W], edge_to_col=e2c[:m],
                  col_offsets=offs, col_to_node=c2n[:u], num_unique=u)
