@@ -126,7 +126,13 @@ constexpr int kEPL = 5;    // edges per lane prefetched for the next window (160
 template <int NT, bool DUAL, bool BIG = false>
 struct Cfg {
   static constexpr int NB = 4;                     // ring depth (blocks)
-  static constexpr int NI = 2 * NB;                // column-id ring
+#ifndef TCG_SPMM_NI
+#define TCG_SPMM_NI 8
+#endif
+  // column-id ring: ids of block s + NI are requested at step s (NI >= 2 NB so
+  // the ids of block s + NB have landed by then); power of two
+  static constexpr int NI = TCG_SPMM_NI;
+  static_assert(NI >= 2 * NB && (NI & (NI - 1)) == 0, "column-id ring depth");
   static constexpr int SLOT = 8 * 32 * NT;         // bytes of one operand's block
   static constexpr int OPS = DUAL ? 2 : 1;
 #ifndef TCG_SPMM_MB
@@ -233,18 +239,18 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32,
     }
   };
   if (lane < 2)
-    for (int s = 0; s < NB; ++s) cp_async<16>(is + s * 32, csl + 32 * s);
+    for (int s = 0; s < NI - NB; ++s) cp_async<16>(is + s * 32, csl + 32 * s);
   cp_commit();
   cp_wait<0>();
   __syncwarp();
   for (int s = 0; s < NB; ++s) {
     issue_x(s * SLOT * C::OPS, s * 32);
-    if (lane < 2) cp_async<16>(is + (s + NB) * 32, csl + 32 * (s + NB));
+    if (lane < 2) cp_async<16>(is + (s + NI - NB) * 32, csl + 32 * (s + NI - NB));
     cp_commit();
   }
-  // ring cursors of the consumed block s: X slot, id slot of s + NB, id slot of s + 2NB
+  // ring cursors of the consumed block s: X slot, id slot of s + NB, id slot of s + NI
   uint32_t xo = 0, io = NB * 32, iw = 0;
-  const char* cnext = csl + 32 * 2 * NB;
+  const char* cnext = csl + 32 * NI;
 
   // ---- window metadata, rolled 3 windows ahead ----
   auto ptr_of = [&](int w) { return (int64_t)__ldg(a.ptr + min((int64_t)w * 16, a.n)); };
