@@ -267,11 +267,22 @@ size_t tcg_gemm_tn_workspace_bytes(int64_t n, int64_t k, int64_t c);
 int tcg_gemm_tn(const float* a, int64_t lda, const float* b, int64_t ldb, const float* mask,
                 int64_t ldm, int64_t n, int64_t k, int64_t c, float* out, float* colsum,
                 void* workspace, size_t workspace_bytes, void* stream);
+size_t tcg_colsum_workspace_bytes(int64_t n, int64_t c);
+/* out[c] = column sums of x[n x c] (row stride ld); fixed-order two-level
+ * reduction (deterministic). The bias gradient of gcn_layer's `+ b`. */
+int tcg_colsum(const float* x, int64_t ld, int64_t n, int64_t c, float* out, void* workspace,
+               size_t workspace_bytes, void* stream);
 size_t tcg_softmax_xent_workspace_bytes(int64_t n);
-/* loss = mean_i -log_softmax(logits_i)[labels_i]; dlogits = (softmax - onehot)/n */
+/* loss = mean_i -log_softmax(logits_i)[labels_i]; dlogits = (softmax - onehot)/n
+ * (dlogits may be null: loss only) */
 int tcg_softmax_xent(const float* logits, int64_t ld, const int64_t* labels, int64_t n, int64_t c,
                      float* loss, float* dlogits, void* workspace, size_t workspace_bytes,
                      void* stream);
+/* dlogits[n x c] = (softmax(logits) - onehot(labels)) / n * g, g = *grad_scale
+ * (device scalar; null => 1): the backward recomputes the softmax from the
+ * logits instead of keeping dlogits from the forward */
+int tcg_softmax_xent_backward(const float* logits, int64_t ld, const int64_t* labels, int64_t n,
+                              int64_t c, const float* grad_scale, float* dlogits, void* stream);
 
 /* ---- TF32 operand rounding: reference tiles.quantize_tf32 (67-82) ------- */
 int tcg_quantize_tf32(const float* in, float* out, int64_t n, void* stream);

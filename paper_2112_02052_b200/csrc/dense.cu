@@ -16,6 +16,8 @@
 //    two-level reduction.
 // All fp32 FMA (no TF32) so the GEMMs keep full fp32 accuracy (SURVEY.md
 // fact 8: TF32 GEMMs would push the 4-layer AGNN past the 5e-3 budget).
+#include <type_traits>
+
 #include "common.cuh"
 #include "dense_rows.cuh"
 
@@ -167,13 +169,15 @@ __global__ void __launch_bounds__(1024) sum_slabs(const float* __restrict__ part
   }
 }
 
-// One warp per row: log-softmax, NLL, dlogits; per-CTA loss partials.
-// 8 lanes per row (32 rows per CTA); the 8 row losses of each lpart entry are
-// summed in row order, so the mean stays a fixed-order reduction.
+// 8 lanes per row (32 rows per CTA): log-softmax, then the NLL of the label
+// (LOSS: per-CTA partials; the 8 row losses of each lpart entry are summed in
+// row order, so the mean stays a fixed-order reduction) and/or
+// dlogits = (softmax - onehot) / n * g (GRAD; g = *gscale or 1).
+template <bool LOSS, bool GRAD>
 __global__ void __launch_bounds__(256)
     softmax_xent(const float* __restrict__ logits, int64_t ld, const int64_t* __restrict__ labels,
-                 int64_t n, int c, float* __restrict__ dlogits, float* __restrict__ lpart,
-                 int64_t parts) {
+                 int64_t n, int c, float* __restrict__ dlogits, const float* __restrict__ gscale,
+                 float* __restrict__ lpart, int64_t parts) {
   __shared__ float rowc[32];
   const int sub = threadIdx.x & 7, lr_ = threadIdx.x >> 3;
   const int64_t row = (int64_t)blockIdx.x * 32 + lr_;
@@ -191,13 +195,16 @@ __global__ void __launch_bounds__(256)
     for (int o = 4; o > 0; o >>= 1) sm += __shfl_xor_sync(gm, sm, o);
     const float lse = mx + logf(sm);
     const int64_t lab = labels[row];
-    const float inv_n = 1.f / (float)n;
-    for (int j = sub; j < c; j += 8) {
-      const float pj = expf(__ldg(lr + j) - lse);
-      dlogits[row * c + j] = (pj - (j == lab ? 1.f : 0.f)) * inv_n;
+    if constexpr (GRAD) {
+      const float inv_n = (gscale ? __ldg(gscale) : 1.f) / (float)n;
+      for (int j = sub; j < c; j += 8) {
+        const float pj = expf(__ldg(lr + j) - lse);
+        dlogits[row * c + j] = (pj - (j == lab ? 1.f : 0.f)) * inv_n;
+      }
     }
     contrib = lse - lr[lab];
   }
+  if constexpr (!LOSS) return;
   if (sub == 0) rowc[lr_] = contrib;
   __syncthreads();
   if (threadIdx.x < 4) {
@@ -379,6 +386,59 @@ int fast_gemm_tn(const float* a, int64_t lda, const float* b, int64_t ldb, const
   return 1;
 }
 
+// Column sums of x[n x c] (row stride ld), first level: CTA `slab` sums rows
+// [slab*rows, (slab+1)*rows). Thread (lane r, column unit j) adds rows r,
+// r+RL, ... of its V columns (V = 4: float4 loads when c, ld are multiples of
+// 4) with 8 independent partials in flight; the RL lane partials are then added
+// in lane order, so the result is deterministic.
+template <int V>
+__global__ void __launch_bounds__(256)
+    colsum_part(const float* __restrict__ x, int64_t ld, int64_t n, int c, int64_t rows,
+                float* __restrict__ part) {
+  using VT = typename std::conditional<V == 4, float4, float>::type;
+  __shared__ VT sh[256];
+  const int units = c / V;
+  const int64_t r0 = (int64_t)blockIdx.x * rows, r1 = min(n, r0 + rows);
+  auto add = [](VT& a, const VT& b) {
+    if constexpr (V == 4) a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
+    else a += b;
+  };
+  for (int ub = 0; ub < units; ub += 256) {
+    const int uw = min(256, units - ub);
+    const int rl = 256 / uw;
+    const int lane_r = threadIdx.x / uw, j = threadIdx.x % uw;
+    VT sp[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) sp[u] = VT{};
+    if (lane_r < rl) {
+      const VT* col = reinterpret_cast<const VT*>(x) + ub + j;
+      const int64_t ldv = ld / V;
+      int64_t r = r0 + lane_r;
+      for (; r + 7 * rl < r1; r += 8 * rl) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) add(sp[u], __ldg(col + (r + u * rl) * ldv));
+      }
+      for (; r < r1; r += rl) add(sp[0], __ldg(col + r * ldv));
+    }
+    add(sp[0], sp[1]), add(sp[2], sp[3]), add(sp[4], sp[5]), add(sp[6], sp[7]);
+    add(sp[0], sp[2]), add(sp[4], sp[6]), add(sp[0], sp[4]);
+    sh[threadIdx.x] = sp[0];
+    __syncthreads();
+    if (threadIdx.x < uw) {
+      VT tot = VT{};
+      for (int q = 0; q < rl; ++q) add(tot, sh[q * uw + threadIdx.x]);
+      reinterpret_cast<VT*>(part + (int64_t)blockIdx.x * c)[ub + threadIdx.x] = tot;
+    }
+    __syncthreads();
+  }
+}
+
+int64_t colsum_slabs(int64_t n) {
+  const int64_t s = (n + 1023) / 1024;
+  const int64_t cap = 2LL * num_sms();
+  return s < 1 ? 1 : (s > cap ? cap : s);
+}
+
 int64_t slabs_for(int64_t n) {
   int64_t s = (n + 63) / 64;  // >= 64 rows per slab; ~4 CTAs per SM per output tile
   const int64_t cap = 4LL * num_sms();
@@ -471,14 +531,58 @@ extern "C" int tcg_softmax_xent(const float* logits, int64_t ld, const int64_t* 
   TCG_REQUIRE(n >= 1 && c >= 1 && ld >= c, "tcg_softmax_xent: bad shape");
   TCG_REQUIRE(workspace_bytes >= tcg_softmax_xent_workspace_bytes(n),
               "tcg_softmax_xent: workspace too small");
-  TCG_REQUIRE(logits && labels && loss && dlogits, "tcg_softmax_xent: null pointer");
+  TCG_REQUIRE(logits && labels && loss, "tcg_softmax_xent: null pointer");
   cudaStream_t s = as_stream(stream);
   const int64_t parts = (n + 7) / 8;
   float* lpart = static_cast<float*>(workspace);
-  softmax_xent<<<(unsigned)((n + 31) / 32), 256, 0, s>>>(logits, ld, labels, n, (int)c, dlogits,
-                                                          lpart, parts);
+  const unsigned grid = (unsigned)((n + 31) / 32);
+  if (dlogits)
+    softmax_xent<true, true><<<grid, 256, 0, s>>>(logits, ld, labels, n, (int)c, dlogits, nullptr,
+                                                  lpart, parts);
+  else
+    softmax_xent<true, false><<<grid, 256, 0, s>>>(logits, ld, labels, n, (int)c, nullptr,
+                                                   nullptr, lpart, parts);
   TCG_LAUNCHED("softmax_xent");
   final_loss<<<1, 256, 0, s>>>(lpart, parts, n, loss);
   TCG_LAUNCHED("final_loss");
+  return TCG_OK;
+}
+
+extern "C" int tcg_softmax_xent_backward(const float* logits, int64_t ld, const int64_t* labels,
+                                         int64_t n, int64_t c, const float* grad_scale,
+                                         float* dlogits, void* stream) {
+  TCG_REQUIRE(n >= 1 && c >= 1 && ld >= c, "tcg_softmax_xent_backward: bad shape");
+  TCG_REQUIRE(logits && labels && dlogits, "tcg_softmax_xent_backward: null pointer");
+  softmax_xent<false, true><<<(unsigned)((n + 31) / 32), 256, 0, as_stream(stream)>>>(
+      logits, ld, labels, n, (int)c, dlogits, grad_scale, nullptr, 0);
+  TCG_LAUNCHED("softmax_xent_backward");
+  return TCG_OK;
+}
+
+extern "C" size_t tcg_colsum_workspace_bytes(int64_t n, int64_t c) {
+  return (size_t)(colsum_slabs(n) * (c > 0 ? c : 1)) * sizeof(float);
+}
+
+extern "C" int tcg_colsum(const float* x, int64_t ld, int64_t n, int64_t c, float* out,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  TCG_REQUIRE(n >= 0 && c >= 1 && ld >= c, "tcg_colsum: bad shape");
+  TCG_REQUIRE(workspace_bytes >= tcg_colsum_workspace_bytes(n, c), "tcg_colsum: workspace too small");
+  TCG_REQUIRE(out && workspace && (n == 0 || x), "tcg_colsum: null pointer");
+  cudaStream_t s = as_stream(stream);
+  if (n == 0) {
+    TCG_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * c, s), "tcg_colsum memset");
+    return TCG_OK;
+  }
+  const int64_t slabs = colsum_slabs(n);
+  const int64_t rows = (n + slabs - 1) / slabs;
+  float* part = static_cast<float*>(workspace);
+  const bool v4 = c % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  if (v4)
+    colsum_part<4><<<(unsigned)slabs, 256, 0, s>>>(x, ld, n, (int)c, rows, part);
+  else
+    colsum_part<1><<<(unsigned)slabs, 256, 0, s>>>(x, ld, n, (int)c, rows, part);
+  TCG_LAUNCHED("colsum_part");
+  sum_slabs<<<(unsigned)((c + 31) / 32), 1024, 0, s>>>(part, (int)slabs, c, out);
+  TCG_LAUNCHED("sum_slabs");
   return TCG_OK;
 }

@@ -6,7 +6,7 @@ hundred) and the softmax cross-entropy loss, as torch.autograd Functions:
   DenseFn       y = act(x W + b);  dx = (g .* [y > 0]) W^T,
                 dW = x^T (g .* [y > 0]), db = colsum(g .* [y > 0])
   SoftmaxXentFn loss = mean -log_softmax(logits)[label];
-                dlogits = (softmax - onehot) / n  (computed in the forward)
+                dlogits = (softmax - onehot) / n * g  (recomputed in the backward)
 
 All reductions are fixed-order (deterministic); no TF32.
 """
@@ -59,18 +59,44 @@ def gemm_tn(a, b, mask=None, colsum=False):
     return out, cs
 
 
-def softmax_xent(logits, labels):
-    """(mean NLL of log_softmax, dlogits)."""
+def colsum(x):
+    """Column sums of a 2-D device tensor (fixed-order, deterministic)."""
+    lib = _lib.load()
+    n, c = x.shape
+    if x.stride(1) != 1:
+        x = x.contiguous()
+    out = torch.empty(c, dtype=torch.float32, device=x.device)
+    wsb = int(lib.tcg_colsum_workspace_bytes(n, c))
+    ws = torch.empty(max(wsb // 4, 1), dtype=torch.float32, device=x.device)
+    _lib.check(lib.tcg_colsum(x.data_ptr(), x.stride(0), n, c, out.data_ptr(), ws.data_ptr(), wsb,
+                              _stream()), "tcg_colsum")
+    return out
+
+
+def softmax_xent(logits, labels, grad=True):
+    """(mean NLL of log_softmax, dlogits or None)."""
     lib = _lib.load()
     n, c = logits.shape
     loss = torch.empty((), dtype=torch.float32, device=logits.device)
-    dl = torch.empty((n, c), dtype=torch.float32, device=logits.device)
+    dl = torch.empty((n, c), dtype=torch.float32, device=logits.device) if grad else None
     wsb = int(lib.tcg_softmax_xent_workspace_bytes(n))
     ws = torch.empty(max(wsb // 4, 1), dtype=torch.float32, device=logits.device)
     _lib.check(lib.tcg_softmax_xent(logits.data_ptr(), logits.stride(0), labels.data_ptr(), n, c,
-                                    loss.data_ptr(), dl.data_ptr(), ws.data_ptr(), wsb, _stream()),
+                                    loss.data_ptr(), _p(dl), ws.data_ptr(), wsb, _stream()),
                "tcg_softmax_xent")
     return loss, dl
+
+
+def softmax_xent_backward(logits, labels, grad_scale=None):
+    """(softmax(logits) - onehot(labels)) / n * grad_scale (a device scalar)."""
+    lib = _lib.load()
+    n, c = logits.shape
+    dl = torch.empty((n, c), dtype=torch.float32, device=logits.device)
+    gs = None if grad_scale is None else grad_scale.float().contiguous()
+    _lib.check(lib.tcg_softmax_xent_backward(logits.data_ptr(), logits.stride(0),
+                                             labels.data_ptr(), n, c, _p(gs), dl.data_ptr(),
+                                             _stream()), "tcg_softmax_xent_backward")
+    return dl
 
 
 class DenseFn(torch.autograd.Function):
@@ -98,14 +124,18 @@ class DenseFn(torch.autograd.Function):
 class SoftmaxXentFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, logits, labels):
-        loss, dl = softmax_xent(logits.contiguous(), labels)
-        ctx.save_for_backward(dl)
+        # loss only; the backward recomputes the softmax from the logits
+        # (one read of the logits instead of writing dlogits, re-reading and
+        # scaling it by the incoming gradient)
+        logits = logits.contiguous()
+        loss, _ = softmax_xent(logits, labels, grad=False)
+        ctx.save_for_backward(logits, labels)
         return loss
 
     @staticmethod
     def backward(ctx, g):
-        (dl,) = ctx.saved_tensors
-        return dl * g, None
+        logits, labels = ctx.saved_tensors
+        return softmax_xent_backward(logits, labels, g), None
 
 
 class Linear(nn.Module):

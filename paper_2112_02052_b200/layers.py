@@ -31,7 +31,7 @@ import torch.nn.functional as F
 
 from . import _lib
 from .dist import ShardPlan, allgather_edges, allgather_rows
-from .dense import DenseFn, Linear, cross_entropy  # noqa: F401  (re-exported)
+from .dense import DenseFn, Linear, colsum, cross_entropy  # noqa: F401  (re-exported)
 from .kernels import (
     agnn_backward_device,
     agnn_forward_device,
@@ -102,7 +102,7 @@ class GcnAggregate(torch.autograd.Function):
             wt = t._aux[key]
         spmm_device(tt.tiled, g, wt, mode=ctx.mode, out=out, win_range=wr, y_row0=r0)
         dh = _finish_rows(out, shard)
-        db = g.sum(0) if ctx.has_bias else None
+        db = colsum(g) if ctx.has_bias else None
         return dh, db, None, None, None
 
 

@@ -45,6 +45,22 @@ def test_dense_forward_backward_kernels(env, n, ci, co):
     assert torch.equal(dw, dw2)
 
 
+@pytest.mark.parametrize("n,c,ld", [(169343, 16, 16), (5000, 47, 48), (1000, 300, 300),
+                                    (7, 3, 3), (0, 5, 5), (100000, 40, 40)])
+def test_colsum(env, n, c, ld):
+    _, dense, _, torch = env
+    buf = torch.randn(max(n, 1), ld, device="cuda")[:n]
+    x = buf[:, :c]
+    got = dense.colsum(x)
+    ref = x.double().sum(0)
+    assert got.shape == (c,)
+    if n:
+        assert rel_l2(got.cpu().numpy(), ref.cpu().numpy()) < 1e-6
+    else:
+        assert torch.equal(got, torch.zeros(c, device="cuda"))
+    assert torch.equal(got, dense.colsum(x))  # deterministic
+
+
 def test_softmax_xent(env):
     _, dense, _, torch = env
     logits = torch.randn(5000, 40, device="cuda") * 3
@@ -55,6 +71,17 @@ def test_softmax_xent(env):
     ref.backward()
     assert abs(float(loss) - float(ref)) < 1e-5 * max(1.0, abs(float(ref)))
     assert rel_l2(dl.cpu().numpy(), lg.grad.cpu().numpy()) < 1e-5
+    # loss-only forward, backward recomputed from the logits with a device grad scale
+    loss2, none = dense.softmax_xent(logits, labels, grad=False)
+    assert none is None and torch.equal(loss, loss2)
+    g = torch.tensor(2.5, device="cuda")
+    dl2 = dense.softmax_xent_backward(logits, labels, g)
+    assert torch.equal(dl2, dense.softmax_xent_backward(logits, labels, g))
+    assert rel_l2(dl2.cpu().numpy(), 2.5 * lg.grad.cpu().numpy()) < 1e-5
+    # autograd: a scaled loss scales the logits gradient
+    lt = logits.clone().requires_grad_(True)
+    (3.0 * dense.cross_entropy(lt, labels)).backward()
+    assert rel_l2(lt.grad.cpu().numpy(), 3.0 * lg.grad.cpu().numpy()) < 1e-5
 
 
 def _copy_weights_agnn(net, cpu):
