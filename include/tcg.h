@@ -267,6 +267,14 @@ size_t tcg_gemm_tn_workspace_bytes(int64_t n, int64_t k, int64_t c);
 int tcg_gemm_tn(const float* a, int64_t lda, const float* b, int64_t ldb, const float* mask,
                 int64_t ldm, int64_t n, int64_t k, int64_t c, float* out, float* colsum,
                 void* workspace, size_t workspace_bytes, void* stream);
+size_t tcg_dense_backward_workspace_bytes(int64_t n, int64_t ci, int64_t co);
+/* Backward of y = x W (W [ci x co], no bias/activation): dx[n x ci] = g W^T and
+ * dw[ci x co] = x^T g. For ci = co = 32 (the AGNN layers) one fused pass reads
+ * g once for both products; other shapes run tcg_dense + tcg_gemm_tn.
+ * Deterministic (fixed-order reductions). */
+int tcg_dense_backward(const float* x, int64_t ldx, const float* g, int64_t ldg, int64_t n,
+                       int64_t ci, int64_t co, const float* w, float* dx, int64_t lddx, float* dw,
+                       void* workspace, size_t workspace_bytes, void* stream);
 size_t tcg_colsum_workspace_bytes(int64_t n, int64_t c);
 /* out[c] = column sums of x[n x c] (row stride ld); fixed-order two-level
  * reduction (deterministic). The bias gradient of gcn_layer's `+ b`. */

@@ -97,6 +97,9 @@ SIGNATURES = {
     "tcg_gemm_tn_workspace_bytes": (_SZ, [_I64, _I64, _I64]),
     "tcg_gemm_tn": (C.c_int, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _SZ,
                               _P]),
+    "tcg_dense_backward_workspace_bytes": (_SZ, [_I64, _I64, _I64]),
+    "tcg_dense_backward": (C.c_int, [_P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P,
+                                     _SZ, _P]),
     "tcg_colsum_workspace_bytes": (_SZ, [_I64, _I64]),
     "tcg_colsum": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _SZ, _P]),
     "tcg_softmax_xent_workspace_bytes": (_SZ, [_I64]),

@@ -586,3 +586,53 @@ extern "C" int tcg_colsum(const float* x, int64_t ld, int64_t n, int64_t c, floa
   TCG_LAUNCHED("sum_slabs");
   return TCG_OK;
 }
+
+extern "C" size_t tcg_dense_backward_workspace_bytes(int64_t n, int64_t ci, int64_t co) {
+  const size_t fused = (size_t)4 * num_sms() * ci * co * sizeof(float);
+  const size_t split = tcg_gemm_tn_workspace_bytes(n, ci, co);
+  return fused > split ? fused : split;
+}
+
+extern "C" int tcg_dense_backward(const float* x, int64_t ldx, const float* g, int64_t ldg,
+                                  int64_t n, int64_t ci, int64_t co, const float* w, float* dx,
+                                  int64_t lddx, float* dw, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  TCG_REQUIRE(n >= 0 && ci >= 1 && co >= 1 && ldx >= ci && ldg >= co && lddx >= ci,
+              "tcg_dense_backward: bad shape");
+  TCG_REQUIRE(workspace_bytes >= tcg_dense_backward_workspace_bytes(n, ci, co),
+              "tcg_dense_backward: workspace too small");
+  TCG_REQUIRE(w && dw && workspace && (n == 0 || (x && g && dx)),
+              "tcg_dense_backward: null pointer");
+  cudaStream_t s = as_stream(stream);
+  if (n == 0) {
+    TCG_CUDA(cudaMemsetAsync(dw, 0, sizeof(float) * ci * co, s), "tcg_dense_backward memset");
+    return TCG_OK;
+  }
+  const bool fused = ci == 32 && co == 32 && n > 0 && ldx % 4 == 0 && ldg % 4 == 0 &&
+                     lddx % 4 == 0 && al16(x) && al16(g) && al16(dx);
+  if (!fused) {
+    const int rc = tcg_dense(g, ldg, n, co, w, ci, 1, nullptr, 0, nullptr, 0, dx, lddx, stream);
+    if (rc != TCG_OK) return rc;
+    return tcg_gemm_tn(x, ldx, g, ldg, nullptr, 0, n, ci, co, dw, nullptr, workspace,
+                       workspace_bytes, stream);
+  }
+  using Cfg = dr::BwdCfg<32, 32>;
+  static int dev_done = -1, per_sm = 1;
+  int dev = 0;
+  TCG_CUDA(cudaGetDevice(&dev), "dense device");
+  if (dev_done != dev) {
+    const int rc = set_smem(dr::dense_bwd_tile<32, 32>, Cfg::SMEM, Cfg::NT, &per_sm);
+    if (rc != TCG_OK) return rc;
+    dev_done = dev;
+  }
+  int64_t blocks = (n + Cfg::ROWS - 1) / Cfg::ROWS;
+  int64_t cap = (int64_t)num_sms() * (per_sm < 4 ? per_sm : 4);
+  if (blocks > cap) blocks = cap;
+  float* part = static_cast<float*>(workspace);
+  dr::dense_bwd_tile<32, 32><<<(unsigned)blocks, Cfg::NT, Cfg::SMEM, s>>>(x, ldx, g, ldg, n, w,
+                                                                          dx, lddx, part);
+  TCG_LAUNCHED("dense_bwd_tile");
+  sum_slabs<<<(unsigned)((ci * co + 31) / 32), 1024, 0, s>>>(part, (int)blocks, ci * co, dw);
+  TCG_LAUNCHED("sum_slabs");
+  return TCG_OK;
+}

@@ -282,5 +282,145 @@ __global__ void __launch_bounds__(GemmCfg<CI, CO, MASK>::NT)
     }
 }
 
+// Fused backward of y = x W (no activation), W [CI x CO]: one pass over the
+// 128-row tiles of x [n x CI] and g [n x CO] computes
+//   dx = g W^T  (thread (rg, q): rows rg + 32 j, columns 4q..4q+3, the
+//               dense_tile<CO, CI, TRANS> dataflow and fold order), and
+//   part[blockIdx] = x^T g over this CTA's tiles (thread (og, rq): a 4 x 4
+//               block of dW over a quarter of each tile's rows; the row groups
+//               are reduced in a fixed order, as gemm_tn_tile),
+// so g is read once for both products. 256 threads: CI / 4 * 32 == 256.
+template <int CI, int CO>
+struct BwdCfg {
+  static constexpr int ROWS = 128;
+  static constexpr int XS = CI + 4, GS = CO + 4;
+  static constexpr int STAGES = 2;  // 78 KB at 32 x 32: two CTAs per SM
+  static constexpr int STAGE = ROWS * (XS + GS);
+  static constexpr int NT = 256;
+  static constexpr int Q = CI / 4;
+  static constexpr int OG = (CI / 4) * (CO / 4);
+  static constexpr int RQ = NT / OG;
+  static_assert(Q * 32 == NT && OG * RQ == NT && ROWS % RQ == 0, "dense_bwd_tile shape");
+  static constexpr size_t SMEM_RING = (size_t)(CO * CI + STAGES * STAGE) * sizeof(float);
+  static constexpr size_t SMEM_RED = (size_t)RQ * CI * CO * sizeof(float);
+  static constexpr size_t SMEM = SMEM_RING > SMEM_RED ? SMEM_RING : SMEM_RED;
+};
+
+template <int CI, int CO>
+__global__ void __launch_bounds__(256)
+    dense_bwd_tile(const float* __restrict__ x, int64_t ldx, const float* __restrict__ g,
+                   int64_t ldg, int64_t n, const float* __restrict__ w, float* __restrict__ dx,
+                   int64_t lddx, float* __restrict__ part) {
+  using C = BwdCfg<CI, CO>;
+  extern __shared__ __align__(16) float sh[];
+  float* wt = sh;               // [CO][CI]: wt[k][c] = W[c][k]
+  float* ring = sh + CO * CI;   // STAGES x ([ROWS][XS] x, [ROWS][GS] g)
+  const int tid = threadIdx.x;
+  for (int i = tid; i < CI * CO; i += C::NT) {
+    const int k = i / CI, c = i % CI;
+    wt[i] = __ldg(w + (int64_t)c * CO + k);
+  }
+  const int64_t ntiles = (n + C::ROWS - 1) / C::ROWS;
+  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto issue = [&](int64_t it) {
+    if (it < my_tiles) {
+      const int64_t tile = blockIdx.x + it * gridDim.x;
+      float* xt = ring + (it % C::STAGES) * C::STAGE;
+      float* gt = xt + C::ROWS * C::XS;
+      for (int i = tid; i < C::ROWS * (CI / 4); i += C::NT) {
+        const int r = i / (CI / 4), c4 = i % (CI / 4);
+        const int64_t gr = tile * C::ROWS + r;
+        const bool ok = gr < n;
+        cp16(xt + r * C::XS + c4 * 4, x + (ok ? gr : 0) * ldx + c4 * 4, ok);
+      }
+      for (int i = tid; i < C::ROWS * (CO / 4); i += C::NT) {
+        const int r = i / (CO / 4), c4 = i % (CO / 4);
+        const int64_t gr = tile * C::ROWS + r;
+        const bool ok = gr < n;
+        cp16(gt + r * C::GS + c4 * 4, g + (ok ? gr : 0) * ldg + c4 * 4, ok);
+      }
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < C::STAGES - 1; ++s) issue(s);
+
+  const int q = tid % C::Q, rg = tid / C::Q;                 // dx role
+  const int og = tid % C::OG, rq = tid / C::OG;              // dW role
+  const int ib = og / (CO / 4), cb = og % (CO / 4);
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
+  constexpr int RPG = C::ROWS / C::RQ;
+  for (int64_t it = 0; it < my_tiles; ++it) {
+    issue(it + C::STAGES - 1);
+    cp_wait<C::STAGES - 1>();
+    __syncthreads();
+    const float* xt = ring + (it % C::STAGES) * C::STAGE;
+    const float* gt = xt + C::ROWS * C::XS;
+    // dx rows of this tile
+    float4 d[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) d[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 2
+    for (int k = 0; k < CO; k += 4) {
+      float4 av[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        av[j] = *reinterpret_cast<const float4*>(gt + (rg + 32 * j) * C::GS + k);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const float4 wv = *reinterpret_cast<const float4*>(wt + (k + kk) * CI + 4 * q);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float a = kk == 0 ? av[j].x : kk == 1 ? av[j].y : kk == 2 ? av[j].z : av[j].w;
+          d[j].x = fmaf(a, wv.x, d[j].x);
+          d[j].y = fmaf(a, wv.y, d[j].y);
+          d[j].z = fmaf(a, wv.z, d[j].z);
+          d[j].w = fmaf(a, wv.w, d[j].w);
+        }
+      }
+    }
+    const int64_t tile = blockIdx.x + it * gridDim.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t row = tile * C::ROWS + rg + 32 * j;
+      if (row < n) *reinterpret_cast<float4*>(dx + row * lddx + 4 * q) = d[j];
+    }
+    // dW partial over this thread's row group
+#pragma unroll 4
+    for (int rr = 0; rr < RPG; ++rr) {
+      const int r = rq * RPG + rr;
+      const float4 av = *reinterpret_cast<const float4*>(xt + r * C::XS + 4 * ib);
+      const float4 bv = *reinterpret_cast<const float4*>(gt + r * C::GS + 4 * cb);
+      const float ai[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i][0] = fmaf(ai[i], bv.x, acc[i][0]);
+        acc[i][1] = fmaf(ai[i], bv.y, acc[i][1]);
+        acc[i][2] = fmaf(ai[i], bv.z, acc[i][2]);
+        acc[i][3] = fmaf(ai[i], bv.w, acc[i][3]);
+      }
+    }
+    __syncthreads();
+  }
+  cp_wait<0>();
+  __syncthreads();
+  float* red = sh;  // [RQ][CI][CO]
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) red[(rq * CI + 4 * ib + i) * CO + 4 * cb + c] = acc[i][c];
+  __syncthreads();
+  float* out = part + (int64_t)blockIdx.x * CI * CO;
+  for (int i = tid; i < CI * CO; i += C::NT) {
+    float s = 0.f;
+    for (int gq = 0; gq < C::RQ; ++gq) s += red[gq * CI * CO + i];
+    out[i] = s;
+  }
+}
+
 }  // namespace dr
 }  // namespace tcg

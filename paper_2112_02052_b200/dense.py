@@ -59,6 +59,22 @@ def gemm_tn(a, b, mask=None, colsum=False):
     return out, cs
 
 
+def dense_backward(x, g, w):
+    """(g W^T, x^T g) for y = x W: one fused pass at 32 x 32 (tcg_dense_backward)."""
+    lib = _lib.load()
+    n, ci = x.shape
+    co = g.shape[1]
+    dx = torch.empty((n, ci), dtype=torch.float32, device=x.device)
+    dw = torch.empty((ci, co), dtype=torch.float32, device=x.device)
+    wsb = int(lib.tcg_dense_backward_workspace_bytes(n, ci, co))
+    ws = torch.empty(max(wsb // 4, 1), dtype=torch.float32, device=x.device)
+    _lib.check(lib.tcg_dense_backward(x.data_ptr(), x.stride(0), g.data_ptr(), g.stride(0), n, ci,
+                                      co, w.data_ptr(), dx.data_ptr(), dx.stride(0),
+                                      dw.data_ptr(), ws.data_ptr(), wsb, _stream()),
+               "tcg_dense_backward")
+    return dx, dw
+
+
 def colsum(x):
     """Column sums of a 2-D device tensor (fixed-order, deterministic)."""
     lib = _lib.load()
@@ -113,6 +129,9 @@ class DenseFn(torch.autograd.Function):
     def backward(ctx, g):
         x, w, y = ctx.saved_tensors
         g = g.contiguous()
+        if not ctx.relu and not ctx.has_b and ctx.needs_input_grad[0]:
+            dx, dw = dense_backward(x, g, w.contiguous())
+            return dx, dw, None, None
         mask = y if ctx.relu else None
         dx = None
         if ctx.needs_input_grad[0]:

@@ -45,6 +45,26 @@ def test_dense_forward_backward_kernels(env, n, ci, co):
     assert torch.equal(dw, dw2)
 
 
+@pytest.mark.parametrize("n,ci,co", [(169343, 32, 32), (1000, 32, 32), (77, 32, 32), (0, 32, 32),
+                                     (5000, 32, 40), (3000, 16, 8)])
+def test_dense_backward(env, n, ci, co):
+    _, dense, _, torch = env
+    gen = torch.Generator(device="cuda").manual_seed(n + ci)
+    x = torch.randn(n, ci, device="cuda", generator=gen)
+    g = torch.randn(n, co, device="cuda", generator=gen)
+    w = torch.randn(ci, co, device="cuda", generator=gen)
+    dx, dw = dense.dense_backward(x, g, w)
+    if n:
+        assert rel_l2(dx.cpu().numpy(), (g.double() @ w.double().T).cpu().numpy()) < 1e-6
+        assert rel_l2(dw.cpu().numpy(), (x.double().T @ g.double()).cpu().numpy()) < 1e-6
+        # the dx fold order is dense_tile's: bitwise equal to the unfused product
+        assert torch.equal(dx, dense.dense(g, w, transposed=True))
+    else:
+        assert torch.equal(dw, torch.zeros_like(dw))
+    dx2, dw2 = dense.dense_backward(x, g, w)
+    assert torch.equal(dx, dx2) and torch.equal(dw, dw2)
+
+
 @pytest.mark.parametrize("n,c,ld", [(169343, 16, 16), (5000, 47, 48), (1000, 300, 300),
                                     (7, 3, 3), (0, 5, 5), (100000, 40, 40)])
 def test_colsum(env, n, c, ld):
