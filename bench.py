@@ -178,6 +178,33 @@ def cpu_epoch_runner(wl):
     return step, workers, g
 
 
+def cpu_ops(workers: int) -> dict:
+    """The per-op CPU times beside the GPU kernels of `extras` (oracle port,
+    arxiv shape, D = 32, best of 2): SGT, TF32 SpMM (weighted), SDDMM."""
+    from oracle import tcg_oracle as o
+    from paper_2112_02052_b200 import synth
+
+    g = synth.shaped_graph("arxiv")
+    ptr, cols, n = g.node_pointer, g.edge_list, g.num_nodes
+    x = synth.random_embeddings(n, 32, seed=2)
+    f = np.full(g.num_edges, 0.5, dtype=np.float32)
+
+    def best(fn):
+        ts = []
+        for _ in range(2):
+            s0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - s0)
+        return round(1000 * min(ts), 1)
+
+    return {
+        "sgt": best(lambda: o.translate(ptr, cols, n, 16, 8)),
+        "spmm_tf32_d32": best(lambda: o.spmm(ptr, cols, x, f=f, mode="tf32", workers=workers)),
+        "sddmm_tf32_d32": best(lambda: o.sddmm(ptr, cols, x, mode="tf32", workers=workers)),
+        "threads": workers,
+    }
+
+
 def arm_config(workload: str, world: int, n: int, m: int) -> dict:
     """The workload description both arms print (same dict for the same N)."""
     shape, model_kind, feats, hidden, classes, nlayers = WORKLOADS[workload]
@@ -596,7 +623,8 @@ def run_ours(args):
             ts.append(time.perf_counter() - s0)
         cpu = {"value": round(1000 * min(ts), 1), "unit": "ms/epoch", "cores": workers,
                "kind": "port",
-               "sample": f"2 full {args.workload} epochs (best), oracle numpy port, tf32 emulation"}
+               "sample": f"2 full {args.workload} epochs (best), oracle numpy port, tf32 emulation",
+               "ops_ms": cpu_ops(workers)}
 
     if rank == 0:
         line = {
