@@ -30,6 +30,26 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// c.xyzw += a * w.xyzw as two packed fp32 FMAs (FFMA2 with a broadcast
+// operand): each lane is an ordinary round-to-nearest fma, so the result is
+// bitwise that of four fmaf, with half the FMA issue slots.
+__device__ __forceinline__ void fma2x(float& c0, float& c1, float a, float w0, float w1) {
+  unsigned long long cp, ap, wp, r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(cp) : "f"(c0), "f"(c1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(ap) : "f"(a));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(wp) : "f"(w0), "f"(w1));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(ap), "l"(wp), "l"(cp));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(r));
+}
+__device__ __forceinline__ void fma4(float4& c, float a, const float4& w) {
+  fma2x(c.x, c.y, a, w.x, w.y);
+  fma2x(c.z, c.w, a, w.z, w.w);
+}
+__device__ __forceinline__ void fma4(float (&c)[4], float a, const float4& w) {
+  fma2x(c[0], c[1], a, w.x, w.y);
+  fma2x(c[2], c[3], a, w.z, w.w);
+}
+
 template <int CI, int CO, bool MASK>
 struct DenseCfg {
   static constexpr int KC = CI <= 64 ? CI : 32;  // k-chunk staged per pipeline item
@@ -123,10 +143,7 @@ __global__ void __launch_bounds__(DenseCfg<CI, CO, MASK>::NT)
 #pragma unroll
         for (int j = 0; j < C::R; ++j) {
           const float av = kk == 0 ? a[j].x : kk == 1 ? a[j].y : kk == 2 ? a[j].z : a[j].w;
-          acc[j].x = fmaf(av, w.x, acc[j].x);
-          acc[j].y = fmaf(av, w.y, acc[j].y);
-          acc[j].z = fmaf(av, w.z, acc[j].z);
-          acc[j].w = fmaf(av, w.w, acc[j].w);
+          fma4(acc[j], av, w);
         }
       }
     }
@@ -245,10 +262,7 @@ __global__ void __launch_bounds__(GemmCfg<CI, CO, MASK>::NT)
       }
 #pragma unroll
       for (int i = 0; i < PB; ++i) {
-        acc[i][0] = fmaf(ai[i], bv.x, acc[i][0]);
-        acc[i][1] = fmaf(ai[i], bv.y, acc[i][1]);
-        acc[i][2] = fmaf(ai[i], bv.z, acc[i][2]);
-        acc[i][3] = fmaf(ai[i], bv.w, acc[i][3]);
+        fma4(acc[i], ai[i], bv);
       }
       if (ib == 0) cs.x += bv.x, cs.y += bv.y, cs.z += bv.z, cs.w += bv.w;
     }
@@ -376,10 +390,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float a = kk == 0 ? av[j].x : kk == 1 ? av[j].y : kk == 2 ? av[j].z : av[j].w;
-          d[j].x = fmaf(a, wv.x, d[j].x);
-          d[j].y = fmaf(a, wv.y, d[j].y);
-          d[j].z = fmaf(a, wv.z, d[j].z);
-          d[j].w = fmaf(a, wv.w, d[j].w);
+          fma4(d[j], a, wv);
         }
       }
     }
@@ -398,10 +409,7 @@ __global__ void __launch_bounds__(256)
       const float ai[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        acc[i][0] = fmaf(ai[i], bv.x, acc[i][0]);
-        acc[i][1] = fmaf(ai[i], bv.y, acc[i][1]);
-        acc[i][2] = fmaf(ai[i], bv.z, acc[i][2]);
-        acc[i][3] = fmaf(ai[i], bv.w, acc[i][3]);
+        fma4(acc[i], ai[i], bv);
       }
     }
     __syncthreads();
