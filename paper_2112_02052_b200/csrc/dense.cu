@@ -150,16 +150,17 @@ __global__ void __launch_bounds__(1024) sum_slabs(const float* __restrict__ part
   __shared__ float sh[32][33];
   const int o = threadIdx.x & 31, j = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * 32 + o;
-  float s0 = 0.f, s1 = 0.f;
+  // 8 independent partials: a slab group's loads are all in flight at once
+  float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (i < len) {
     int q = j;
-    for (; q + 32 < slabs; q += 64) {
-      s0 += part[(int64_t)q * len + i];
-      s1 += part[(int64_t)(q + 32) * len + i];
+    for (; q + 7 * 32 < slabs; q += 8 * 32) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sp[u] += part[(int64_t)(q + 32 * u) * len + i];
     }
-    for (; q < slabs; q += 32) s0 += part[(int64_t)q * len + i];
+    for (; q < slabs; q += 32) sp[0] += part[(int64_t)q * len + i];
   }
-  sh[j][o] = s0 + s1;
+  sh[j][o] = ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
   __syncthreads();
   if (j == 0 && i < len) {
     float tot = 0.f;
