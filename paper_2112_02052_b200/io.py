@@ -1,5 +1,8 @@
-"""TCGT / TCEM binary formats: cache a GPU SGT result
-and embedding matrices across runs.
+"""Graph and matrix files.
+
+TCGT / TCEM binary formats cache a GPU SGT result and embedding matrices
+across runs; the text loaders (edge lists, Matrix Market coordinate files)
+feed the command-line harness (cli.py).
 
 Same on-disk layout as the reference `tcgraph.io` (io.py:208-291), so files
 are interchangeable byte for byte (tests/golden/*.tcgt, *.tcem):
@@ -16,10 +19,14 @@ refuse it, the tile accounting works on it; `device=` also uploads it.
 from __future__ import annotations
 
 import struct
+from pathlib import Path
 
 import numpy as np
 
+from .graph import CsrGraph
 from .sgt import BlockConfig, TiledGraph
+
+MAX_NODE_ID = 0xFFFFFFFF
 
 TCGT_MAGIC = b"TCGT"
 TCEM_MAGIC = b"TCEM"
@@ -125,3 +132,139 @@ def read_tcem(path) -> np.ndarray:
     if off != len(buf):
         raise GraphFormatError(f"{path}: trailing bytes after embedding payload")
     return data.reshape(int(n), int(d)).astype(np.float32)
+
+
+# ---- text formats (reference io.py:28-193) ----------------------------------
+
+def _node_id(token: str, path, lineno: int) -> int:
+    try:
+        v = int(token)
+    except ValueError:
+        raise GraphFormatError(
+            f"{path}:{lineno}: expected a non-negative integer node id, got {token!r}"
+        ) from None
+    if v < 0:
+        raise GraphFormatError(f"{path}:{lineno}: negative node id {v}")
+    if v > MAX_NODE_ID:
+        raise GraphFormatError(f"{path}:{lineno}: node id {v} exceeds the 32-bit id width")
+    return v
+
+
+def _data_lines(fh, first_lineno: int):
+    """(lineno, fields) of the non-blank, non-comment lines."""
+    for lineno, line in enumerate(fh, first_lineno):
+        st = line.strip()
+        if st and st[0] not in "#%":
+            yield lineno, st.split()
+
+
+def load_edge_list(path, num_nodes_hint: int | None = None) -> CsrGraph:
+    """'src dst' lines ('#' / '%' comments) -> normalised CsrGraph; N is the
+    largest id + 1 unless the hint is larger (reference io.py:44-68)."""
+    src, dst = [], []
+    with open(path, "r", encoding="utf-8") as fh:
+        for lineno, parts in _data_lines(fh, 1):
+            if len(parts) != 2:
+                raise GraphFormatError(
+                    f"{path}:{lineno}: expected 'src dst', got {len(parts)} fields")
+            src.append(_node_id(parts[0], path, lineno))
+            dst.append(_node_id(parts[1], path, lineno))
+    n = max(max(src, default=-1), max(dst, default=-1)) + 1
+    if num_nodes_hint is not None:
+        n = max(n, int(num_nodes_hint))
+    return CsrGraph.from_edges(np.asarray(src, np.int64), np.asarray(dst, np.int64), n)
+
+
+def save_edge_list(g: CsrGraph, path) -> None:
+    """'src dst' lines in CSR order (weights are not representable)."""
+    rows = np.repeat(np.arange(g.num_nodes, dtype=np.int64), np.diff(g.node_pointer))
+    with open(path, "w", encoding="utf-8") as fh:
+        for i, j in zip(rows.tolist(), g.edge_list.tolist()):
+            fh.write(f"{i} {j}\n")
+
+
+def load_matrix_market(path) -> CsrGraph:
+    """Matrix Market coordinate file (pattern / real, general / symmetric) as
+    an adjacency: 1-based -> 0-based, symmetric off-diagonals mirrored, real
+    values kept (duplicates summed by from_edges) (reference io.py:79-172)."""
+    with open(path, "r", encoding="utf-8") as fh:
+        header = fh.readline()
+        if not header.startswith("%%MatrixMarket"):
+            raise GraphFormatError(f"{path}:1: missing %%MatrixMarket header")
+        tok = header.split()
+        if len(tok) != 5:
+            raise GraphFormatError(f"{path}:1: malformed header {header.strip()!r}")
+        obj, fmt, field, sym = (x.lower() for x in tok[1:])
+        if obj != "matrix" or fmt != "coordinate":
+            raise GraphFormatError(
+                f"{path}:1: unsupported object/format '{obj} {fmt}' (need matrix coordinate)")
+        if field not in ("pattern", "real"):
+            raise GraphFormatError(f"{path}:1: unsupported field {field!r}")
+        if sym not in ("general", "symmetric"):
+            raise GraphFormatError(f"{path}:1: unsupported symmetry {sym!r}")
+        lines = _data_lines(fh, 2)
+        first = next(lines, None)
+        if first is None:
+            raise GraphFormatError(f"{path}: missing size line")
+        lineno, parts = first
+        size_line = " ".join(parts)
+        if len(parts) != 3:
+            raise GraphFormatError(f"{path}:{lineno}: malformed size line {size_line!r}")
+        try:
+            rows, cols, nnz = (int(x) for x in parts)
+        except ValueError:
+            raise GraphFormatError(f"{path}:{lineno}: malformed size line {size_line!r}") from None
+        if rows != cols:
+            raise GraphFormatError(
+                f"{path}:{lineno}: adjacency matrix must be square, got {rows}x{cols}")
+        if rows > MAX_NODE_ID + 1:
+            raise GraphFormatError(f"{path}:{lineno}: {rows} nodes exceed the 32-bit id width")
+        real = field == "real"
+        want = 3 if real else 2
+        src, dst, vals = [], [], ([] if real else None)
+        seen = 0
+        for lineno, parts in lines:
+            if len(parts) != want:
+                raise GraphFormatError(f"{path}:{lineno}: expected {want} fields, got {len(parts)}")
+            try:
+                i, j = int(parts[0]), int(parts[1])
+            except ValueError:
+                raise GraphFormatError(f"{path}:{lineno}: malformed entry indices") from None
+            if not (1 <= i <= rows and 1 <= j <= cols):
+                raise GraphFormatError(
+                    f"{path}:{lineno}: index ({i}, {j}) out of declared bounds {rows}x{cols}")
+            if real:
+                try:
+                    v = float(parts[2])
+                except ValueError:
+                    raise GraphFormatError(f"{path}:{lineno}: malformed entry value") from None
+            seen += 1
+            src.append(i - 1)
+            dst.append(j - 1)
+            if real:
+                vals.append(v)
+            if sym == "symmetric" and i != j:
+                src.append(j - 1)
+                dst.append(i - 1)
+                if real:
+                    vals.append(v)
+        if seen != nnz:
+            raise GraphFormatError(f"{path}: declared {nnz} entries, found {seen}")
+    return CsrGraph.from_edges(np.asarray(src, np.int64), np.asarray(dst, np.int64), rows,
+                               values=None if vals is None else np.asarray(vals, np.float64))
+
+
+def detect_format(path) -> str:
+    suffix = Path(path).suffix.lower()
+    return {".mtx": "mtx", ".tcgt": "tcgt"}.get(suffix, "edgelist")
+
+
+def load_graph(path, fmt: str = "auto", num_nodes_hint: int | None = None) -> CsrGraph:
+    """Edge-list or Matrix Market file -> CsrGraph (reference io.py:184-193)."""
+    if fmt == "auto":
+        fmt = detect_format(path)
+    if fmt == "edgelist":
+        return load_edge_list(path, num_nodes_hint)
+    if fmt == "mtx":
+        return load_matrix_market(path)
+    raise GraphFormatError(f"format {fmt!r} does not describe a loadable graph")
