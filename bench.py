@@ -202,6 +202,8 @@ def cpu_ops(workers: int) -> dict:
         "spmm_tf32_d32": best(lambda: o.spmm(ptr, cols, x, f=f, mode="tf32", workers=workers)),
         "sddmm_tf32_d32": best(lambda: o.sddmm(ptr, cols, x, mode="tf32", workers=workers)),
         "threads": workers,
+        "spmm_tf32_d32_1thread": best(lambda: o.spmm(ptr, cols, x, f=f, mode="tf32", workers=1)),
+        "sddmm_tf32_d32_1thread": best(lambda: o.sddmm(ptr, cols, x, mode="tf32", workers=1)),
     }
 
 
