@@ -543,15 +543,19 @@ def run_ours(args):
         b_sgt = algorithmic_bytes_sgt(n, m, u, W)
         peak, peak_kind = measured_peaks()
         achieved = b_spmm / (t_spmm * 1e-3) / 1e9
-        traffic = None
+        traffic = tensor_pct = None
         tf = ROOT / "profiles" / "spmm_traffic.json"
         if tf.exists():
-            traffic = json.loads(tf.read_text()).get(f"{shape}_d{d}")
+            prof = json.loads(tf.read_text())
+            traffic = prof.get(f"{shape}_d{d}")
+            tensor_pct = prof.get(f"{shape}_d{d}_tensor_pipe_pct")
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": traffic,
                     "peak_kind": peak_kind, "kernel": f"spmm_tc weighted D={d} ({shape})",
                     "algorithmic_bytes": b_spmm, "launch_us": round(t_spmm * 1e3, 2),
-                    "l2": "cold (flushed before each launch)"}
+                    "l2": "cold (flushed before each launch)",
+                    "warm_us": round(t_spmm_warm * 1e3, 2),
+                    "tensor_pipe_pct_ncu": tensor_pct}
         # 8(f) rows: graph normalisation / invariant check / tile accounting on the device
         gen = torch.Generator(device=dev).manual_seed(1)
         src_r = torch.randint(0, n, (m,), device=dev, generator=gen)
