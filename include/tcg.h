@@ -286,11 +286,12 @@ size_t tcg_softmax_xent_workspace_bytes(int64_t n);
 int tcg_softmax_xent(const float* logits, int64_t ld, const int64_t* labels, int64_t n, int64_t c,
                      float* loss, float* dlogits, void* workspace, size_t workspace_bytes,
                      void* stream);
-/* dlogits[n x c] = (softmax(logits) - onehot(labels)) / n * g, g = *grad_scale
- * (device scalar; null => 1): the backward recomputes the softmax from the
- * logits instead of keeping dlogits from the forward */
+/* dlogits[n x c] (row stride ldd) = (softmax(logits) - onehot(labels)) / n * g,
+ * g = *grad_scale (device scalar; null => 1): the backward recomputes the
+ * softmax from the logits instead of keeping dlogits from the forward */
 int tcg_softmax_xent_backward(const float* logits, int64_t ld, const int64_t* labels, int64_t n,
-                              int64_t c, const float* grad_scale, float* dlogits, void* stream);
+                              int64_t c, const float* grad_scale, float* dlogits, int64_t ldd,
+                              void* stream);
 
 /* ---- TF32 operand rounding: reference tiles.quantize_tf32 (67-82) ------- */
 int tcg_quantize_tf32(const float* in, float* out, int64_t n, void* stream);

@@ -104,7 +104,7 @@ SIGNATURES = {
     "tcg_colsum": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _SZ, _P]),
     "tcg_softmax_xent_workspace_bytes": (_SZ, [_I64]),
     "tcg_softmax_xent": (C.c_int, [_P, _I64, _P, _I64, _I64, _P, _P, _P, _SZ, _P]),
-    "tcg_softmax_xent_backward": (C.c_int, [_P, _I64, _P, _I64, _I64, _P, _P, _P]),
+    "tcg_softmax_xent_backward": (C.c_int, [_P, _I64, _P, _I64, _I64, _P, _P, _I64, _P]),
 }
 
 _lib = None

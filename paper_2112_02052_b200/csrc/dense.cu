@@ -177,8 +177,8 @@ __global__ void __launch_bounds__(1024) sum_slabs(const float* __restrict__ part
 template <bool LOSS, bool GRAD>
 __global__ void __launch_bounds__(256)
     softmax_xent(const float* __restrict__ logits, int64_t ld, const int64_t* __restrict__ labels,
-                 int64_t n, int c, float* __restrict__ dlogits, const float* __restrict__ gscale,
-                 float* __restrict__ lpart, int64_t parts) {
+                 int64_t n, int c, float* __restrict__ dlogits, int64_t ldd,
+                 const float* __restrict__ gscale, float* __restrict__ lpart, int64_t parts) {
   __shared__ float rowc[32];
   const int sub = threadIdx.x & 7, lr_ = threadIdx.x >> 3;
   const int64_t row = (int64_t)blockIdx.x * 32 + lr_;
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(256)
       const float inv_n = (gscale ? __ldg(gscale) : 1.f) / (float)n;
       for (int j = sub; j < c; j += 8) {
         const float pj = expf(__ldg(lr + j) - lse);
-        dlogits[row * c + j] = (pj - (j == lab ? 1.f : 0.f)) * inv_n;
+        dlogits[row * ldd + j] = (pj - (j == lab ? 1.f : 0.f)) * inv_n;
       }
     }
     contrib = lse - lr[lab];
@@ -326,6 +326,8 @@ int fast_dense(const float* x, int64_t ldx, int64_t n, int ci, const float* m, i
   TCG_FD(32)
   TCG_FD(40)
   TCG_FD(64)
+  TCG_FD(96)
+  TCG_FD(100)
   TCG_FD(128)
 #undef TCG_FD
   return 1;
@@ -383,6 +385,8 @@ int fast_gemm_tn(const float* a, int64_t lda, const float* b, int64_t ldb, const
   if (k == 32) return gemm_tn_co<32>(a, lda, b, ldb, mask, ldm, n, c, part, colpart, cap_slabs, used, s);
   if (k == 40) return gemm_tn_co<40>(a, lda, b, ldb, mask, ldm, n, c, part, colpart, cap_slabs, used, s);
   if (k == 64) return gemm_tn_co<64>(a, lda, b, ldb, mask, ldm, n, c, part, colpart, cap_slabs, used, s);
+  if (k == 96) return gemm_tn_co<96>(a, lda, b, ldb, mask, ldm, n, c, part, colpart, cap_slabs, used, s);
+  if (k == 100) return gemm_tn_co<100>(a, lda, b, ldb, mask, ldm, n, c, part, colpart, cap_slabs, used, s);
   if (k == 128) return gemm_tn_co<128>(a, lda, b, ldb, mask, ldm, n, c, part, colpart, cap_slabs, used, s);
   return 1;
 }
@@ -538,10 +542,10 @@ extern "C" int tcg_softmax_xent(const float* logits, int64_t ld, const int64_t* 
   float* lpart = static_cast<float*>(workspace);
   const unsigned grid = (unsigned)((n + 31) / 32);
   if (dlogits)
-    softmax_xent<true, true><<<grid, 256, 0, s>>>(logits, ld, labels, n, (int)c, dlogits, nullptr,
-                                                  lpart, parts);
+    softmax_xent<true, true><<<grid, 256, 0, s>>>(logits, ld, labels, n, (int)c, dlogits, c,
+                                                  nullptr, lpart, parts);
   else
-    softmax_xent<true, false><<<grid, 256, 0, s>>>(logits, ld, labels, n, (int)c, nullptr,
+    softmax_xent<true, false><<<grid, 256, 0, s>>>(logits, ld, labels, n, (int)c, nullptr, 0,
                                                    nullptr, lpart, parts);
   TCG_LAUNCHED("softmax_xent");
   final_loss<<<1, 256, 0, s>>>(lpart, parts, n, loss);
@@ -551,17 +555,18 @@ extern "C" int tcg_softmax_xent(const float* logits, int64_t ld, const int64_t* 
 
 extern "C" int tcg_softmax_xent_backward(const float* logits, int64_t ld, const int64_t* labels,
                                          int64_t n, int64_t c, const float* grad_scale,
-                                         float* dlogits, void* stream) {
-  TCG_REQUIRE(n >= 1 && c >= 1 && ld >= c, "tcg_softmax_xent_backward: bad shape");
+                                         float* dlogits, int64_t ldd, void* stream) {
+  TCG_REQUIRE(n >= 1 && c >= 1 && ld >= c && ldd >= c, "tcg_softmax_xent_backward: bad shape");
   TCG_REQUIRE(logits && labels && dlogits, "tcg_softmax_xent_backward: null pointer");
   softmax_xent<false, true><<<(unsigned)((n + 31) / 32), 256, 0, as_stream(stream)>>>(
-      logits, ld, labels, n, (int)c, dlogits, grad_scale, nullptr, 0);
+      logits, ld, labels, n, (int)c, dlogits, ldd, grad_scale, nullptr, 0);
   TCG_LAUNCHED("softmax_xent_backward");
   return TCG_OK;
 }
 
 extern "C" size_t tcg_colsum_workspace_bytes(int64_t n, int64_t c) {
-  return (size_t)(colsum_slabs(n) * (c > 0 ? c : 1)) * sizeof(float);
+  const int64_t c4 = c > 0 ? (c + 3) / 4 * 4 : 4;
+  return (size_t)((colsum_slabs(n) + 1) * c4) * sizeof(float);
 }
 
 extern "C" int tcg_colsum(const float* x, int64_t ld, int64_t n, int64_t c, float* out,
@@ -577,13 +582,26 @@ extern "C" int tcg_colsum(const float* x, int64_t ld, int64_t n, int64_t c, floa
   const int64_t slabs = colsum_slabs(n);
   const int64_t rows = (n + slabs - 1) / slabs;
   float* part = static_cast<float*>(workspace);
-  const bool v4 = c % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
-  if (v4)
-    colsum_part<4><<<(unsigned)slabs, 256, 0, s>>>(x, ld, n, (int)c, rows, part);
-  else
+  // rows padded to a multiple of 4 floats take the float4 path over the padded
+  // width; the padding columns land in partials that are never read
+  const int64_t c4 = (c + 3) / 4 * 4;
+  const bool v4 = ld % 4 == 0 && c4 <= ld && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  if (v4) {
+    colsum_part<4><<<(unsigned)slabs, 256, 0, s>>>(x, ld, n, (int)c4, rows, part);
+    TCG_LAUNCHED("colsum_part");
+    if (c4 == c) {
+      sum_slabs<<<(unsigned)((c + 31) / 32), 1024, 0, s>>>(part, (int)slabs, c, out);
+    } else {
+      float* tmp = part + slabs * c4;
+      sum_slabs<<<(unsigned)((c4 + 31) / 32), 1024, 0, s>>>(part, (int)slabs, c4, tmp);
+      TCG_CUDA(cudaMemcpyAsync(out, tmp, sizeof(float) * c, cudaMemcpyDeviceToDevice, s),
+               "tcg_colsum copy");
+    }
+  } else {
     colsum_part<1><<<(unsigned)slabs, 256, 0, s>>>(x, ld, n, (int)c, rows, part);
-  TCG_LAUNCHED("colsum_part");
-  sum_slabs<<<(unsigned)((c + 31) / 32), 1024, 0, s>>>(part, (int)slabs, c, out);
+    TCG_LAUNCHED("colsum_part");
+    sum_slabs<<<(unsigned)((c + 31) / 32), 1024, 0, s>>>(part, (int)slabs, c, out);
+  }
   TCG_LAUNCHED("sum_slabs");
   return TCG_OK;
 }

@@ -52,8 +52,10 @@ __device__ __forceinline__ void fma4(float (&c)[4], float a, const float4& w) {
 
 template <int CI, int CO, bool MASK>
 struct DenseCfg {
-  static constexpr int KC = CI <= 64 ? CI : 32;  // k-chunk staged per pipeline item
+  // k-chunk staged per pipeline item (a divisor of CI: 32 for 96 / 128, 20 for 100)
+  static constexpr int KC = CI <= 64 ? CI : CI % 32 == 0 ? 32 : CI % 20 == 0 ? 20 : 4;
   static constexpr int NKC = CI / KC;
+  static_assert(CI % KC == 0 && KC % 4 == 0, "dense_tile k-chunk");
   static constexpr int XS = KC + 4;  // padded row stride: conflict-free LDS.128
   static constexpr int Q = CO / 4;   // column quads
   static constexpr int NT = Q * 32;  // threads

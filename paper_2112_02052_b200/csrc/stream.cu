@@ -1017,7 +1017,9 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
   }
   while (d < dim) {
     const int rem = dim - d;
-    const int nt = (rem >= 16 && ok_at(2, d)) ? 2 : 1;
+    // every pass costs about the same (it walks the whole block stream), so a
+    // 9..15-wide tail is one masked 16-wide pass rather than two 8-wide ones
+    const int nt = (rem > 8 && ok_at(2, d)) ? 2 : 1;
     if (nt == 1 && !ok_at(1, d)) return d == 0 ? TCG_E_UNSUPPORTED : TCG_E_INVALID;
     a.d0 = d;
     a.dv = rem < 8 * nt ? rem : 8 * nt;

@@ -30,6 +30,21 @@ def _p(t):
     return None if t is None else t.data_ptr()
 
 
+def rows_empty(n: int, d: int, device):
+    """[n x d] f32 with 16-B aligned rows: widths above 16 that are not a
+    multiple of 4 (class counts such as 47 or 22) get a padded row stride, so
+    the sparse engine and the dense kernels read them with vector slices and
+    nothing has to be copied into an aligned buffer later."""
+    if d > 16 and d % 4:
+        return torch.empty((n, (d + 3) // 4 * 4), dtype=torch.float32, device=device)[:, :d]
+    return torch.empty((n, d), dtype=torch.float32, device=device)
+
+
+def rows_ok(x):
+    """x as is when its rows are unit-stride (any row stride), else a copy."""
+    return x if x.dim() == 2 and x.stride(1) == 1 else x.contiguous()
+
+
 def dense(x, w, bias=None, relu=False, mask=None, transposed=False, out=None):
     """y = act((x .* [mask>0]) M + bias), M = w ([ci x co]) or w^T when
     `transposed` (w then [co x ci])."""
@@ -37,7 +52,7 @@ def dense(x, w, bias=None, relu=False, mask=None, transposed=False, out=None):
     n, ci = x.shape
     co = w.shape[0] if transposed else w.shape[1]
     if out is None:
-        out = torch.empty((n, co), dtype=torch.float32, device=x.device)
+        out = rows_empty(n, co, x.device)
     _lib.check(lib.tcg_dense(x.data_ptr(), x.stride(0), n, ci, w.data_ptr(), co, int(transposed),
                              _p(bias), int(relu), _p(mask), mask.stride(0) if mask is not None else 0,
                              out.data_ptr(), out.stride(0), _stream()), "tcg_dense")
@@ -107,18 +122,19 @@ def softmax_xent_backward(logits, labels, grad_scale=None):
     """(softmax(logits) - onehot(labels)) / n * grad_scale (a device scalar)."""
     lib = _lib.load()
     n, c = logits.shape
-    dl = torch.empty((n, c), dtype=torch.float32, device=logits.device)
+    dl = rows_empty(n, c, logits.device)
     gs = None if grad_scale is None else grad_scale.float().contiguous()
     _lib.check(lib.tcg_softmax_xent_backward(logits.data_ptr(), logits.stride(0),
                                              labels.data_ptr(), n, c, _p(gs), dl.data_ptr(),
-                                             _stream()), "tcg_softmax_xent_backward")
+                                             dl.stride(0), _stream()),
+               "tcg_softmax_xent_backward")
     return dl
 
 
 class DenseFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, b, relu: bool):
-        x = x.contiguous()
+        x = rows_ok(x)
         y = dense(x, w.contiguous(), bias=b, relu=relu)
         ctx.relu = relu
         ctx.has_b = b is not None
@@ -128,7 +144,7 @@ class DenseFn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g):
         x, w, y = ctx.saved_tensors
-        g = g.contiguous()
+        g = rows_ok(g)
         if not ctx.relu and not ctx.has_b and ctx.needs_input_grad[0]:
             dx, dw = dense_backward(x, g, w.contiguous())
             return dx, dw, None, None
@@ -146,7 +162,7 @@ class SoftmaxXentFn(torch.autograd.Function):
         # loss only; the backward recomputes the softmax from the logits
         # (one read of the logits instead of writing dlogits, re-reading and
         # scaling it by the incoming gradient)
-        logits = logits.contiguous()
+        logits = rows_ok(logits)
         loss, _ = softmax_xent(logits, labels, grad=False)
         ctx.save_for_backward(logits, labels)
         return loss

@@ -31,7 +31,7 @@ import torch.nn.functional as F
 
 from . import _lib
 from .dist import ShardPlan, allgather_edges, allgather_rows
-from .dense import DenseFn, Linear, colsum, cross_entropy  # noqa: F401  (re-exported)
+from .dense import DenseFn, Linear, colsum, cross_entropy, rows_empty  # noqa: F401  (re-exported)
 from .kernels import (
     agnn_backward_device,
     agnn_forward_device,
@@ -51,7 +51,7 @@ def _edge_weights(t: TiledGraph):
 
 def _rows_out(t: TiledGraph, d: int, like: torch.Tensor, shard: ShardPlan | None):
     if shard is None:
-        return torch.empty((t.num_nodes, d), dtype=torch.float32, device=like.device), 0, None
+        return rows_empty(t.num_nodes, d, like.device), 0, None
     r0, _ = shard.my_rows
     slab = torch.empty((shard.rows_max, d), dtype=torch.float32, device=like.device)
     return slab, r0, shard.my_windows
@@ -65,8 +65,10 @@ def _rows16(x):
     """x with 16-B aligned rows: the TF32 engine stages rows in 16/8-byte slices,
     so an odd width (GCN class counts, e.g. products' 47) is copied once into a
     padded-stride buffer instead of falling back to 4-byte slices."""
-    x = x.contiguous()
     d = x.shape[1]
+    if x.stride(1) == 1 and x.stride(0) % 4 == 0 and x.data_ptr() % 16 == 0:
+        return x  # already 16-B aligned rows (padded stride from rows_empty)
+    x = x.contiguous()
     if d <= 16 or d % 4 == 0:
         return x
     buf = torch.empty((x.shape[0], (d + 3) // 4 * 4), dtype=x.dtype, device=x.device)

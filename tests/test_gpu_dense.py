@@ -23,7 +23,9 @@ def env():
 
 @pytest.mark.parametrize("n,ci,co", [(1000, 128, 32), (777, 32, 40), (50, 1433, 16), (3, 7, 3),
                                      (4096, 32, 128), (20000, 32, 32), (5001, 40, 32),
-                                     (3333, 64, 7), (999, 16, 8), (30000, 128, 40), (129, 32, 12)])
+                                     (3333, 64, 7), (999, 16, 8), (30000, 128, 40), (129, 32, 12),
+                                     (20011, 100, 16), (7000, 96, 32), (5000, 96, 22),
+                                     (3001, 100, 47)])
 def test_dense_forward_backward_kernels(env, n, ci, co):
     _, dense, _, torch = env
     g = torch.Generator(device="cuda").manual_seed(n)
