@@ -996,6 +996,7 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
                : (dual ? stream::launch_t<NTV, true, false, MK>(a, nchunks, s)            \
                        : stream::launch_t<NTV, false, false, MK>(a, nchunks, s));
     TCG_SL(4, false)
+    TCG_SL(4, true)
     TCG_SL(2, false)
     TCG_SL(2, true)
     TCG_SL(1, false)
@@ -1018,8 +1019,9 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
   while (d < dim) {
     const int rem = dim - d;
     // every pass costs about the same (it walks the whole block stream), so a
-    // 9..15-wide tail is one masked 16-wide pass rather than two 8-wide ones
-    const int nt = (rem > 8 && ok_at(2, d)) ? 2 : 1;
+    // tail is one masked pass of the narrowest chunk that holds it (17..31
+    // features: 32-wide, 9..15: 16-wide) rather than several narrow ones
+    const int nt = (rem > 16 && ok_at(4, d)) ? 4 : (rem > 8 && ok_at(2, d)) ? 2 : 1;
     if (nt == 1 && !ok_at(1, d)) return d == 0 ? TCG_E_UNSUPPORTED : TCG_E_INVALID;
     a.d0 = d;
     a.dv = rem < 8 * nt ? rem : 8 * nt;
