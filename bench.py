@@ -267,7 +267,6 @@ def run_reference(args):
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    import torch.nn.functional as F
 
     import paper_2112_02052_b200 as tcg
     from paper_2112_02052_b200 import _lib, dist as tdist, layers
