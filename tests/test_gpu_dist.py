@@ -48,14 +48,16 @@ def _worker(rank, world, port, out_dir):
     rng = np.random.default_rng(0)
     x = torch.from_numpy(rng.standard_normal((6000, 48)).astype(np.float32)).cuda()
     y = torch.from_numpy(rng.integers(0, 5, 6000)).cuda()
+    y47 = torch.from_numpy(rng.integers(0, 47, 6000)).cuda()
     res = {}
-    for kind in ("agnn", "gcn"):
+    # gcn47: an odd class count (padded-stride rows through the sharded path)
+    for kind in ("agnn", "gcn", "gcn47"):
         grads = []
         for shard in (None, plan):
             torch.manual_seed(0)
             net = (layers.AGNN(48, 32, 5, layers=2) if kind == "agnn"
-                   else layers.GCN(48, 16, 5)).cuda()
-            loss = layers.cross_entropy(net(x, t, shard), y)
+                   else layers.GCN(48, 16, 47 if kind == "gcn47" else 5)).cuda()
+            loss = layers.cross_entropy(net(x, t, shard), y47 if kind == "gcn47" else y)
             loss.backward()
             grads.append([float(loss)] + [p.grad.detach().cpu().numpy() for p in net.parameters()])
         ref, got = grads
