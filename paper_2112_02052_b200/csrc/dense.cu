@@ -273,7 +273,7 @@ int set_smem(K kern, size_t bytes, int threads, int* per_sm) {
 }
 
 template <int CI, int CO, bool TRANS, bool MASK>
-int run_dense_tile(const float* x, int64_t ldx, int64_t n, const float* m, int co,
+int run_dense_tile(const float* x, int64_t ldx, int64_t n, int ci, const float* m, int co,
                    const float* bias, int relu, const float* mask, int64_t ldm, float* y,
                    int64_t ldy, cudaStream_t s) {
   using Cfg = dr::DenseCfg<CI, CO, MASK>;
@@ -290,20 +290,21 @@ int run_dense_tile(const float* x, int64_t ldx, int64_t n, const float* m, int c
   if (blocks > cap) blocks = cap;
   const int vec_out = (ldy % 4 == 0) && al16(y);
   dr::dense_tile<CI, CO, TRANS, MASK><<<(unsigned)blocks, Cfg::NT, Cfg::SMEM, s>>>(
-      x, ldx, n, m, co, bias, relu, mask, ldm, y, ldy, vec_out);
+      x, ldx, n, m, co, bias, relu, mask, ldm, y, ldy, vec_out, ci);
   TCG_LAUNCHED("dense_tile");
   return TCG_OK;
 }
 
 template <int CI, bool TRANS>
-int dense_co(const float* x, int64_t ldx, int64_t n, const float* m, int co, const float* bias,
-             int relu, const float* mask, int64_t ldm, float* y, int64_t ldy, cudaStream_t s) {
-#define TCG_DC(COV)                                                                          \
-  if (co <= COV)                                                                             \
-    return mask ? run_dense_tile<CI, COV, TRANS, true>(x, ldx, n, m, co, bias, relu, mask,   \
-                                                       ldm, y, ldy, s)                       \
-                : run_dense_tile<CI, COV, TRANS, false>(x, ldx, n, m, co, bias, relu, mask,  \
-                                                        ldm, y, ldy, s);
+int dense_co(const float* x, int64_t ldx, int64_t n, int ci, const float* m, int co,
+             const float* bias, int relu, const float* mask, int64_t ldm, float* y, int64_t ldy,
+             cudaStream_t s) {
+#define TCG_DC(COV)                                                                            \
+  if (co <= COV)                                                                               \
+    return mask ? run_dense_tile<CI, COV, TRANS, true>(x, ldx, n, ci, m, co, bias, relu, mask, \
+                                                       ldm, y, ldy, s)                         \
+                : run_dense_tile<CI, COV, TRANS, false>(x, ldx, n, ci, m, co, bias, relu,      \
+                                                        mask, ldm, y, ldy, s);
   TCG_DC(8)
   TCG_DC(16)
   TCG_DC(32)
@@ -318,13 +319,18 @@ int fast_dense(const float* x, int64_t ldx, int64_t n, int ci, const float* m, i
                const float* bias, int relu, const float* mask, int64_t ldm, float* y, int64_t ldy,
                cudaStream_t s) {
   if (co > 64 || ldx % 4 || !al16(x) || (mask && (ldm % 4 || !al16(mask)))) return 1;
+  // widths that are not a multiple of 4 run the next tile width up (zero-filled
+  // tail columns); the padded row stride keeps the 16-B staging in bounds
+  const int ci4 = (ci + 3) / 4 * 4;
+  if (ci4 > ldx || (mask && ci4 > ldm)) return 1;
 #define TCG_FD(CIV)                                                                            \
-  if (ci == CIV)                                                                               \
-    return trans ? dense_co<CIV, true>(x, ldx, n, m, co, bias, relu, mask, ldm, y, ldy, s)     \
-                 : dense_co<CIV, false>(x, ldx, n, m, co, bias, relu, mask, ldm, y, ldy, s);
+  if (ci4 == CIV)                                                                              \
+    return trans ? dense_co<CIV, true>(x, ldx, n, ci, m, co, bias, relu, mask, ldm, y, ldy, s) \
+                 : dense_co<CIV, false>(x, ldx, n, ci, m, co, bias, relu, mask, ldm, y, ldy, s);
   TCG_FD(16)
   TCG_FD(32)
   TCG_FD(40)
+  TCG_FD(48)
   TCG_FD(64)
   TCG_FD(96)
   TCG_FD(100)

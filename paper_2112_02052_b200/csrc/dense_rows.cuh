@@ -24,6 +24,12 @@ __device__ __forceinline__ void cp16(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(sz)
                : "memory");
 }
+// 16-byte copy of the first `bytes` (0..16) bytes of src, the rest zero-filled
+__device__ __forceinline__ void cp16n(void* dst, const void* src, int bytes) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -66,13 +72,15 @@ struct DenseCfg {
   static constexpr size_t SMEM = (size_t)(CI * CO + STAGES * STAGE) * sizeof(float);
 };
 
-// y[n x co] = act((x .* [mask > 0]) . M + b); M [CI x co] (or [co x CI] when TRANS);
-// CI, CO multiples of 4 (CO = co rounded up), ldx, ldm multiples of 4.
+// y[n x co] = act((x .* [mask > 0]) . M + b); M [ci x co] (or [co x ci] when TRANS);
+// CI = ci rounded up to a multiple of 4 (the columns past ci are zero-filled
+// in shared memory, so padded-stride inputs need no clean padding), CO = co
+// rounded up; ldx, ldm multiples of 4.
 template <int CI, int CO, bool TRANS, bool MASK>
 __global__ void __launch_bounds__(DenseCfg<CI, CO, MASK>::NT)
     dense_tile(const float* __restrict__ x, int64_t ldx, int64_t n, const float* __restrict__ m,
                int co, const float* __restrict__ bias, int relu, const float* __restrict__ mask,
-               int64_t ldm, float* __restrict__ y, int64_t ldy, int vec_out) {
+               int64_t ldm, float* __restrict__ y, int64_t ldy, int vec_out, int ci) {
   using C = DenseCfg<CI, CO, MASK>;
   extern __shared__ __align__(16) float sh[];
   float* ws = sh;            // [CI][CO]
@@ -81,7 +89,9 @@ __global__ void __launch_bounds__(DenseCfg<CI, CO, MASK>::NT)
   const int q = tid % C::Q, rg = tid / C::Q;
   for (int i = tid; i < CI * CO; i += C::NT) {
     const int k = i / CO, c = i % CO;
-    ws[i] = c < co ? (TRANS ? __ldg(m + (int64_t)c * CI + k) : __ldg(m + (int64_t)k * co + c)) : 0.f;
+    ws[i] = c < co && k < ci
+                ? (TRANS ? __ldg(m + (int64_t)c * ci + k) : __ldg(m + (int64_t)k * co + c))
+                : 0.f;
   }
   const int64_t ntiles = (n + C::ROWS - 1) / C::ROWS;
   const int64_t my_tiles =
@@ -97,12 +107,12 @@ __global__ void __launch_bounds__(DenseCfg<CI, CO, MASK>::NT)
       for (int i = tid; i < C::ROWS * F4; i += C::NT) {
         const int r = i / F4, c4 = i % F4;
         const int64_t gr = tile * C::ROWS + r;
-        const bool ok = gr < n;
-        const int64_t grc = ok ? gr : 0;
-        cp16(st + r * C::XS + c4 * 4, x + grc * ldx + kc * C::KC + c4 * 4, ok);
-        if (MASK)
-          cp16(st + C::ROWS * C::XS + r * C::XS + c4 * 4, mask + grc * ldm + kc * C::KC + c4 * 4,
-               ok);
+        const int col = kc * C::KC + c4 * 4;
+        const int nb = gr < n ? min(16, max(0, 4 * (ci - col))) : 0;
+        const int64_t grc = nb ? gr : 0;
+        const int colc = nb ? col : 0;
+        cp16n(st + r * C::XS + c4 * 4, x + grc * ldx + colc, nb);
+        if (MASK) cp16n(st + C::ROWS * C::XS + r * C::XS + c4 * 4, mask + grc * ldm + colc, nb);
       }
     }
     cp_commit();

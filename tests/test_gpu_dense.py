@@ -47,6 +47,25 @@ def test_dense_forward_backward_kernels(env, n, ci, co):
     assert torch.equal(dw, dw2)
 
 
+@pytest.mark.parametrize("ci,co", [(47, 16), (22, 32), (45, 40), (13, 8)])
+def test_dense_padded_stride_inputs(env, ci, co):
+    """Odd widths in padded-stride buffers (rows_empty) run the next tile width
+    up; the padding columns hold NaN here and must not leak into the result."""
+    _, dense, _, torch = env
+    n = 3001
+    gen = torch.Generator(device="cuda").manual_seed(ci)
+    ld = (ci + 3) // 4 * 4
+    buf = torch.full((n, ld), float("nan"), device="cuda")
+    x = buf[:, :ci]
+    x.copy_(torch.randn(n, ci, device="cuda", generator=gen))
+    w = torch.randn(ci, co, device="cuda", generator=gen)
+    y = dense.dense(x, w)
+    assert rel_l2(y.cpu().numpy(), (x.double() @ w.double()).cpu().numpy()) < 1e-6
+    wt = torch.randn(co, ci, device="cuda", generator=gen)  # dense(x, wt, transposed) = x wt^T
+    yt = dense.dense(x, wt, transposed=True)
+    assert rel_l2(yt.cpu().numpy(), (x.double() @ wt.double().T).cpu().numpy()) < 1e-6
+
+
 @pytest.mark.parametrize("n,ci,co", [(169343, 32, 32), (1000, 32, 32), (77, 32, 32), (0, 32, 32),
                                      (5000, 32, 40), (3000, 16, 8)])
 def test_dense_backward(env, n, ci, co):
