@@ -208,15 +208,31 @@ def _glorot(fan_in, fan_out, gen=None):
 
 
 class GCNConv(nn.Module):
-    """TC-GNN GCNConv: Y = A (X W) + b."""
+    """TC-GNN GCNConv: Y = A X W + b.
 
-    def __init__(self, in_dim: int, out_dim: int, mode: str = "tf32", gen=None):
+    The sparse product runs at the narrower of the two widths: A (X W) + b when
+    the layer narrows (in_dim >= out_dim), (A X) W + b -- the reference
+    gcn_layer's own order, `spmm(t, x) @ w + b` (kernels.py:559-583) -- when
+    it widens (e.g. 16 -> 47 classes: one 16-wide aggregation instead of a
+    32-wide and a 16-wide pass, forward and backward). Same maths; only the
+    fp32 association differs. `order` = "auto" | "transform_first" |
+    "aggregate_first"."""
+
+    def __init__(self, in_dim: int, out_dim: int, mode: str = "tf32", gen=None,
+                 order: str = "auto"):
         super().__init__()
+        if order not in ("auto", "transform_first", "aggregate_first"):
+            raise ValueError(f"unknown order {order!r}")
         self.weight = nn.Parameter(_glorot(in_dim, out_dim, gen))
         self.bias = nn.Parameter(torch.zeros(out_dim))
         self.mode = mode
+        self.aggregate_first = (order == "aggregate_first"
+                                or (order == "auto" and in_dim < out_dim))
 
     def forward(self, x, t: TiledGraph, shard: ShardPlan | None = None):
+        if self.aggregate_first:
+            h = GcnAggregate.apply(x, None, t, self.mode, shard)
+            return DenseFn.apply(h, self.weight, self.bias, False)
         h = DenseFn.apply(x, self.weight, None, False)
         return GcnAggregate.apply(h, self.bias, t, self.mode, shard)
 
