@@ -119,6 +119,7 @@ struct Args {
   int64_t ldy, y_row0;
   int accumulate;
   int vec_out;           // 16-B aligned output rows
+  int x16;               // NT = 2: operand rows 16-B aligned (one 16-B copy per lane)
 };
 
 constexpr int kEPL = 5;    // edges per lane prefetched for the next window (160)
@@ -218,7 +219,33 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32,
   // masked tail chunk: this lane's slice holds min(NT, dv - g NT) real features
   const int vb = MASK ? max(0, min(CP, (a.dv - g * NT) * 4)) : CP;
   constexpr bool masked = MASK;
+  // 16-wide chunks (64-B row slices): lane L copies 16 B -- quarter L%4 of row
+  // L/4 -- so a block's 8 rows take one 16-B cp.async per lane instead of two
+  // 8-B ones (the staged layout is the same: 16-B pieces land on swizzle-paired
+  // 8-B granules, which stay adjacent because the swizzle only flips bit 2)
+  const int qr = lane >> 2, qk = lane & 3;
+  const uint32_t q_id = 4u * (qr < 4 ? 2 * qr : 2 * qr - 7);
+  const uint32_t q_dst = qr * 64 + ((2 * qk) ^ (4 * ((qr >> 1) & 1))) * 8;
+  const int q_vb = MASK ? max(0, min(16, (a.dv - 4 * qk) * 4)) : 16;
+  const char* q_x = reinterpret_cast<const char*>(a.x + d0) + 16 * qk;
+  const char* q_x2 = DUAL ? reinterpret_cast<const char*>(a.x2 + d0) + 16 * qk : nullptr;
   auto issue_x = [&](uint32_t xo, uint32_t io) {
+    if (NT == 2 && a.x16) {
+      const uint32_t id = *reinterpret_cast<const uint32_t*>(iring_p + io + q_id);
+      const uint32_t d = ring + xo + q_dst;
+      if constexpr (masked) {
+        cp_async_n<16>(d, q_vb ? (const void*)(q_x + (uint64_t)id * xrow) : (const void*)a.x,
+                       q_vb);
+        if constexpr (DUAL)
+          cp_async_n<16>(d + SLOT,
+                         q_vb ? (const void*)(q_x2 + (uint64_t)id * xrow2) : (const void*)a.x,
+                         q_vb);
+      } else {
+        cp_async<16>(d, q_x + (uint64_t)id * xrow);
+        if constexpr (DUAL) cp_async<16>(d + SLOT, q_x2 + (uint64_t)id * xrow2);
+      }
+      return;
+    }
     const uint2 id = *reinterpret_cast<const uint2*>(iring_p + 8 * t + io);
     if constexpr (masked) {
       const void* z1 = a.x;  // any valid address when nothing is copied
@@ -989,6 +1016,8 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
     a.vec_out = (a.dv == 8 * nt) && q.vec_out &&
                 ((a.d0 % 4) == 0);  // float4 / float2 row stores need aligned slices
     const bool mk = a.dv < 8 * nt;
+    a.x16 = nt == 2 && al(q.x + a.d0, 16) && (q.ldx * 4) % 16 == 0 &&
+            (!dual || (al(q.x2 + a.d0, 16) && (q.ldx2 * 4) % 16 == 0));
 #define TCG_SL(NTV, MK)                                                                   \
   if (nt == NTV && mk == MK)                                                              \
     return big ? (dual ? stream::launch_t<NTV, true, true, MK>(a, nchunks, s)             \
