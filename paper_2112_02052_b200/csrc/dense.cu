@@ -328,6 +328,7 @@ int fast_dense(const float* x, int64_t ldx, int64_t n, int ci, const float* m, i
     return trans ? dense_co<CIV, true>(x, ldx, n, ci, m, co, bias, relu, mask, ldm, y, ldy, s) \
                  : dense_co<CIV, false>(x, ldx, n, ci, m, co, bias, relu, mask, ldm, y, ldy, s);
   TCG_FD(16)
+  TCG_FD(24)
   TCG_FD(32)
   TCG_FD(40)
   TCG_FD(48)

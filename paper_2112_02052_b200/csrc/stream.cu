@@ -1011,7 +1011,10 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
   a.x = q.x, a.x2 = q.x2, a.w = q.w, a.widx = q.widx, a.w2 = q.w2, a.widx2 = q.widx2;
   a.bias = q.bias, a.y = q.y, a.ldy = q.ldy, a.y_row0 = q.y_row0, a.accumulate = q.accumulate;
   // big windows (products: ~400 edges each) stage their edges in shared memory
-  const bool big = t->num_windows > 0 && t->num_edges > 128 * t->num_windows;
+#ifndef TCG_BIG_EPW
+#define TCG_BIG_EPW 256  // measured: amazon0601 (134 edges per window) is faster without staging
+#endif
+  const bool big = t->num_windows > 0 && t->num_edges > TCG_BIG_EPW * t->num_windows;
   auto launch = [&](int nt, int nchunks) -> int {
     a.vec_out = (a.dv == 8 * nt) && q.vec_out &&
                 ((a.d0 % 4) == 0);  // float4 / float2 row stores need aligned slices
