@@ -26,7 +26,10 @@ namespace tcg {
 namespace {
 
 constexpr int kRankThreads = 128;
-constexpr int kSmemCap = 4096;  // keys per window on the shared-memory path
+#ifndef TCG_SGT_CAP
+#define TCG_SGT_CAP 4096
+#endif
+constexpr int kSmemCap = TCG_SGT_CAP;  // keys per window on the shared-memory path
 constexpr int kBigCtas = 32;    // concurrent big-window CTAs (bitmap scratch each)
 constexpr int kBigThreads = 512;
 
