@@ -9,9 +9,10 @@
 // correct sort yields bit-exact reference output.
 //
 // Kernels (tcg_sgt = tcg_sgt_count + tcg_sgt_fill, stream-ordered):
-//   sgt_rank     one CTA per window: (col<<32 | local edge) keys -> smem
-//                bitonic sort -> head flags -> block scan -> edge_to_col,
-//                u_w. Windows with more than kSmemCap edges are queued.
+//   sgt_rank     one CTA per window: column ids -> smem bitonic sort -> head
+//                flags -> block scan -> compacted unique set; edge_to_col by
+//                binary search in it, u_w. Windows with more than kSmemCap
+//                edges are queued.
 //   sgt_rank_big the queued windows: bitmap over the node range in global
 //                scratch, rank = prefix popcount (no sort).
 //   cub ExclusiveSum of u_w -> col_offsets.
@@ -41,7 +42,12 @@ __global__ void __launch_bounds__(kRankThreads)
     sgt_rank(const int64_t* __restrict__ ptr, const uint32_t* __restrict__ cols, int64_t n,
              int64_t num_windows, int bh, uint32_t* __restrict__ e2c,
              int64_t* __restrict__ ucount, int* __restrict__ big_list, int* __restrict__ big_count) {
-  __shared__ uint64_t keys[kSmemCap];
+  // 32-bit column ids are sorted (half the shared-memory traffic of sorting
+  // (col, edge) pairs), compacted to the window's unique set, and every edge
+  // is ranked by a binary search in it -- the reference's unique +
+  // searchsorted (sgt.py:116-120)
+  __shared__ uint32_t keys[kSmemCap];
+  __shared__ uint32_t uniq[kSmemCap];
   __shared__ int scan_scratch[33];
   const int tid = threadIdx.x;
   for (int64_t w = blockIdx.x; w < num_windows; w += gridDim.x) {
@@ -61,8 +67,7 @@ __global__ void __launch_bounds__(kRankThreads)
       continue;
     }
     const uint32_t P = pow2_ceil((uint32_t)E);
-    for (uint32_t i = tid; i < P; i += kRankThreads)
-      keys[i] = i < E ? ((uint64_t)cols[e0 + i] << 32) | i : ~0ull;
+    for (uint32_t i = tid; i < P; i += kRankThreads) keys[i] = i < E ? cols[e0 + i] : ~0u;
     __syncthreads();
     // bitonic sort, ascending
     for (uint32_t k = 2; k <= P; k <<= 1) {
@@ -70,7 +75,7 @@ __global__ void __launch_bounds__(kRankThreads)
         for (uint32_t i = tid; i < (P >> 1); i += kRankThreads) {
           const uint32_t lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
           const uint32_t hi = lo | j;
-          const uint64_t a = keys[lo], b = keys[hi];
+          const uint32_t a = keys[lo], b = keys[hi];
           const bool up = (lo & k) == 0;
           if ((a > b) == up) {
             keys[lo] = b;
@@ -80,17 +85,26 @@ __global__ void __launch_bounds__(kRankThreads)
         __syncthreads();
       }
     }
-    // head flags over contiguous per-thread chunks, block scan -> ranks
+    // head flags over contiguous per-thread chunks, block scan -> compacted set
     const uint32_t per = (uint32_t)((E + kRankThreads - 1) / kRankThreads);
     const uint32_t beg = min((uint32_t)E, tid * per), end = min((uint32_t)E, beg + per);
     int heads = 0;
-    for (uint32_t i = beg; i < end; ++i)
-      heads += (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;
+    for (uint32_t i = beg; i < end; ++i) heads += (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
     int total;
     int rank = block_excl_scan<kRankThreads>(heads, scan_scratch, &total);
-    for (uint32_t i = beg; i < end; ++i) {
-      rank += (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;
-      e2c[e0 + (keys[i] & 0xffffffffu)] = (uint32_t)(rank - 1);
+    for (uint32_t i = beg; i < end; ++i)
+      if (i == 0 || keys[i] != keys[i - 1]) uniq[rank++] = keys[i];
+    __syncthreads();
+    // rank of every edge's column in the unique set (lower bound)
+    for (int64_t i = tid; i < E; i += kRankThreads) {
+      const uint32_t c = cols[e0 + i];
+      int lo = 0, hi = total;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (uniq[mid] < c) lo = mid + 1;
+        else hi = mid;
+      }
+      e2c[e0 + i] = (uint32_t)lo;
     }
     if (tid == 0) ucount[w] = total;
     __syncthreads();
