@@ -296,6 +296,20 @@ int tcg_softmax_xent_backward(const float* logits, int64_t ld, const int64_t* la
 /* ---- TF32 operand rounding: reference tiles.quantize_tf32 (67-82) ------- */
 int tcg_quantize_tf32(const float* in, float* out, int64_t n, void* stream);
 
+/* ---- direct CSR evaluation (the reference oracle API) ------------------------
+ * Replace tcgraph.oracle.ref_spmm / ref_sddmm (oracle.py:28-91): no tiling,
+ * CSR order. acc_f64 = 0: f32 fold, product rounded then add rounded, from
+ * +0.0 (oracle.py:54-59, 86-90), bitwise the reference; `out` is float.
+ * acc_f64 = 1: the product (rounded in f32) is widened and summed in double;
+ * `out` is double. values = NULL means all ones. tcg_csr_sddmm needs a
+ * u32[num_edges] workspace for the edge rows. */
+int tcg_csr_spmm(const int64_t* node_ptr, const uint32_t* edge_list, const float* values,
+                 int64_t num_nodes, const float* x, int64_t ldx, int64_t dim, void* out,
+                 int64_t ldo, int32_t acc_f64, void* stream);
+int tcg_csr_sddmm(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_nodes,
+                  int64_t num_edges, const float* x, int64_t ldx, int64_t dim, uint32_t* row_ws,
+                  void* out, int32_t acc_f64, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

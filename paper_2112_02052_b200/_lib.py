@@ -68,7 +68,7 @@ SIGNATURES = {
     "tcg_edge_frag": (C.c_int, [C.POINTER(TcgTiling), _P, _P]),
     "tcg_edge_to_row": (C.c_int, [_P, _I64, _I32, _P, _P]),
     "tcg_block_stream": (C.c_int, [C.POINTER(TcgTiling), _P, _P, _P]),
-    "tcg_permute_f32": (C.c_int, [_P, _P, _I64, _P, _P]),
+    "tcg_permute_f32": (C.c_int, [_P, _P, _P, _I64, _P]),
     "tcg_permute2_f32": (C.c_int, [_P, _P, _P, _P, _P, _I64, _P]),
     "tcg_csr_transpose_workspace_bytes": (_SZ, [_I64, _I64]),
     "tcg_csr_transpose": (C.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P, _SZ, _P]),
@@ -92,6 +92,8 @@ SIGNATURES = {
     "tcg_scatter_f32": (C.c_int, [_P, _P, _P, _I64, _P]),
     "tcg_invert_perm": (C.c_int, [_P, _I64, _P, _P]),
     "tcg_quantize_tf32": (C.c_int, [_P, _P, _I64, _P]),
+    "tcg_csr_spmm": (C.c_int, [_P, _P, _P, _I64, _P, _I64, _I64, _P, _I64, _I32, _P]),
+    "tcg_csr_sddmm": (C.c_int, [_P, _P, _I64, _I64, _P, _I64, _I64, _P, _P, _I32, _P]),
     "tcg_dense": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _I32, _P, _I32, _P, _I64, _P, _I64,
                             _P]),
     "tcg_gemm_tn_workspace_bytes": (_SZ, [_I64, _I64, _I64]),

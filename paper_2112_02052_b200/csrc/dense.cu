@@ -196,14 +196,18 @@ __global__ void __launch_bounds__(256)
     for (int o = 4; o > 0; o >>= 1) sm += __shfl_xor_sync(gm, sm, o);
     const float lse = mx + logf(sm);
     const int64_t lab = labels[row];
+    // a label outside [0, c) (e.g. an ignore index) poisons the loss and the
+    // row's gradient with NaN instead of reading out of bounds
+    const bool ok = lab >= 0 && lab < c;
+    const float bad = __int_as_float(0x7fc00000);
     if constexpr (GRAD) {
       const float inv_n = (gscale ? __ldg(gscale) : 1.f) / (float)n;
       for (int j = sub; j < c; j += 8) {
         const float pj = expf(__ldg(lr + j) - lse);
-        dlogits[row * ldd + j] = (pj - (j == lab ? 1.f : 0.f)) * inv_n;
+        dlogits[row * ldd + j] = ok ? (pj - (j == lab ? 1.f : 0.f)) * inv_n : bad;
       }
     }
-    contrib = lse - lr[lab];
+    contrib = ok ? lse - __ldg(lr + lab) : bad;
   }
   if constexpr (!LOSS) return;
   if (sub == 0) rowc[lr_] = contrib;

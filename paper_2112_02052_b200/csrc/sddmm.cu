@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cstdlib>
 // Edge attention scores F[e] = <Xa[row e], Xb[col e]> over the SGT tiling —
 // replaces the reference kernels.sddmm (/root/reference/pkg/src/tcgraph/
@@ -192,6 +193,14 @@ extern "C" int tcg_sddmm(const tcg_tiling* t, const float* xa, int64_t lda, cons
   return TCG_OK;
 }
 
+// Output row r of a window-range call lands at y[r - y_row0]: valid when
+// 0 <= y_row0 <= the range's first row (empty ranges write nothing).
+static bool row0_ok(const tcg_tiling* t, int64_t win_begin, int64_t win_end, int64_t y_row0) {
+  const int64_t rb = win_begin * t->blk_h;
+  const int64_t re = std::min<int64_t>(win_end * (int64_t)t->blk_h, t->num_nodes);
+  return rb >= re || (y_row0 >= 0 && y_row0 <= rb);
+}
+
 extern "C" int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim,
                                 float* p, float* y, int64_t ldy, int64_t y_row0,
                                 int64_t win_begin, int64_t win_end, void* stream) {
@@ -201,6 +210,8 @@ extern "C" int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz
               "tf32 mode requires the 16x8 tile shape, got %dx%d", t->blk_h, t->blk_w);
   TCG_REQUIRE(0 <= win_begin && win_begin <= win_end && win_end <= t->num_windows,
               "tcg_agnn_forward: window range outside [0, %lld)", (long long)t->num_windows);
+  TCG_REQUIRE(row0_ok(t, win_begin, win_end, y_row0),
+              "tcg_agnn_forward: y_row0 %lld beyond first output row", (long long)y_row0);
   const int nt = win::nt_for(dim);
   static const bool no_stream = std::getenv("TCG_NO_STREAM") != nullptr;
   if (!no_stream && dim == 32 && t->num_edges > 0 && win_begin < win_end && z && p && y) {
@@ -251,6 +262,9 @@ extern "C" int tcg_agnn_backward_fused(const tcg_tiling* t, const float* z, int6
   TCG_REQUIRE(0 <= win_begin && win_begin <= win_end && win_end <= t->num_windows,
               "tcg_agnn_backward_fused: window range outside [0, %lld)",
               (long long)t->num_windows);
+  TCG_REQUIRE(row0_ok(t, win_begin, win_end, dz_row0),
+              "tcg_agnn_backward_fused: dz_row0 %lld beyond first output row",
+              (long long)dz_row0);
   static const bool no_stream = std::getenv("TCG_NO_STREAM") != nullptr;
   if (!no_stream && dim == 32 && t->num_edges > 0 && win_begin < win_end) {
     TCG_REQUIRE(z && gy && y_fwd && p && ds && dz, "tcg_agnn_backward_fused: null pointer");
@@ -277,6 +291,8 @@ extern "C" int tcg_agnn_backward(const tcg_tiling* t, const float* z, int64_t ld
               "tf32 mode requires the 16x8 tile shape, got %dx%d", t->blk_h, t->blk_w);
   TCG_REQUIRE(0 <= win_begin && win_begin <= win_end && win_end <= t->num_windows,
               "tcg_agnn_backward: window range outside [0, %lld)", (long long)t->num_windows);
+  TCG_REQUIRE(row0_ok(t, win_begin, win_end, dz_row0),
+              "tcg_agnn_backward: dz_row0 %lld beyond first output row", (long long)dz_row0);
   const int nt = win::nt_for(dim);
   if (t->num_edges == 0 || dim > 64 || !fits_fused(t, nt)) {
     if (t->num_edges) {

@@ -234,7 +234,10 @@ extern "C" int tcg_sgt_count(const int64_t* node_ptr, const uint32_t* edge_list,
   int64_t* ucount = reinterpret_cast<int64_t*>(ws + L.ucount);
   int* big_count = reinterpret_cast<int*>(ws + L.big_count);
   int* big_list = reinterpret_cast<int*>(ws + L.big_list);
-  if (W == 0) return TCG_OK;
+  if (W == 0) {  // zero-node graph: col_offsets = [0] (the reference's zeros(1))
+    if (col_offsets) TCG_CUDA(cudaMemsetAsync(col_offsets, 0, sizeof(int64_t), s), "tcg_sgt memset");
+    return TCG_OK;
+  }
   TCG_REQUIRE(node_ptr && col_offsets, "tcg_sgt: null pointer");
   TCG_CUDA(cudaMemsetAsync(ws + L.ucount, 0, sizeof(int64_t) * (W + 1), s), "tcg_sgt memset");
   TCG_CUDA(cudaMemsetAsync(big_count, 0, sizeof(int), s), "tcg_sgt memset");

@@ -149,8 +149,10 @@ extern "C" int tcg_spmm(const tcg_tiling* t, const float* x, int64_t ldx, int64_
   a.nwin = win_end - win_begin;
   a.dim = (int)dim;
   a.accumulate = accumulate;
-  TCG_REQUIRE(a.row_begin <= a.y_row0 || a.row_begin >= a.row_end,
-              "tcg_spmm: y_row0 beyond first output row");
+  // output row r lands at y[r - y_row0]: valid when 0 <= y_row0 <= first row
+  TCG_REQUIRE((a.y_row0 >= 0 && a.y_row0 <= a.row_begin) || a.row_begin >= a.row_end,
+              "tcg_spmm: y_row0 %lld beyond first output row %lld", (long long)a.y_row0,
+              (long long)a.row_begin);
 
   if (precision == TCG_PREC_F32) {
     TCG_REQUIRE(t->edge_list != nullptr || t->num_edges == 0, "tcg_spmm: null edge_list");

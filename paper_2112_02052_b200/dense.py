@@ -104,10 +104,24 @@ def colsum(x):
     return out
 
 
+def _labels(labels, n: int, device):
+    """Class labels as the kernel reads them: int64, contiguous, 1-D of length
+    n on the logits' device (int32 / host labels are converted, anything
+    else is rejected). Labels outside [0, C) turn the loss into NaN."""
+    if not torch.is_tensor(labels):
+        raise TypeError("labels must be a torch tensor")
+    if labels.dtype not in (torch.int64, torch.int32, torch.int16, torch.uint8):
+        raise TypeError(f"labels must be an integer tensor, got {labels.dtype}")
+    if labels.dim() != 1 or labels.shape[0] != n:
+        raise ValueError(f"labels must be 1-D of length {n}, got shape {tuple(labels.shape)}")
+    return labels.to(device=device, dtype=torch.int64).contiguous()
+
+
 def softmax_xent(logits, labels, grad=True):
     """(mean NLL of log_softmax, dlogits or None)."""
     lib = _lib.load()
     n, c = logits.shape
+    labels = _labels(labels, n, logits.device)
     loss = torch.empty((), dtype=torch.float32, device=logits.device)
     dl = torch.empty((n, c), dtype=torch.float32, device=logits.device) if grad else None
     wsb = int(lib.tcg_softmax_xent_workspace_bytes(n))
@@ -122,6 +136,7 @@ def softmax_xent_backward(logits, labels, grad_scale=None):
     """(softmax(logits) - onehot(labels)) / n * grad_scale (a device scalar)."""
     lib = _lib.load()
     n, c = logits.shape
+    labels = _labels(labels, n, logits.device)
     dl = rows_empty(n, c, logits.device)
     gs = None if grad_scale is None else grad_scale.float().contiguous()
     _lib.check(lib.tcg_softmax_xent_backward(logits.data_ptr(), logits.stride(0),

@@ -89,19 +89,10 @@ def read_tcgt(path, device=None) -> TiledGraph:
     c2n, off = _array(buf, off, "<u4", int(co[-1]) if W else 0, "col_to_node", path)
     if off != len(buf):
         raise GraphFormatError(f"{path}: trailing bytes after tiling payload")
-    t = TiledGraph(None, BlockConfig(blk_h=blk_h, blk_w=blk_w), int(n), int(m), int(W))
-    t._host.update(win_partition=wp.astype(np.uint32), edge_to_col=e2c.astype(np.uint32),
-                   col_offsets=co, col_to_node=c2n.astype(np.uint32))
+    t = TiledGraph(None, BlockConfig(blk_h=blk_h, blk_w=blk_w), int(n), int(m), int(W),
+                   wp.astype(np.uint32), e2c.astype(np.uint32), co, c2n.astype(np.uint32))
     if device is not None:
-        import torch
-
-        dev = torch.device(device)
-        t.dev.update(
-            win_partition=torch.from_numpy(wp.view(np.int32)).to(dev),
-            edge_to_col=torch.from_numpy(e2c.view(np.int32)).to(dev),
-            col_offsets=torch.from_numpy(co).to(dev),
-            col_to_node=torch.from_numpy(c2n.view(np.int32)).to(dev),
-            num_unique=int(co[-1]) if W else 0)
+        t._upload(device)
     return t
 
 

@@ -429,8 +429,11 @@ def segment_softmax(values, indptr):
 def gcn_layer(t: TiledGraph, x, w, b=None, mode: str | None = None, plan: TaskPlan | None = None,
               workers: int = 1, counters: Counters | None = None, engine: str = "b200"):
     """Aggregate then update: spmm(t, x) @ w + b (kernels.py:559-583); the
-    update is an fp32 GEMM (TF32 disabled) on the device."""
+    update is the fp32 tall-skinny GEMM tcg_dense (no TF32), the same kernel
+    GCNConv runs."""
     import torch
+
+    from .dense import dense, rows_ok
 
     host = not _is_torch(x)
     agg = spmm(t, x if host else x, mode=mode, plan=plan, workers=workers, counters=counters,
@@ -440,21 +443,14 @@ def gcn_layer(t: TiledGraph, x, w, b=None, mode: str | None = None, plan: TaskPl
     if wd.dim() != 2 or wd.shape[0] != aggd.shape[1]:
         raise ValueError(
             f"weight shape {tuple(wd.shape)} incompatible with aggregated dim {aggd.shape[1]}")
-    wd = wd.to(aggd.device, torch.float32)
+    wd = wd.to(aggd.device, torch.float32).contiguous()
     bd = None
     if b is not None:
         bd = torch.as_tensor(np.ascontiguousarray(b, dtype=np.float32)) if not _is_torch(b) else b
         if tuple(bd.shape) != (wd.shape[1],):
             raise ValueError(f"bias shape {tuple(bd.shape)} != ({wd.shape[1]},)")
-        bd = bd.to(aggd.device, torch.float32)
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    try:
-        out = aggd @ wd
-        if bd is not None:
-            out = out + bd
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
+        bd = bd.to(aggd.device, torch.float32).contiguous()
+    out = dense(rows_ok(aggd.to(torch.float32)), wd, bias=bd)
     return out.cpu().numpy() if host else out
 
 

@@ -11,7 +11,7 @@ the reference exposes (`win_partition`, `edge_to_col`, `col_offsets`,
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -42,20 +42,57 @@ def _to_np_u32(t) -> np.ndarray:
     return t.cpu().numpy().view(np.uint32)
 
 
-@dataclass
-class TiledGraph:
-    """SGT result (sgt.py:43-98). Device tensors live in `dev`:
-    node_ptr i64[N+1], edge_list/edge_to_col/col_to_node/win_partition as
-    int32 tensors holding u32 bits, col_offsets i64[W+1]."""
+_SGT_ARRAYS = ("win_partition", "edge_to_col", "col_offsets", "col_to_node")
 
-    graph: CsrGraph | None
-    config: BlockConfig
-    num_nodes: int
-    num_edges: int
-    num_row_windows: int
-    dev: dict = field(default_factory=dict, repr=False)
-    _host: dict = field(default_factory=dict, repr=False, compare=False)
-    _aux: dict = field(default_factory=dict, repr=False, compare=False)
+
+class TiledGraph:
+    """SGT result (sgt.py:43-98), constructed with the reference's positional
+    fields: (graph, config, num_nodes, num_edges, num_row_windows,
+    win_partition, edge_to_col, col_offsets, col_to_node, _aux).
+
+    The four arrays are resident in HBM in `dev` (node_ptr i64[N+1];
+    edge_list / edge_to_col / col_to_node / win_partition as int32 tensors
+    holding u32 bits; col_offsets i64[W+1]); the numpy views the reference
+    exposes are materialised lazily. A TiledGraph built from host arrays (as
+    reference code does) uploads them on first kernel use. `graph=None` means
+    structure only: kernels raise (sgt.py:92-98)."""
+
+    def __init__(self, graph: CsrGraph | None, config: BlockConfig, num_nodes: int,
+                 num_edges: int, num_row_windows: int, win_partition=None, edge_to_col=None,
+                 col_offsets=None, col_to_node=None, _aux: dict | None = None, *,
+                 dev: dict | None = None):
+        self.graph = graph
+        self.config = config
+        self.num_nodes = int(num_nodes)
+        self.num_edges = int(num_edges)
+        self.num_row_windows = int(num_row_windows)
+        self.dev = {} if dev is None else dev
+        self._host = {}
+        self._aux = {} if _aux is None else _aux
+        given = dict(zip(_SGT_ARRAYS, (win_partition, edge_to_col, col_offsets, col_to_node)))
+        for k, v in given.items():
+            if v is not None:
+                self._host[k] = (np.asarray(v, dtype=np.int64) if k == "col_offsets"
+                                 else np.asarray(v, dtype=np.uint32))
+
+    def __repr__(self) -> str:
+        return (f"TiledGraph(config={self.config}, num_nodes={self.num_nodes}, "
+                f"num_edges={self.num_edges}, num_row_windows={self.num_row_windows})")
+
+    def _upload(self, device=None) -> None:
+        """Host arrays (constructed from numpy / read from a file) -> HBM."""
+        import torch
+
+        if all(k in self.dev for k in _SGT_ARRAYS):
+            return
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        for k in _SGT_ARRAYS:
+            a = self._host[k]
+            self.dev[k] = torch.from_numpy(
+                np.ascontiguousarray(a if k == "col_offsets" else a.view(np.int32))).to(dev)
+        self.dev["num_unique"] = int(self._host["col_offsets"][-1]) if self.num_row_windows else 0
 
     # ---- host views (reference attribute names) ---------------------------
     def _host_array(self, name, conv):
@@ -137,8 +174,12 @@ class TiledGraph:
         """The `tcg_tiling` descriptor handed to every kernel call."""
         s = self._aux.get("abi")
         if s is None:
-            self._require_graph()
+            g = self._require_graph()
+            self._upload()
             d = self.dev
+            if "node_ptr" not in d:
+                ptr, cols, _ = g.device_arrays()
+                d.update(node_ptr=ptr, edge_list=cols)
             s = _lib.TcgTiling(
                 self.num_nodes, self.num_edges, self.num_row_windows, self.num_unique,
                 self.config.blk_h, self.config.blk_w,
@@ -330,9 +371,12 @@ class _DeviceCsr(CsrGraph):
 def count_blocks_before(g: CsrGraph, cfg: BlockConfig, device=None) -> tuple[int, np.ndarray]:
     """Occupied blk_w-wide original-column buckets per window (sgt.py:140-157).
     With `device` it is the GPU structure count on the (GPU) SGT of g — the
-    condensed columns keep each window's distinct neighbour set."""
-    if device is not None:
-        t = translate(g, cfg, device)
+    condensed columns keep each window's distinct neighbour set. The default
+    is the GPU whenever CUDA is present; `device="cpu"` keeps the host count."""
+    from .graph import _on_device
+
+    if _on_device(device):
+        t = translate(g, cfg, None if device in (None, "auto") else device)
         return structure_blocks_device(t, cfg.blk_w)
     n, bh, bw = g.num_nodes, cfg.blk_h, cfg.blk_w
     W = -(-n // bh)

@@ -156,7 +156,7 @@ def test_agnn_train_step_vs_oracle(env, oracle):
                  *[cv.weight.grad for cv in net.convs], net.lin_out.weight.grad,
                  net.lin_out.bias.grad]
     for gg, gc in zip(grads_gpu, grads_cpu):
-        assert rel_l2(gg.cpu().numpy(), gc) <= 2 * TF32_REL_L2
+        assert rel_l2(gg.cpu().numpy(), gc) <= TF32_REL_L2
     # the Adam step moved every parameter
     assert all(not np.array_equal(a, b) for a, b in zip(params0, cpu.params))
 
@@ -179,4 +179,4 @@ def test_gcn_train_step_vs_oracle(env, oracle):
     grads_cpu = [m / (1 - cpu.opt.b1) for m in cpu.opt.m]
     grads_gpu = [net.c1.weight.grad, net.c1.bias.grad, net.c2.weight.grad, net.c2.bias.grad]
     for gg, gc in zip(grads_gpu, grads_cpu):
-        assert rel_l2(gg.cpu().numpy(), gc) <= 2 * TF32_REL_L2
+        assert rel_l2(gg.cpu().numpy(), gc) <= TF32_REL_L2
