@@ -33,6 +33,11 @@
 // used by the A^T pass of the AGNN backward. Feature chunks of 8*NT (NT = 1,
 // 2, 4) run as gridDim.y slices.
 #include "common.cuh"
+
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <cstring>
 #include "window.cuh"
 
 namespace tcg {
@@ -124,22 +129,20 @@ struct Args {
 
 constexpr int kEPL = 5;    // edges per lane prefetched for the next window (160)
 
+// Ring depth, fragment area and CTA shape. Round 2 measured the alternatives
+// at arxiv D = 32 (cold, clean L2): NB 8 / MB 8 / 4 warps 35.7 us, NB 8 / MB 16
+// / 4 warps 35.9 us, NB 4 / MB 8 / 4 warps 34.9 us, against 33.8 us for this
+// shape: more bytes in flight do not help, the ring is not what bounds it.
 template <int NT, bool DUAL, bool BIG = false>
 struct Cfg {
-  static constexpr int NB = 4;                     // ring depth (blocks)
-#ifndef TCG_SPMM_NI
-#define TCG_SPMM_NI 8
-#endif
+  static constexpr int NB = 4;  // ring depth (blocks)
   // column-id ring: ids of block s + NI are requested at step s (NI >= 2 NB so
   // the ids of block s + NB have landed by then); power of two
-  static constexpr int NI = TCG_SPMM_NI;
+  static constexpr int NI = 2 * NB;
   static_assert(NI >= 2 * NB && (NI & (NI - 1)) == 0, "column-id ring depth");
   static constexpr int SLOT = 8 * 32 * NT;         // bytes of one operand's block
   static constexpr int OPS = DUAL ? 2 : 1;
-#ifndef TCG_SPMM_MB
-#define TCG_SPMM_MB 16
-#endif
-  static constexpr int MB = (DUAL || BIG) ? 8 : TCG_SPMM_MB;  // A-fragment blocks resident (one round)
+  static constexpr int MB = (DUAL || BIG) ? 8 : 16;  // A-fragment blocks resident (one round)
   static constexpr int RING = NB * SLOT * OPS;
   static constexpr int IDX = NI * 32;              // column-id pairs of NI blocks
   static constexpr int AFR = MB * 512 * OPS;
@@ -172,11 +175,7 @@ __device__ __forceinline__ int warp_lower_bound(const int32_t* __restrict__ a, i
 }
 
 template <int NT, bool DUAL, bool BIG, bool MASK>
-#ifndef TCG_SPMM_MINB
-#define TCG_SPMM_MINB 1
-#endif
-__global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32,
-                                  (DUAL || BIG) ? 1 : TCG_SPMM_MINB) spmm_stream(const Args a) {
+__global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32, 1) spmm_stream(const Args a) {
   using C = Cfg<NT, DUAL, BIG>;
   constexpr int NB = C::NB, NI = C::NI, SLOT = C::SLOT, MB = C::MB;
   constexpr uint32_t RS = MB * 128;  // fragment slots of one round
@@ -474,8 +473,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32,
           lds_slice<NT>(x1, xs + xo + d1);
           const uint4 af = lds_frag(fa);
 #pragma unroll
-          for (int j = 0; j < NT; ++j)
-            mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
+          for (int j = 0; j < NT; ++j) mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
         }
         if constexpr (DUAL) {
           float x0[NT], x1[NT];
@@ -483,8 +481,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32,
           lds_slice<NT>(x1, xs + xo + SLOT + d1);
           const uint4 af = lds_frag(fa + MB * 512);
 #pragma unroll
-          for (int j = 0; j < NT; ++j)
-            mma_tf32(acc[j], af.x, af.y, af.z, af.w, tf32_rn(x0[j]), tf32_rn(x1[j]));
+          for (int j = 0; j < NT; ++j) mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
         }
         // refill: X of block s + NB into this slot, ids of block s + 2NB
         issue_x(xo, io);
@@ -508,6 +505,304 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32,
     e0 = e1, e1 = e2, e2 = e3, e3 = ptr_of(w + 4);
   }
   cp_wait<0>();
+}
+
+// ---- TMA-gather block stream (round 2) -----------------------------------------
+//
+// The neighbour rows of a block are fetched by two TMA tile::gather4 loads
+// (UTMALDG.GATHER4: 4 rows of the 2-D tensor map each) straight into a per-warp
+// shared-memory ring with an mbarrier per slot, so the gather bypasses the L1
+// data pipe and the registers: the bytes in flight live in shared memory
+// (NS KB per warp) and a block costs two single-lane TMA instructions. The
+// column ids of block s + NI are copied (cp.async, 16 B by lanes 0-1) NS steps
+// before the gathers that use them. The ring slot of a block holds its rows in
+// the column stream's pair-interleaved order (c0 c4 c1 c5 | c2 c6 c3 c7), so
+// mma lane (g, t) reads k-rows t / t+4 from slot rows 2t / 2t+1; with the
+// 128-B TMA swizzle (chunk ^= row) these LDS.128 are conflict-free.
+template <int MB_, int NS_>
+struct TmaCfg {
+  static constexpr int MB = MB_, NS = NS_, NI = 2 * NS_;
+  static_assert((NI & (NI - 1)) == 0 && NI <= TCG_STREAM_PAD, "id ring depth");
+  static constexpr int RING = NS * 1024;
+  static constexpr int AFR = MB * 512;
+  static constexpr int IDX = NI * 32;
+  static constexpr int BAR = NS * 8;
+  static constexpr int WARP = (RING + AFR + IDX + BAR + 1023) & ~1023;
+  static constexpr int WPC = 4;
+  static constexpr int SMEM = WPC * WARP + 1024;  // + alignment slack
+};
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nTCG_MBW:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra TCG_MBW;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* tm, int x, uint4 rows,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(rows.x), "r"(rows.y), "r"(rows.z), "r"(rows.w),
+      "r"(bar)
+      : "memory");
+}
+
+template <int MB_, int NS_>
+__global__ void __launch_bounds__(TmaCfg<MB_, NS_>::WPC * 32)
+    spmm_tma(const Args a, const __grid_constant__ CUtensorMap tmx) {
+  using C = TmaCfg<MB_, NS_>;
+  constexpr int MB = C::MB, NS = C::NS, NI = C::NI;
+  constexpr uint32_t RS = MB * 128;
+  extern __shared__ unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gw = blockIdx.x * C::WPC + wid;
+  const int g = lane >> 2, t = lane & 3;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t ring = base + wid * C::WARP;
+  const uint32_t afr_s = ring + C::RING;
+  uint32_t* afr = reinterpret_cast<uint32_t*>(smem_raw + (afr_s - smem_u32(smem_raw)));
+  const uint32_t iring = afr_s + C::AFR;
+  const unsigned char* iring_p = smem_raw + (iring - smem_u32(smem_raw));
+  const uint32_t bars = iring + C::IDX;
+
+  const int B0 = __ldg(a.boff + a.win_begin), B1 = __ldg(a.boff + a.win_end);
+  const int64_t TBr = B1 - B0;
+  const int lo_b = B0 + (int)(TBr * gw / a.nwarps);
+  const int hi_b = B0 + (int)(TBr * (gw + 1) / a.nwarps);
+  const int ws = warp_lower_bound(a.boff, a.win_begin, a.win_end, lo_b);
+  const int we = gw + 1 == a.nwarps ? a.win_end : warp_lower_bound(a.boff, ws, a.win_end, hi_b);
+  if (ws >= we) return;
+  const int gb0 = __ldg(a.boff + ws);
+  const int nb = __ldg(a.boff + we) - gb0;
+  const int xcol = a.d0 + blockIdx.y * 32;
+
+  if (lane == 0) {
+    for (int q = 0; q < NS; ++q) mbar_init(bars + 8 * q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // ids: lanes 0-1 copy 16 B (half a block) each; each lane only reads back its own
+  const char* csl = reinterpret_cast<const char*>(a.cs + 8 * (int64_t)gb0) + 16 * lane;
+  const uint32_t is = iring + 16 * lane;
+  auto copy_ids = [&](int b) {
+    if (lane < 2) cp_async<16>(is + (b & (NI - 1)) * 32, csl + 32 * (int64_t)b);
+  };
+  auto issue_rows = [&](int b) {  // after the ids of block b have landed
+    if (lane < 2 && b < nb) {
+      const uint4 r = *reinterpret_cast<const uint4*>(iring_p + (b & (NI - 1)) * 32 + 16 * lane);
+      const uint32_t bar = bars + 8 * (b % NS);
+      if (lane == 0) mbar_expect_tx(bar, 1024);
+      tma_gather4(ring + (b % NS) * 1024 + 512 * lane, &tmx, xcol, r, bar);
+    }
+  };
+  for (int b = 0; b < NS; ++b) copy_ids(b);
+  cp_commit();
+  cp_wait<0>();
+  for (int b = 0; b < NS; ++b) issue_rows(b);
+  for (int b = NS; b < NI; ++b) {
+    copy_ids(b);
+    cp_commit();
+  }
+
+  auto ptr_of = [&](int w) { return (int64_t)__ldg(a.ptr + min((int64_t)w * 16, a.n)); };
+  auto blk_of = [&](int w) { return __ldg(a.boff + min(w, a.win_end)) - gb0; };
+  int w = ws;
+  int cb0 = 0, cb1 = blk_of(ws + 1), nb2 = blk_of(ws + 2), nb3 = blk_of(ws + 3);
+  int64_t e0 = ptr_of(ws), e1 = ptr_of(ws + 1), e2 = ptr_of(ws + 2), e3 = ptr_of(ws + 3);
+  uint32_t pf[kEPL], of[kEPL];
+  float pw[kEPL], ow[kEPL];
+  auto weight = [&](int64_t e) {
+    return a.w ? (a.widx ? __ldg(a.w + __ldg(a.widx + e)) : __ldg(a.w + e)) : 1.f;
+  };
+  auto prefetch = [&](int64_t lo, int64_t hi) {
+#pragma unroll
+    for (int k = 0; k < kEPL; ++k) {
+      const int64_t e = lo + lane + 32 * k;
+      const bool ok = e < hi;
+      pf[k] = ok ? __ldg(a.efrag + e) : 0xffffffffu;
+      pw[k] = ok ? weight(e) : 0.f;
+    }
+  };
+  auto clear_frags = [&]() {
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < MB; ++q) reinterpret_cast<uint4*>(afr)[q * 32 + lane] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+  };
+  auto put_round = [&](uint32_t lo, bool zero) {
+#pragma unroll
+    for (int k = 0; k < kEPL; ++k) {
+      const uint32_t f = of[k] - lo;
+      if (f < RS) afr[f] = zero ? 0u : tf32_rn(ow[k]);
+    }
+  };
+  auto hub_load = [&](int r0) {
+    clear_frags();
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const uint32_t f = __ldg(a.efrag + e) - (uint32_t)(r0 * 128);
+      if (f < RS) afr[f] = tf32_rn(weight(e));
+    }
+    __syncwarp();
+  };
+  float acc[4][4];
+  auto store = [&]() {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t r = (int64_t)w * 16 + g + 8 * h;
+      if (r >= a.n) continue;
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] = acc[j][2 * h] + 0.f, o[4 + j] = acc[j][2 * h + 1] + 0.f;
+      const int fo = xcol + 8 * t;
+      float* yr = a.y + (r - a.y_row0) * a.ldy + fo;
+      if (a.bias) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] += __ldg(a.bias + fo + q);
+      }
+      if (a.accumulate) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] += yr[q];
+      }
+      if (!a.vec_out) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) yr[q] = o[q];
+      } else {
+        reinterpret_cast<float4*>(yr)[0] = make_float4(o[0], o[1], o[2], o[3]);
+        reinterpret_cast<float4*>(yr)[1] = make_float4(o[4], o[5], o[6], o[7]);
+      }
+    }
+  };
+  bool hub = false;
+  auto begin_window = [&]() {
+#pragma unroll
+    for (int k = 0; k < kEPL; ++k) of[k] = pf[k], ow[k] = pw[k];
+    hub = e1 - e0 > 32 * kEPL;
+    __syncwarp();
+    if (!hub) {
+      put_round(0, false);
+      __syncwarp();
+    } else {
+      hub_load(0);
+    }
+    prefetch(e1, e2);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  };
+  auto end_window = [&]() {
+    store();
+    const int nbw = cb1 - cb0;
+    __syncwarp();
+    if (!hub) {
+      put_round((uint32_t)(nbw > 0 ? ((nbw - 1) & ~(MB - 1)) : 0) * 128, true);
+    } else {
+      clear_frags();
+    }
+    ++w;
+    cb0 = cb1, cb1 = nb2, nb2 = nb3, nb3 = blk_of(w + 3);
+    e0 = e1, e1 = e2, e2 = e3, e3 = ptr_of(w + 3);
+  };
+
+  // lane (g, t): k-row t is slot row 2t, k-row t+4 is slot row 2t+1 (128-B swizzle)
+  const uint32_t b0o = (2 * t) * 128 + ((g ^ (2 * t)) & 7) * 16;
+  const uint32_t b1o = (2 * t + 1) * 128 + ((g ^ (2 * t + 1)) & 7) * 16;
+  const uint32_t as = afr_s + lane * 16;
+  clear_frags();
+  prefetch(e0, e1);
+  begin_window();
+  for (int s = 0; s < nb; ++s) {
+    while (s == cb1) {
+      end_window();
+      begin_window();
+    }
+    const int lb = s - cb0;
+    if (lb > 0 && (lb & (MB - 1)) == 0) {
+      if (!hub) {
+        __syncwarp();
+        put_round((uint32_t)(lb - MB) * 128, true);
+        __syncwarp();
+        put_round((uint32_t)lb * 128, false);
+        __syncwarp();
+      } else {
+        hub_load(lb);
+      }
+    }
+    const uint32_t slot = ring + (s % NS) * 1024;
+    mbar_wait(bars + 8 * (s % NS), (uint32_t)(s / NS) & 1u);
+    {
+      float x0[4], x1[4];
+      lds_slice<4>(x0, slot + b0o);
+      lds_slice<4>(x1, slot + b1o);
+      const uint4 af = lds_frag(as + (uint32_t)(lb & (MB - 1)) * 512);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
+    }
+    __syncwarp();
+    // refill this slot: ids of block s + NS (copied NS steps ago), then ids of s + NI
+    cp_wait<NS - 1>();
+    issue_rows(s + NS);
+    copy_ids(s + NI);
+    cp_commit();
+  }
+  for (;;) {
+    end_window();
+    if (w >= we) break;
+    begin_window();
+  }
+  cp_wait<0>();
+}
+
+template <int MB, int NS>
+int launch_tma(Args& a, const CUtensorMap& tm, int nchunks, cudaStream_t s) {
+  using C = TmaCfg<MB, NS>;
+  auto kern = spmm_tma<MB, NS>;
+  static int configured = -1;
+  int dev = 0;
+  TCG_CUDA(cudaGetDevice(&dev), "spmm_tma device");
+  if (configured != dev) {
+    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
+             "spmm_tma attr");
+    configured = dev;
+  }
+  int per_sm = 1;
+  TCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPC * 32, C::SMEM),
+           "spmm_tma occupancy");
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ctas = (int64_t)num_sms() * per_sm;
+  a.nwarps = (int)(ctas * C::WPC);
+  dim3 grid((unsigned)ctas, (unsigned)nchunks);
+  kern<<<grid, C::WPC * 32, C::SMEM, s>>>(a, tm);
+  TCG_LAUNCHED("spmm_tma");
+  return TCG_OK;
+}
+
+// 2-D tensor map over X (rows = nodes, inner = features), 32-feature boxes of one
+// row, 128-B swizzle: the operand of tile::gather4. false when it cannot be made.
+bool make_row_map(CUtensorMap* tm, const float* x, int64_t rows, int64_t dim, int64_t ld) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fp);
+  }();
+  if (!enc || rows < 1 || rows >= (1LL << 31) || (reinterpret_cast<uintptr_t>(x) & 15) || (ld * 4) % 16)
+    return false;
+  cuuint64_t gd[2] = {(cuuint64_t)dim, (cuuint64_t)rows};
+  cuuint64_t gs[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32, 1}, es[2] = {1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x), gd, gs, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // ---- fused AGNN aggregation on the block stream (D = 32) -------------------
@@ -1021,6 +1316,16 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
     const bool mk = a.dv < 8 * nt;
     a.x16 = nt == 2 && al(q.x + a.d0, 16) && (q.ldx * 4) % 16 == 0 &&
             (!dual || (al(q.x2 + a.d0, 16) && (q.ldx2 * 4) % 16 == 0));
+    // TMA tile::gather4 engine: opt-in (TCG_SPMM_ENGINE=tma), measured slower
+    // than the cp.async ring on B200 (profiles/r02)
+    static const char* eng = std::getenv("TCG_SPMM_ENGINE");
+    const bool use_tma = eng && std::strcmp(eng, "tma") == 0;
+    if (use_tma && !dual && !big && !mk && nt == 4) {
+      CUtensorMap tm;
+      if (stream::make_row_map(&tm, q.x, q.n, q.dim, q.ldx)) {
+        return stream::launch_tma<8, 8>(a, tm, nchunks, s);
+      }
+    }
 #define TCG_SL(NTV, MK)                                                                   \
   if (nt == NTV && mk == MK)                                                              \
     return big ? (dual ? stream::launch_t<NTV, true, true, MK>(a, nchunks, s)             \

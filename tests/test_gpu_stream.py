@@ -243,3 +243,47 @@ def test_stream_spmm_big_windows(env, oracle, dim):
                              x2=torch.from_numpy(x2).cuda(), weights2=torch.from_numpy(w2).cuda())
     ref = oracle.spmm(ptr, cols, x, f=w) + oracle.spmm(ptr, cols, x2, f=w2)
     assert rel_l2(yd.cpu().numpy(), ref) <= TF32_REL_L2
+
+
+_TMA_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import torch
+import paper_2112_02052_b200 as tcg
+from paper_2112_02052_b200 import _lib
+from oracle import tcg_oracle as oracle
+from paper_2112_02052_b200.kernels import spmm_device
+worst = 0.0
+for n, deg, d, seed in ((3001, 7, 32, 1), (1500, 12, 64, 2), (777, 3, 40, 3)):
+    g = tcg.synth.gen_uniform(n, deg, seed)
+    t = tcg.translate(g, tcg.BlockConfig())
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    w = rng.random(g.num_edges).astype(np.float32)
+    c0 = _lib.launch_count()
+    y = spmm_device(t, torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), mode="tf32")
+    torch.cuda.synchronize()
+    assert _lib.launch_count() > c0
+    ref = oracle.spmm(g.node_pointer, g.edge_list, x, f=w)
+    e = float(np.linalg.norm(y.cpu().numpy() - ref) / np.linalg.norm(ref))
+    worst = max(worst, e)
+print(worst)
+"""
+
+
+def test_tma_gather_engine_opt_in(tmp_path):
+    """The opt-in TMA tile::gather4 SpMM (TCG_SPMM_ENGINE=tma; measured slower
+    than the cp.async ring, kept as the A/B of DESIGN.md section 3) matches
+    the oracle, including a 64-wide (two chunk) and a masked 40-wide operand."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    env = dict(os.environ, TCG_SPMM_ENGINE="tma")
+    r = subprocess.run([sys.executable, "-c", _TMA_SCRIPT, str(ROOT)], env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= TF32_REL_L2
