@@ -112,9 +112,11 @@ int tcg_structure_blocks(const tcg_tiling* t, int64_t tile_width, int64_t* per_w
 size_t tcg_sgt_workspace_bytes(int64_t num_nodes, int64_t num_edges, int32_t blk_h);
 /* Two-phase form. tcg_sgt_count writes edge_to_col[M]
  * and col_offsets[W+1] (exclusive scan of the per-window unique counts, so
- * U = col_offsets[W]); the caller reads U, allocates col_to_node[U] and calls
- * tcg_sgt_fill, which writes col_to_node and win_partition[W]. Workspace as
- * tcg_sgt_workspace_bytes (count only; fill needs none). */
+ * U = col_offsets[W]); the caller allocates col_to_node (U entries, or its
+ * upper bound M without reading U back) and calls tcg_sgt_fill, which writes
+ * col_to_node and win_partition[W]. Windows of <= 512 edges are ranked by one
+ * warp each (register bitonic sort of (column, edge) keys, warp-scan dedup);
+ * larger ones by a CTA. Workspace as tcg_sgt_workspace_bytes (count only). */
 int tcg_sgt_count(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_nodes,
                   int64_t num_edges, int32_t blk_h, int32_t blk_w, uint32_t* edge_to_col,
                   int64_t* col_offsets, void* workspace, size_t workspace_bytes, void* stream);
@@ -122,6 +124,25 @@ int tcg_sgt_fill(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num
                  int64_t num_edges, int32_t blk_h, int32_t blk_w, const uint32_t* edge_to_col,
                  const int64_t* col_offsets, uint32_t* win_partition, uint32_t* col_to_node,
                  void* stream);
+/* Row-window shard of SGT (windows are independent; no
+ * reference counterpart, sgt.py:101-137 restricted to windows
+ * [win_begin, win_end)). Count: edge_to_col of the range's edges,
+ * win_partition[win_begin..win_end) and col_offsets[win_begin..win_end] =
+ * exclusive scan of the range's unique counts starting at 0 (arrays are
+ * global-sized; nothing outside the range is touched). Fill: col_to_node at
+ * col_offsets[w] + base for the range's windows, then
+ * col_offsets[win_begin..win_end] += base -- with base = the exclusive scan of
+ * the lower shards' totals the range matches the whole-graph SGT bit for bit.
+ * tcg_sgt_count / tcg_sgt_fill / tcg_sgt are the whole-graph forms. */
+int tcg_sgt_count_range(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_nodes,
+                        int64_t num_edges, int32_t blk_h, int32_t blk_w, int64_t win_begin,
+                        int64_t win_end, uint32_t* edge_to_col, int64_t* col_offsets,
+                        uint32_t* win_partition, void* workspace, size_t workspace_bytes,
+                        void* stream);
+int tcg_sgt_fill_range(const int64_t* node_ptr, const uint32_t* edge_list, int64_t num_nodes,
+                       int64_t num_edges, int32_t blk_h, int64_t win_begin, int64_t win_end,
+                       int64_t base, const uint32_t* edge_to_col, int64_t* col_offsets,
+                       uint32_t* col_to_node, void* stream);
 /* One stream-ordered call (count + fill): per-window sort/dedup/rank on the GPU.
  * Writes win_partition[W], edge_to_col[M], col_offsets[W+1] and
  * col_to_node[0..U) where U = col_offsets[W] (col_to_node capacity must be

@@ -65,6 +65,9 @@ SIGNATURES = {
     "tcg_sgt": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
     "tcg_sgt_count": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _SZ, _P]),
     "tcg_sgt_fill": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
+    "tcg_sgt_count_range": (C.c_int, [_P, _P, _I64, _I64, _I32, _I32, _I64, _I64, _P, _P, _P, _P, _SZ,
+                                      _P]),
+    "tcg_sgt_fill_range": (C.c_int, [_P, _P, _I64, _I64, _I32, _I64, _I64, _I64, _P, _P, _P, _P]),
     "tcg_edge_frag": (C.c_int, [C.POINTER(TcgTiling), _P, _P]),
     "tcg_edge_to_row": (C.c_int, [_P, _I64, _I32, _P, _P]),
     "tcg_block_stream": (C.c_int, [C.POINTER(TcgTiling), _P, _P, _P]),

@@ -116,13 +116,18 @@ class TiledGraph:
 
     @property
     def col_to_node(self) -> np.ndarray:
-        return self._host_array("col_to_node", _to_np_u32)
+        # the device array may be allocated at its upper bound (GPU SGT): U first
+        return self._host_array("col_to_node", lambda t: _to_np_u32(t[: self.num_unique]))
 
     @property
     def num_unique(self) -> int:
-        if "num_unique" in self.dev:
-            return int(self.dev["num_unique"])
-        return int(self.col_offsets[-1]) if self.num_row_windows else 0
+        if "num_unique" not in self.dev:
+            if "col_offsets" in self.dev:
+                co = self.dev["col_offsets"]
+                self.dev["num_unique"] = int(co[-1].item()) if self.num_row_windows else 0
+            else:
+                return int(self.col_offsets[-1]) if self.num_row_windows else 0
+        return int(self.dev["num_unique"])
 
     def unique_count(self, window: int) -> int:
         return int(self.col_offsets[window + 1] - self.col_offsets[window])
@@ -283,18 +288,90 @@ def _sgt_device(ptr, cols, n: int, m: int, cfg: BlockConfig, graph) -> TiledGrap
     wsb = int(lib.tcg_sgt_workspace_bytes(n, m, cfg.blk_h))
     ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
     cp = cols.data_ptr() if m else None
-    # two-phase: ranks + scanned counts, then col_to_node sized exactly U
+    # two phases, no host round trip between them: col_to_node is allocated at
+    # its upper bound M (U <= M) and U = col_offsets[W] is read lazily, on the
+    # first use that needs it as a host integer (TiledGraph.num_unique)
     _lib.check(lib.tcg_sgt_count(ptr.data_ptr(), cp, n, m, cfg.blk_h, cfg.blk_w, e2c.data_ptr(),
                                  offs.data_ptr(), ws.data_ptr(), wsb, _stream_ptr()), "tcg_sgt")
-    u = int(offs[-1].item()) if W else 0
-    c2n = torch.empty(max(u, 1), dtype=torch.int32, device=dev)
+    c2n = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
     _lib.check(lib.tcg_sgt_fill(ptr.data_ptr(), cp, n, m, cfg.blk_h, cfg.blk_w, e2c.data_ptr(),
                                 offs.data_ptr(), wp.data_ptr(), c2n.data_ptr(), _stream_ptr()),
                "tcg_sgt")
     t = TiledGraph(graph, cfg, n, m, W)
     t.dev.update(node_ptr=ptr, edge_list=cols, win_partition=wp[:W], edge_to_col=e2c[:m],
-                 col_offsets=offs, col_to_node=c2n[:u], num_unique=u)
+                 col_offsets=offs, col_to_node=c2n)
     return t
+
+
+class ShardSgt:
+    """SGT of one row-window shard [wb, we) (windows are
+    independent, so a rank translates only its own). Phase 1 (`count`) ranks
+    the shard's edges and scans its unique counts from 0; the shard's total U_r
+    is `total` (a device scalar). Phase 2 (`fill`) writes col_to_node at the
+    global offsets once `base` = sum of the lower shards' totals is known (an
+    exclusive scan of P integers: dist.translate_sharded all-gathers them).
+    The result is a TiledGraph with global-sized arrays of which only the
+    shard's windows / edges are filled -- bit for bit the whole-graph SGT
+    restricted to the shard; kernels run on it with win_range = (wb, we)."""
+
+    def __init__(self, g: CsrGraph, cfg: BlockConfig, win_range: tuple[int, int], device=None):
+        import torch
+
+        if not isinstance(cfg, BlockConfig):
+            raise TypeError("cfg must be a BlockConfig")
+        self.g, self.cfg = g, cfg
+        self.ptr, self.cols, _ = g.device_arrays(device)
+        n, m = g.num_nodes, g.num_edges
+        self.W = -(-n // cfg.blk_h)
+        wb, we = (int(win_range[0]), int(win_range[1]))
+        if not 0 <= wb <= we <= self.W:
+            raise IndexError(f"window range [{wb}, {we}) outside [0, {self.W})")
+        self.wb, self.we = wb, we
+        dev = self.ptr.device
+        self.wp = torch.zeros(max(self.W, 1), dtype=torch.int32, device=dev)
+        self.e2c = torch.zeros(max(m, 1), dtype=torch.int32, device=dev)
+        self.offs = torch.zeros(self.W + 1, dtype=torch.int64, device=dev)
+        self.c2n = torch.zeros(max(m, 1), dtype=torch.int32, device=dev)
+        self._counted = self._filled = False
+
+    def count(self) -> "ShardSgt":
+        import torch
+
+        lib = _lib.load()
+        n, m = self.g.num_nodes, self.g.num_edges
+        wsb = int(lib.tcg_sgt_workspace_bytes(n, m, self.cfg.blk_h))
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=self.ptr.device)
+        _lib.check(lib.tcg_sgt_count_range(
+            self.ptr.data_ptr(), self.cols.data_ptr() if m else None, n, m, self.cfg.blk_h,
+            self.cfg.blk_w, self.wb, self.we, self.e2c.data_ptr(), self.offs.data_ptr(),
+            self.wp.data_ptr(), ws.data_ptr(), wsb, _stream_ptr()), "tcg_sgt_count_range")
+        self._counted = True
+        return self
+
+    @property
+    def total(self):
+        """U_r, the shard's unique-column count (device int64 scalar tensor)."""
+        return self.offs[self.we: self.we + 1]
+
+    def fill(self, base: int) -> TiledGraph:
+        if not self._counted:
+            self.count()
+        n, m = self.g.num_nodes, self.g.num_edges
+        _lib.check(_lib.load().tcg_sgt_fill_range(
+            self.ptr.data_ptr(), self.cols.data_ptr() if m else None, n, m, self.cfg.blk_h,
+            self.wb, self.we, int(base), self.e2c.data_ptr(), self.offs.data_ptr(),
+            self.c2n.data_ptr(), _stream_ptr()), "tcg_sgt_fill_range")
+        t = TiledGraph(self.g, self.cfg, n, m, self.W)
+        t.dev.update(node_ptr=self.ptr, edge_list=self.cols, win_partition=self.wp[: self.W],
+                     edge_to_col=self.e2c[:m], col_offsets=self.offs, col_to_node=self.c2n)
+        t.shard_windows = (self.wb, self.we)
+        return t
+
+
+def translate_range(g: CsrGraph, cfg: BlockConfig, win_range, base: int = 0, device=None) -> TiledGraph:
+    """SGT of the windows in `win_range` only, col_offsets shifted by `base`
+    (see ShardSgt; base=0 with the full range is `translate`)."""
+    return ShardSgt(g, cfg, win_range, device).count().fill(base)
 
 
 def translate(g: CsrGraph, cfg: BlockConfig, device=None) -> TiledGraph:
