@@ -336,27 +336,42 @@ def run_ours(args):
             flush_rd.sum()
 
     # ---- SGT (timed separately, as the reference does: cli.py:149-151) ----
+    # N > 1: each rank translates only its own row windows (dist.translate_sharded:
+    # one all-gather of the shard totals for the global col_offsets base); the
+    # reported time is the max over ranks
     ptr_d, cols_d, _ = g.device_arrays(dev)
+    plan = (tdist.make_shard_plan(g.node_pointer, n, 16, rank=rank, world=world)
+            if world > 1 else None)
     sgt_ms = []
     for i in range(4):
         flush()
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         s, e = ev(), ev()
         s.record()
-        t = tcg.translate(g, cfg, device=dev)
+        if plan is None:
+            t = tcg.translate(g, cfg, device=dev)
+        else:
+            t = tdist.translate_sharded(g, cfg, plan.my_windows, device=dev)
         e.record()
         torch.cuda.synchronize()
         if i:
             sgt_ms.append(s.elapsed_time(e))
     sgt_ms = statistics.median(sgt_ms)
-    tt = t.transpose()
-    u = t.num_unique
-    W = t.num_row_windows
+    if world > 1:
+        tm = torch.tensor([sgt_ms], device=dev)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        sgt_ms = float(tm.item())
 
     shard = None
     if world > 1:
-        shard = tdist.make_shard_plan(g.node_pointer, n, 16, t.win_partition,
-                                      tt.tiled.win_partition, rank, world)
+        shard = tdist.Shard.build(g, cfg, plan, device=dev)
+        t = shard.t
+    else:
+        t.transpose()
+    u = t.num_unique
+    W = t.num_row_windows
 
     # ---- model + one training step ----
     torch.manual_seed(0)
@@ -370,8 +385,13 @@ def run_ours(args):
 
     def train_step():
         opt.zero_grad(set_to_none=True)
-        loss = layers.cross_entropy(net(x_dev, t, shard), y_dev)
+        if shard is None:
+            loss = layers.cross_entropy(net(x_dev, t), y_dev)
+        else:  # this rank's rows; weight gradients summed over the ranks
+            loss = layers.cross_entropy_sharded(net(x_dev, t, shard), y_dev, shard)
         loss.backward()
+        if shard is not None:
+            shard.allreduce_grads(net.parameters())
         opt.step()
         return loss.detach()
 
@@ -515,9 +535,11 @@ def run_ours(args):
     roofline = None
     if not args.no_extras:
         # dominant kernel: AGNN aggregation SpMM (weighted, D=hidden) alone, cold L2
+        # (N > 1: this rank's windows of its SGT shard)
         d = hidden if model_kind == "agnn" else hidden
+        wr = plan.my_windows if world > 1 else None
         z = torch.randn(n, d, device=dev)
-        p = sddmm_device(t, z, mode="tf32", epilogue=_lib.EPI_SOFTMAX)
+        p = sddmm_device(t, z, mode="tf32", epilogue=_lib.EPI_SOFTMAX, win_range=wr)
         out = torch.empty(n, d, device=dev)
 
         def kernel_ms(fn, reps=50, clean=True):
@@ -552,17 +574,27 @@ def run_ours(args):
             e.synchronize()
             return s.elapsed_time(e) / reps
 
-        spmm_fn = lambda: spmm_device(t, z, p, mode="tf32", out=out)  # noqa: E731
+        spmm_fn = lambda: spmm_device(t, z, p, mode="tf32", out=out, win_range=wr)  # noqa: E731
         t_spmm = kernel_ms(spmm_fn)
         t_spmm_dirty = kernel_ms(spmm_fn, clean=False)
         t_spmm_warm = warm_ms(spmm_fn)
-        t_spmm_f32 = kernel_ms(lambda: spmm_device(t, z, p, mode="f32", out=out))
+        t_spmm_f32 = kernel_ms(lambda: spmm_device(t, z, p, mode="f32", out=out, win_range=wr))
         sd_out = torch.empty(m, device=dev)
         t_sddmm = kernel_ms(lambda: sddmm_device(t, z, mode="tf32", epilogue=_lib.EPI_SOFTMAX,
-                                                 out=sd_out))
-        b_spmm = algorithmic_bytes_spmm(n, m, u, W, d, weighted=True)
-        b_sddmm = algorithmic_bytes_sddmm(n, m, u, W, d)
-        b_sgt = algorithmic_bytes_sgt(n, m, u, W)
+                                                 out=sd_out, win_range=wr))
+        if world > 1:
+            # per rank: the whole X is read, the rest is the shard's
+            (r0, r1), (e0, e1), (w0, w1) = plan.my_rows, plan.my_edges, plan.my_windows
+            co = t.dev["col_offsets"]
+            u_r = int((co[w1] - co[w0]).item())
+            nr, mr, wn = r1 - r0, e1 - e0, w1 - w0
+            b_spmm = 4 * n * d + 4 * nr * d + 8 * mr + 4 * u_r + 8 * (nr + 1) + 12 * wn
+            b_sddmm = 4 * n * d + 8 * mr + 4 * u_r + 8 * (nr + 1) + 12 * wn
+            b_sgt = algorithmic_bytes_sgt(nr, mr, u_r, wn)
+        else:
+            b_spmm = algorithmic_bytes_spmm(n, m, u, W, d, weighted=True)
+            b_sddmm = algorithmic_bytes_sddmm(n, m, u, W, d)
+            b_sgt = algorithmic_bytes_sgt(n, m, u, W)
         peak, peak_kind = measured_peaks()
         achieved = b_spmm / (t_spmm * 1e-3) / 1e9
         traffic = tensor_pct = None
@@ -598,13 +630,13 @@ def run_ours(args):
         t_fe = timed(lambda: tcg.CsrGraph.from_edges(src_r, dst_r, n))
         g_dev = tcg.CsrGraph.from_edges(src_r, dst_r, n)
         t_val = timed(lambda: tcg.validate(g_dev))
-        t_blk = timed(lambda: tcg.structure_blocks_before(t, 8))
+        t_blk = timed(lambda: tcg.structure_blocks_before(t, 8)) if world == 1 else None
         del src_r, dst_r, g_dev
         extras = {
             "e2e_serial_ms": round(e2e_serial, 4),
             "from_edges_ms": round(t_fe, 3),
             "validate_ms": round(t_val, 3),
-            "structure_blocks_ms": round(t_blk, 3),
+            "structure_blocks_ms": round(t_blk, 3) if t_blk is not None else None,
             "sgt_ms": round(sgt_ms, 4),
             "sgt_gbs": round(b_sgt / (sgt_ms * 1e-3) / 1e9, 1),
             "spmm_tc_us_cold": round(t_spmm * 1e3, 2),
@@ -613,7 +645,8 @@ def run_ours(args):
             "spmm_exact_f32_us_cold": round(t_spmm_f32 * 1e3, 2),
             "sddmm_softmax_tc_us_cold": round(t_sddmm * 1e3, 2),
             "sddmm_gbs": round(b_sddmm / (t_sddmm * 1e-3) / 1e9, 1),
-            "spmm_useful_gflops": round(2 * m * d / (t_spmm * 1e-3) / 1e9, 1),
+            "spmm_useful_gflops": round(2 * (m if world == 1 else plan.my_edges[1] - plan.my_edges[0])
+                                        * d / (t_spmm * 1e-3) / 1e9, 1),
             "gather_bytes_4UD": 4 * u * d,
         }
         if model_kind == "agnn" and world == 1:

@@ -152,3 +152,10 @@ def launch_count() -> int:
 
 def version() -> str:
     return load().tcg_version().decode()
+
+
+def current_stream():
+    """torch's current CUDA stream as the ABI's `void* stream`."""
+    import torch
+
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)

@@ -15,9 +15,11 @@ here keep those forward semantics and add the backward passes:
       dZ = A_dS Z + A^T_{P} G + A^T_{dS} Z            (one SpMM on A, one dual
                                                        SpMM on A^T)
 
-Every sparse op is a libtcg_b200.so kernel; the dense GEMMs are torch fp32
-(TF32 disabled). With a ShardPlan (dist.py) each rank
-computes its window range and the results are all-gathered.
+Every sparse op is a libtcg_b200.so kernel; the dense GEMMs are fp32
+libtcg_b200.so kernels too (TF32 disabled). With a Shard
+(dist.py) each rank runs its row windows and its rows of every dense op, the
+inputs of the sparse ops are all-gathered in place, and the weight gradients
+are all-reduced (Shard.allreduce_grads).
 """
 
 from __future__ import annotations
@@ -30,8 +32,16 @@ import torch.nn as nn
 import torch.nn.functional as F
 
 from . import _lib
-from .dist import ShardPlan, allgather_edges, allgather_rows
-from .dense import DenseFn, Linear, colsum, cross_entropy, rows_empty  # noqa: F401  (re-exported)
+from .dist import Shard, allgather_edges, allgather_rows
+from .dense import (  # noqa: F401  (re-exported)
+    DenseFn,
+    Linear,
+    SoftmaxXentFn,
+    colsum,
+    cross_entropy,
+    rows_empty,
+    rows_ok,
+)
 from .kernels import (
     agnn_backward_device,
     agnn_forward_device,
@@ -49,16 +59,8 @@ def _edge_weights(t: TiledGraph):
     return None if g.edge_values is None else g.device_arrays(t.device)[2]
 
 
-def _rows_out(t: TiledGraph, d: int, like: torch.Tensor, shard: ShardPlan | None):
-    if shard is None:
-        return rows_empty(t.num_nodes, d, like.device), 0, None
-    r0, _ = shard.my_rows
-    slab = torch.empty((shard.rows_max, d), dtype=torch.float32, device=like.device)
-    return slab, r0, shard.my_windows
-
-
-def _finish_rows(slab, shard):
-    return slab if shard is None else allgather_rows(slab, shard)
+def _rows_out(t: TiledGraph, d: int, like: torch.Tensor):
+    return rows_empty(t.num_nodes, d, like.device)
 
 
 def _rows16(x):
@@ -81,31 +83,67 @@ class GcnAggregate(torch.autograd.Function):
     """Y = A_w H + b, w = stored edge values (or 1)."""
 
     @staticmethod
-    def forward(ctx, h, bias, t: TiledGraph, mode: str, shard: ShardPlan | None):
+    def forward(ctx, h, bias, t: TiledGraph, mode: str):
         h = _rows16(h) if mode == "tf32" else h.contiguous()
-        out, r0, wr = _rows_out(t, h.shape[1], h, shard)
-        spmm_device(t, h, _edge_weights(t), mode=mode, out=out, bias=bias, win_range=wr,
-                    y_row0=r0)
-        ctx.t, ctx.mode, ctx.shard = t, mode, shard
+        out = _rows_out(t, h.shape[1], h)
+        spmm_device(t, h, _edge_weights(t), mode=mode, out=out, bias=bias)
+        ctx.t, ctx.mode = t, mode
         ctx.has_bias = bias is not None
-        return _finish_rows(out, shard)
+        return out
 
     @staticmethod
     def backward(ctx, g):
-        t, shard = ctx.t, ctx.shard
+        t = ctx.t
         g = _rows16(g) if ctx.mode == "tf32" else g.contiguous()
         tt = t.transpose()
-        out, r0, wr = _rows_out(t, g.shape[1], g, shard)
-        wt = _edge_weights(t)
-        if wt is not None:  # stored edge values in A^T edge order (cached per tiling)
-            key = ("edge_values_T", wt.data_ptr())
-            if key not in t._aux:
-                t._aux[key] = permute_device(wt, tt.perm)
-            wt = t._aux[key]
-        spmm_device(tt.tiled, g, wt, mode=ctx.mode, out=out, win_range=wr, y_row0=r0)
-        dh = _finish_rows(out, shard)
+        out = _rows_out(t, g.shape[1], g)
+        spmm_device(tt.tiled, g, _edge_weights_t(t, tt.perm), mode=ctx.mode, out=out)
         db = colsum(g) if ctx.has_bias else None
-        return dh, db, None, None, None
+        return out, db, None, None
+
+
+def _edge_weights_t(t: TiledGraph, perm):
+    """Stored edge values in A^T edge order (cached per tiling), or None."""
+    wt = _edge_weights(t)
+    if wt is None:
+        return None
+    key = ("edge_values_T", wt.data_ptr())
+    if key not in t._aux:
+        t._aux[key] = permute_device(wt, perm)
+    return t._aux[key]
+
+
+class GcnAggShard(torch.autograd.Function):
+    """Sharded Y_r = A_w H + b over this rank's row windows: H's rows are
+    all-gathered in place (persistent buffer), Y_r = the rank's rows. Backward:
+    G's rows all-gathered, dH_r = (A^T)_w G on this rank's A^T windows."""
+
+    @staticmethod
+    def forward(ctx, h_local, bias, sh: Shard, key, mode: str):
+        d = h_local.shape[1]
+        buf, full, mine = sh.rows_buffer(("gcn_in", key), d)
+        mine.copy_(h_local)
+        allgather_rows(buf, sh.plan, sh.group)
+        r0, r1 = sh.plan.my_rows
+        out = rows_empty(r1 - r0, d, h_local.device)
+        spmm_device(sh.t, full, _edge_weights(sh.t), mode=mode, out=out, bias=bias,
+                    win_range=sh.plan.my_windows, y_row0=r0)
+        ctx.sh, ctx.mode, ctx.has_bias = sh, mode, bias is not None
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        sh = ctx.sh
+        d = g.shape[1]
+        buf, full, mine = sh.rows_buffer("grad", d)
+        mine.copy_(g)
+        allgather_rows(buf, sh.plan, sh.group)
+        r0, r1 = sh.plan.my_rows
+        out = rows_empty(r1 - r0, d, g.device)
+        spmm_device(sh.tt, full, _edge_weights_t(sh.t, sh.perm), mode=ctx.mode, out=out,
+                    win_range=sh.plan.my_windows, y_row0=r0)
+        db = colsum(rows_ok(g)) if ctx.has_bias else None
+        return out, db, None, None, None
 
 
 # measured: permuting P / dS once (2 x 9 us) beats gathering them through perm
@@ -133,74 +171,119 @@ class AgnnAggregate(torch.autograd.Function):
     """Y = spmm(A, P; Z), P = rowsoftmax(sddmm(Z, Z))."""
 
     @staticmethod
-    def forward(ctx, z, t: TiledGraph, mode: str, shard: ShardPlan | None):
+    def forward(ctx, z, t: TiledGraph, mode: str):
         z = z.contiguous()
         m = t.num_edges
         p = torch.empty(max(m, 1), dtype=torch.float32, device=z.device)
-        out, r0, wr = _rows_out(t, z.shape[1], z, shard)
+        out = _rows_out(t, z.shape[1], z)
         p_t = None
-        if mode == "tf32" and shard is None and m and _FUSED_PT:
+        if mode == "tf32" and m and _FUSED_PT:
             # P also written in A^T edge order by the same epilogue (no permute pass)
             p_t = torch.empty(m, dtype=torch.float32, device=z.device)
             agnn_forward_device(t, z, p=p, out=out, p_t=p_t, inv_perm=_inv_perm(t))
         elif mode == "tf32":
-            agnn_forward_device(t, z, p=p, out=out, win_range=wr, y_row0=r0)
+            agnn_forward_device(t, z, p=p, out=out)
         else:
             if m:
-                sddmm_device(t, z, mode=mode, epilogue=_lib.EPI_SOFTMAX, out=p, win_range=wr)
-            spmm_device(t, z, p if m else None, mode=mode, out=out, win_range=wr, y_row0=r0)
-        if shard is not None and m:
-            e0, e1 = shard.my_edges
-            loc = torch.zeros(shard.edges_max, dtype=torch.float32, device=z.device)
-            loc[: e1 - e0] = p[e0:e1]
-            p = allgather_edges(loc, shard)
-        y = _finish_rows(out, shard)
-        ctx.save_for_backward(z, p, y if mode == "tf32" else None, p_t)
-        ctx.t, ctx.mode, ctx.shard = t, mode, shard
-        return y
+                sddmm_device(t, z, mode=mode, epilogue=_lib.EPI_SOFTMAX, out=p)
+            spmm_device(t, z, p if m else None, mode=mode, out=out)
+        ctx.save_for_backward(z, p, out if mode == "tf32" else None, p_t)
+        ctx.t, ctx.mode = t, mode
+        return out
 
     @staticmethod
     def backward(ctx, g):
         z, p, y_fwd, p_t = ctx.saved_tensors
-        t, mode, shard = ctx.t, ctx.mode, ctx.shard
+        t, mode = ctx.t, ctx.mode
         g = g.contiguous()
         m = t.num_edges
-        out, r0, wr = _rows_out(t, z.shape[1], z, shard)
+        out = _rows_out(t, z.shape[1], z)
         if m == 0:
             out.zero_()
-            return _finish_rows(out, shard), None, None, None
+            return out, None, None
         ds = torch.empty(m, dtype=torch.float32, device=z.device)
         ds_t = torch.empty(m, dtype=torch.float32, device=z.device) if p_t is not None else None
         if mode == "tf32":
             # dS and A_dS Z from one gather of Z's neighbour rows (dS also in A^T order)
-            agnn_backward_device(t, z, g, p, ds=ds, out=out, win_range=wr, y_row0=r0,
-                                 y_fwd=y_fwd, ds_t=ds_t,
+            agnn_backward_device(t, z, g, p, ds=ds, out=out, y_fwd=y_fwd, ds_t=ds_t,
                                  inv_perm=_inv_perm(t) if ds_t is not None else None)
         else:
-            sddmm_device(t, g, z, mode=mode, epilogue=_lib.EPI_SOFTMAX_BWD, aux=p, out=ds,
-                         win_range=wr)
-        if shard is not None:
-            e0, e1 = shard.my_edges
-            loc = torch.zeros(shard.edges_max, dtype=torch.float32, device=z.device)
-            loc[: e1 - e0] = ds[e0:e1]
-            ds = allgather_edges(loc, shard)
-        if mode != "tf32":
-            spmm_device(t, z, ds, mode=mode, out=out, win_range=wr, y_row0=r0)
+            sddmm_device(t, g, z, mode=mode, epilogue=_lib.EPI_SOFTMAX_BWD, aux=p, out=ds)
+            spmm_device(t, z, ds, mode=mode, out=out)
         tt = t.transpose()
-        # one dual SpMM on A^T reading P and dS through the edge permutation
-        # (A^T edge k = A edge perm[k]; gathered a window ahead in the kernel)
+        # one dual SpMM on A^T: A^T_P G + A^T_dS Z
         if p_t is not None:
-            spmm_device(tt.tiled, g, p_t, x2=z, weights2=ds_t, mode=mode, out=out,
-                        accumulate=True, win_range=wr, y_row0=r0)
+            spmm_device(tt.tiled, g, p_t, x2=z, weights2=ds_t, mode=mode, out=out, accumulate=True)
         elif mode == "tf32" and not _PERMUTE_WEIGHTS:
-            spmm_device(tt.tiled, g, p, weight_idx=tt.perm, x2=z, weights2=ds,
-                        weight_idx2=tt.perm, mode=mode, out=out, accumulate=True, win_range=wr,
-                        y_row0=r0)
+            spmm_device(tt.tiled, g, p, weight_idx=tt.perm, x2=z, weights2=ds, weight_idx2=tt.perm,
+                        mode=mode, out=out, accumulate=True)
         else:
             pt, dst = permute2_device(p, ds, tt.perm)
-            spmm_device(tt.tiled, g, pt, x2=z, weights2=dst, mode=mode, out=out,
-                        accumulate=True, win_range=wr, y_row0=r0)
-        return _finish_rows(out, shard), None, None, None
+            spmm_device(tt.tiled, g, pt, x2=z, weights2=dst, mode=mode, out=out, accumulate=True)
+        return out, None, None
+
+
+class AgnnAggShard(torch.autograd.Function):
+    """Sharded AGNN aggregation of this rank's rows.
+
+    Forward: Z's rows all-gathered in place; the fused kernel runs on the
+    rank's windows, writing Y's rows into a persistent row buffer (the
+    backward reads them at absolute row ids) and P of the rank's edges into
+    its slice of the layer's padded edge buffer.
+    Backward: G's rows all-gathered; the A-side kernel writes dS of the rank's
+    edges and dZ_r = A_dS Z; one in-place all-gather exchanges [P | dS] of all
+    ranks; both are permuted into A^T edge order for the rank's own A^T edges
+    only (perm_pad) and one dual SpMM on its A^T windows adds
+    A^T_P G + A^T_dS Z."""
+
+    @staticmethod
+    def forward(ctx, z_local, sh: Shard, key, mode: str):
+        d = z_local.shape[1]
+        zbuf, zf, zmine = sh.rows_buffer(("z", key), d)
+        zmine.copy_(z_local)
+        allgather_rows(zbuf, sh.plan, sh.group)
+        _, yf, ymine = sh.rows_buffer(("y", key), d)
+        ebuf, pv, dsv = sh.edge_buffer(key)
+        wr = sh.plan.my_windows
+        if mode == "tf32":
+            agnn_forward_device(sh.t, zf, p=pv, out=yf, win_range=wr, y_row0=0)
+        else:
+            sddmm_device(sh.t, zf, mode=mode, epilogue=_lib.EPI_SOFTMAX, out=pv, win_range=wr)
+            spmm_device(sh.t, zf, pv, mode=mode, out=yf, win_range=wr, y_row0=0)
+        ctx.sh, ctx.key, ctx.mode = sh, key, mode
+        return ymine.clone()
+
+    @staticmethod
+    def backward(ctx, g):
+        sh, key, mode = ctx.sh, ctx.key, ctx.mode
+        d = g.shape[1]
+        _, zf, _ = sh.rows_buffer(("z", key), d)
+        _, yf, _ = sh.rows_buffer(("y", key), d)
+        gbuf, gf, gmine = sh.rows_buffer("grad", d)
+        gmine.copy_(g)
+        allgather_rows(gbuf, sh.plan, sh.group)
+        ebuf, pv, dsv = sh.edge_buffer(key)
+        wr = sh.plan.my_windows
+        r0, r1 = sh.plan.my_rows
+        out = rows_empty(r1 - r0, d, g.device)
+        if mode == "tf32":
+            agnn_backward_device(sh.t, zf, gf, pv, ds=dsv, out=out, win_range=wr, y_row0=r0,
+                                 y_fwd=yf)
+        else:
+            sddmm_device(sh.t, gf, zf, mode=mode, epilogue=_lib.EPI_SOFTMAX_BWD, aux=pv, out=dsv,
+                         win_range=wr)
+            spmm_device(sh.t, zf, dsv, mode=mode, out=out, win_range=wr, y_row0=r0)
+        allgather_edges(ebuf, sh.plan, sh.group)
+        pt, dst = sh.at_buffers()
+        kb, ke = sh.t_edges
+        if ke > kb:
+            _lib.check(_lib.load().tcg_permute2_f32(
+                ebuf.data_ptr(), ebuf.data_ptr() + 4 * sh.plan.edges_max,
+                sh.perm_pad.data_ptr() + 4 * kb, pt.data_ptr() + 4 * kb, dst.data_ptr() + 4 * kb,
+                ke - kb, _lib.current_stream()), "tcg_permute2_f32")
+        spmm_device(sh.tt, gf, pt, x2=zf, weights2=dst, mode=mode, out=out, accumulate=True,
+                    win_range=wr, y_row0=r0)
+        return out, None, None, None
 
 
 def _glorot(fan_in, fan_out, gen=None):
@@ -229,12 +312,18 @@ class GCNConv(nn.Module):
         self.aggregate_first = (order == "aggregate_first"
                                 or (order == "auto" and in_dim < out_dim))
 
-    def forward(self, x, t: TiledGraph, shard: ShardPlan | None = None):
+    def forward(self, x, t: TiledGraph, shard: Shard | None = None, key=None):
+        if shard is not None:  # x: this rank's rows
+            if self.aggregate_first:
+                h = GcnAggShard.apply(x, None, shard, key, self.mode)
+                return DenseFn.apply(h, self.weight, self.bias, False)
+            h = DenseFn.apply(x, self.weight, None, False)
+            return GcnAggShard.apply(h, self.bias, shard, key, self.mode)
         if self.aggregate_first:
-            h = GcnAggregate.apply(x, None, t, self.mode, shard)
+            h = GcnAggregate.apply(x, None, t, self.mode)
             return DenseFn.apply(h, self.weight, self.bias, False)
         h = DenseFn.apply(x, self.weight, None, False)
-        return GcnAggregate.apply(h, self.bias, t, self.mode, shard)
+        return GcnAggregate.apply(h, self.bias, t, self.mode)
 
 
 class AGNNConv(nn.Module):
@@ -245,8 +334,11 @@ class AGNNConv(nn.Module):
         self.weight = nn.Parameter(_glorot(in_dim, out_dim, gen))
         self.mode = mode
 
-    def forward(self, x, t: TiledGraph, shard: ShardPlan | None = None):
-        return AgnnAggregate.apply(DenseFn.apply(x, self.weight, None, False), t, self.mode, shard)
+    def forward(self, x, t: TiledGraph, shard: Shard | None = None, key=None):
+        z = DenseFn.apply(x, self.weight, None, False)
+        if shard is not None:  # x: this rank's rows
+            return AgnnAggShard.apply(z, shard, key, self.mode)
+        return AgnnAggregate.apply(z, t, self.mode)
 
 
 class GCN(nn.Module):
@@ -260,7 +352,11 @@ class GCN(nn.Module):
         self.c2 = GCNConv(hidden, classes, mode, gen)
 
     def forward(self, x, t, shard=None):
-        return self.c2(F.relu(self.c1(x, t, shard)), t, shard)
+        """Logits of all rows, or with a Shard of this rank's rows (x: all rows)."""
+        if shard is not None:
+            r0, r1 = shard.plan.my_rows
+            x = x[r0:r1]
+        return self.c2(F.relu(self.c1(x, t, shard, 1)), t, shard, 2)
 
 
 class AGNN(nn.Module):
@@ -275,7 +371,20 @@ class AGNN(nn.Module):
         self.lin_out = Linear(hidden, classes, bias=True, gen=gen)
 
     def forward(self, x, t, shard=None):
+        """Logits of all rows, or with a Shard of this rank's rows (x: all rows)."""
+        if shard is not None:
+            r0, r1 = shard.plan.my_rows
+            x = x[r0:r1]
         h = self.lin_in(x)
-        for c in self.convs:
-            h = c(h, t, shard)
+        for i, c in enumerate(self.convs):
+            h = c(h, t, shard, i)
         return self.lin_out(h)
+
+
+def cross_entropy_sharded(logits_local, labels, shard: Shard):
+    """This rank's share of the mean cross-entropy over all N rows: the mean
+    over its rows scaled by n_r / N, so that the sum over ranks is the loss
+    and each rank's dlogits are exactly its rows of the full gradient."""
+    r0, r1 = shard.plan.my_rows
+    n = shard.plan.num_nodes
+    return SoftmaxXentFn.apply(logits_local, labels[r0:r1]) * ((r1 - r0) / n)

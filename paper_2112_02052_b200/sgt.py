@@ -226,17 +226,18 @@ class TiledGraph:
         whether the fused AGNN kernels can keep a whole window on chip."""
         mx = self._aux.get("maxima")
         if mx is None:
-            if self.num_row_windows == 0:
+            wb, we = getattr(self, "shard_windows", (0, self.num_row_windows))
+            if we <= wb:
                 mx = (0, 0)
             else:
                 ptr = self.dev["node_ptr"]
                 bh = self.config.blk_h
-                idx = np.minimum(np.arange(self.num_row_windows + 1) * bh, self.num_nodes)
+                idx = np.minimum(np.arange(wb, we + 1) * bh, self.num_nodes)
                 import torch
 
                 eb = ptr[torch.from_numpy(idx).to(ptr.device)]
                 me = int((eb[1:] - eb[:-1]).max().item())
-                co = self.dev["col_offsets"]
+                co = self.dev["col_offsets"][wb: we + 1]
                 mu = int((co[1:] - co[:-1]).max().item())
                 mx = (me, mu)
             self._aux["maxima"] = mx
@@ -383,13 +384,24 @@ def translate(g: CsrGraph, cfg: BlockConfig, device=None) -> TiledGraph:
     return _sgt_device(ptr, cols, g.num_nodes, g.num_edges, cfg, g)
 
 
+def csr_transpose_device(g: CsrGraph, device=None):
+    """(A^T as a device-resident CsrGraph, perm): A^T edge k is A edge perm[k]
+    (tcg_csr_transpose; the backward's graph)."""
+    ptr, cols, _ = g.device_arrays(device)
+    return _csr_transpose(ptr, cols, g.num_nodes, g.num_edges, g)
+
+
 def _transpose(t: TiledGraph) -> TransposedTiling:
+    g = t._require_graph()
+    gt, perm = _csr_transpose(t.dev["node_ptr"], t.dev["edge_list"], t.num_nodes, t.num_edges, g)
+    tt = _sgt_device(gt._ptr_d, gt._cols_d, t.num_nodes, t.num_edges, t.config, gt)
+    return TransposedTiling(tt, perm)
+
+
+def _csr_transpose(ptr, cols, n: int, m: int, g):
     import torch
 
     lib = _lib.load()
-    g = t._require_graph()
-    n, m = t.num_nodes, t.num_edges
-    ptr, cols = t.dev["node_ptr"], t.dev["edge_list"]
     dev = ptr.device
     ptr_t = torch.empty(n + 1, dtype=torch.int64, device=dev)
     cols_t = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
@@ -400,9 +412,7 @@ def _transpose(t: TiledGraph) -> TransposedTiling:
                                      ptr_t.data_ptr(), cols_t.data_ptr(), perm.data_ptr(),
                                      ws.data_ptr(), wsb, _stream_ptr()), "tcg_csr_transpose")
     cols_t, perm = cols_t[:m], perm[:m]
-    gt = _DeviceCsr(n, ptr_t, cols_t, g)
-    tt = _sgt_device(ptr_t, cols_t, n, m, t.config, gt)
-    return TransposedTiling(tt, perm)
+    return _DeviceCsr(n, ptr_t, cols_t, g), perm
 
 
 class _DeviceCsr(CsrGraph):

@@ -44,14 +44,15 @@ def _worker(rank, world, port, q):
         full_p = o.segment_softmax(o.sddmm(ptr, cols, x), ptr)
         r0, r1 = plan.my_rows
         e0, e1 = plan.my_edges
-        # rank-local computation: only this rank's rows / edges
-        y_local = full_y[r0:r1]
-        slab = torch.zeros(plan.rows_max, 8)
-        slab[: r1 - r0] = torch.from_numpy(y_local)
-        got = tdist.allgather_rows(slab, plan).numpy()
-        vec = torch.zeros(plan.edges_max)
-        vec[: e1 - e0] = torch.from_numpy(full_p[e0:e1])
-        got_p = tdist.allgather_edges(vec, plan).numpy()
+        # rank-local computation: only this rank's rows / edges, written into its
+        # slice of the persistent padded buffers; the all-gathers run in place
+        buf = torch.zeros(plan.padded_rows, 8)
+        buf[r0:r1] = torch.from_numpy(full_y[r0:r1])
+        got = tdist.allgather_rows(buf, plan)[:n].numpy()
+        ebuf = torch.zeros(world * 2 * plan.edges_max)
+        ebuf[torch.from_numpy(plan.edge_slot(np.arange(e0, e1)))] = torch.from_numpy(full_p[e0:e1])
+        tdist.allgather_edges(ebuf, plan)
+        got_p = ebuf[torch.from_numpy(plan.edge_slot(np.arange(cols.shape[0])))].numpy()
         ok = np.array_equal(got, full_y) and np.array_equal(got_p, full_p)
         # windows cover [0, W) once, rows/edges contiguous
         W = -(-n // 16)
@@ -105,3 +106,25 @@ def test_shard_plan_rows_edges(world):
     assert all(rows[i][1] == rows[i + 1][0] for i in range(world - 1))
     edges = plans[0].edges
     assert edges[0][0] == 0 and edges[-1][1] == cols.shape[0]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_uniform_plan_layout(world):
+    """Equal row ranges (multiples of blk_h) so every exchange is one in-place
+    all_gather_into_tensor; every rank's padded edge slice starts at or after
+    its first edge id (the kernels write P / dS at absolute edge ids through a
+    non-negative pointer offset); edge slots are a bijection into the layout."""
+    from oracle import tcg_oracle as o
+    from paper_2112_02052_b200.dist import make_shard_plan
+
+    n = 1237
+    ptr, cols, _ = o.gen_uniform(n, 6, seed=2)
+    wp, _, _, _ = o.translate(ptr, cols, n, 16, 8)
+    for r in range(world):
+        p = make_shard_plan(ptr, n, 16, wp, None, r, world)
+        assert p.R % 16 == 0 and p.padded_rows >= n and p.imbalance >= 1.0
+        assert all(r1 - r0 <= p.R for r0, r1 in p.rows)
+        assert all(q * 2 * p.edges_max >= e0 for q, (e0, _) in enumerate(p.edges))
+        assert all(a[0] * 16 == min(r0, n) or r0 == n for a, (r0, _) in zip(p.windows, p.rows))
+    slots = p.edge_slot(np.arange(cols.shape[0]))
+    assert np.unique(slots).shape[0] == cols.shape[0] and slots.max() < world * 2 * p.edges_max

@@ -47,7 +47,7 @@ def test_agnn_backward_vs_oracle(env, oracle, mode, tol):
     z = rng.standard_normal((3000, 32)).astype(np.float32)
     gy = rng.standard_normal((3000, 32)).astype(np.float32)
     zt = torch.from_numpy(z).cuda().requires_grad_(True)
-    y = layers.AgnnAggregate.apply(zt, t, mode, None)
+    y = layers.AgnnAggregate.apply(zt, t, mode)
     y.backward(torch.from_numpy(gy).cuda())
     ptr, cols = g.node_pointer, g.edge_list
     p = oracle.segment_softmax(oracle.sddmm(ptr, cols, z), ptr)
@@ -70,7 +70,7 @@ def test_gcn_backward_vs_oracle(env, oracle, weighted):
     gy = rng.standard_normal((2000, 16)).astype(np.float32)
     ht = torch.from_numpy(h).cuda().requires_grad_(True)
     bt = torch.from_numpy(b).cuda().requires_grad_(True)
-    y = layers.GcnAggregate.apply(ht, bt, t, "f32", None)
+    y = layers.GcnAggregate.apply(ht, bt, t, "f32")
     y.backward(torch.from_numpy(gy).cuda())
     ptr, cols = g.node_pointer, g.edge_list
     assert np.array_equal(y.detach().cpu().numpy(),

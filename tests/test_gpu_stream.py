@@ -167,7 +167,7 @@ def test_stream_agnn_forward_backward(env, oracle, kind):
     assert rel_l2(ds.cpu().numpy()[: g.num_edges], ds_ref) <= TF32_REL_L2
     assert rel_l2(dz_a.cpu().numpy(), oracle.spmm(ptr, cols, z, f=ds_ref)) <= TF32_REL_L2
     zt.requires_grad_(True)
-    out = layers.AgnnAggregate.apply(zt, t, "tf32", None)
+    out = layers.AgnnAggregate.apply(zt, t, "tf32")
     out.backward(gyt)
     dz_ref = oracle.agnn_backward(ptr, cols, z, p_ref, gy)
     assert rel_l2(zt.grad.cpu().numpy(), dz_ref) <= TF32_REL_L2
