@@ -285,7 +285,8 @@ def run_ours(args):
 
     import paper_2112_02052_b200 as tcg
     from paper_2112_02052_b200 import _lib, dist as tdist, layers
-    from paper_2112_02052_b200.kernels import sddmm_device, spmm_device
+    from paper_2112_02052_b200.kernels import (agnn_backward_device, agnn_forward_device,
+                                               permute2_device, sddmm_device, spmm_device)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -649,6 +650,37 @@ def run_ours(args):
                                         * d / (t_spmm * 1e-3) / 1e9, 1),
             "gather_bytes_4UD": 4 * u * d,
         }
+        if world == 1 and model_kind == "agnn":
+            # the epoch's other dominant kernels, each cold and alone, against the
+            # same HBM peak (algorithmic bytes: every array read / written once)
+            tt = t.transpose()
+            ut = tt.tiled.num_unique
+            meta = 4 * u + 8 * (n + 1) + 8 * (W + 1) + 4 * W
+            meta_t = 4 * ut + 8 * (n + 1) + 8 * (W + 1) + 4 * W
+            pz = torch.empty(m, device=dev)
+            yf = torch.empty(n, d, device=dev)
+            gy = torch.randn(n, d, device=dev)
+            ds = torch.empty(m, device=dev)
+            dz = torch.empty(n, d, device=dev)
+            agnn_forward_device(t, z, p=pz, out=yf)
+            pt, dst = permute2_device(pz, pz, tt.perm)
+            kern = {
+                # S = <Z_i, Z_j>, online softmax, P written, Y = A_P Z: Z, Y, P, e2c
+                "agnn_fwd": (lambda: agnn_forward_device(t, z, p=pz, out=yf),
+                             8 * n * d + 8 * m + meta),
+                # one-pass A-side backward: Z, G, Y_fwd read, dZ written; P read, dS written, e2c
+                "agnn_bwd": (lambda: agnn_backward_device(t, z, gy, pz, ds=ds, out=dz, y_fwd=yf),
+                             16 * n * d + 12 * m + meta),
+                # dual A^T SpMM: G, Z read, dZ read + written; P^T, dS^T, e2c(A^T)
+                "dual_at_spmm": (lambda: spmm_device(tt.tiled, gy, pt, x2=z, weights2=dst, out=dz,
+                                                     accumulate=True),
+                                 16 * n * d + 12 * m + meta_t),
+            }
+            extras["kernels"] = {}
+            for name, (fn, b) in kern.items():
+                us = kernel_ms(fn, reps=30) * 1e3
+                extras["kernels"][name] = {"us_cold": round(us, 2), "algorithmic_bytes": b,
+                                           "frac": round(b / (us * 1e-6) / 1e9 / peak, 4)}
         if model_kind == "agnn" and world == 1:
             # the GCN-2 epoch on the same graph (second half of the metric)
             gnet = layers.GCN(feats, 16, classes, mode="tf32").to(dev)

@@ -483,7 +483,12 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32, 1) spmm_stream(c
 #pragma unroll
           for (int j = 0; j < NT; ++j) mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
         }
-        // refill: X of block s + NB into this slot, ids of block s + 2NB
+        // refill: X of block s + NB into this slot, ids of block s + 2NB. The
+        // 16-wide path's lanes read slices copied by other lanes: all reads of
+        // this slot must be done before any lane re-fills it (racecheck)
+        if constexpr (NT == 2) {
+          if (a.x16) __syncwarp();
+        }
         issue_x(xo, io);
         if (lane < 2) cp_async<16>(is + iw, cnext);
         cp_commit();
