@@ -63,6 +63,11 @@ typedef struct tcg_tiling {
   const uint32_t* col_stream;   /* u32[8*(TB+TCG_STREAM_PAD)], TB = block_offsets[W]:
                                    col_to_node padded per window to whole
                                    8-column blocks, pair-interleaved          */
+  /* Pair stream (tcg_block_stream_pairs; optional): the same with every
+   * window padded to an even block count, for the 16-wide SpMM that consumes
+   * two blocks per step. */
+  const int32_t* pair_offsets;  /* i32[W+1] exclusive cumsum of win_partition rounded up to even */
+  const uint32_t* pair_stream;  /* u32[8*(TP+TCG_STREAM_PAD)], TP = pair_offsets[W] */
 } tcg_tiling;
 
 /* Blocks of padding tcg_block_stream appends after the column stream. */
@@ -172,6 +177,11 @@ int tcg_edge_frag(const tcg_tiling* t, uint32_t* edge_frag, void* stream);
  * 8*(TB+TCG_STREAM_PAD) u32). Derived once per tiling. */
 int tcg_block_stream(const tcg_tiling* t, int32_t* block_offsets, uint32_t* col_stream,
                      void* stream);
+/* The pair stream of the 16-wide SpMM (tcg_tiling.pair_offsets / pair_stream):
+ * as tcg_block_stream with win_partition rounded up to even per window (the
+ * padding block repeats the window's first node; its A tile is zero). */
+int tcg_block_stream_pairs(const tcg_tiling* t, int32_t* pair_offsets, uint32_t* pair_stream,
+                           void* stream);
 /* dst[k] = src[idx[k]] — carries A's edge weights (P, dS, edge values) into
  * A^T edge order once per backward, so the A^T SpMM reads them coalesced. */
 int tcg_permute_f32(const float* src, const uint32_t* idx, float* dst, int64_t n, void* stream);

@@ -43,6 +43,8 @@ class TcgTiling(C.Structure):
         ("max_window_unique", C.c_int64),
         ("block_offsets", C.c_void_p),
         ("col_stream", C.c_void_p),
+        ("pair_offsets", C.c_void_p),
+        ("pair_stream", C.c_void_p),
     ]
 
 
@@ -71,6 +73,7 @@ SIGNATURES = {
     "tcg_edge_frag": (C.c_int, [C.POINTER(TcgTiling), _P, _P]),
     "tcg_edge_to_row": (C.c_int, [_P, _I64, _I32, _P, _P]),
     "tcg_block_stream": (C.c_int, [C.POINTER(TcgTiling), _P, _P, _P]),
+    "tcg_block_stream_pairs": (C.c_int, [C.POINTER(TcgTiling), _P, _P, _P]),
     "tcg_permute_f32": (C.c_int, [_P, _P, _P, _I64, _P]),
     "tcg_permute2_f32": (C.c_int, [_P, _P, _P, _P, _P, _I64, _P]),
     "tcg_csr_transpose_workspace_bytes": (_SZ, [_I64, _I64]),

@@ -133,9 +133,15 @@ constexpr int kEPL = 5;    // edges per lane prefetched for the next window (160
 // at arxiv D = 32 (cold, clean L2): NB 8 / MB 8 / 4 warps 35.7 us, NB 8 / MB 16
 // / 4 warps 35.9 us, NB 4 / MB 8 / 4 warps 34.9 us, against 33.8 us for this
 // shape: more bytes in flight do not help, the ring is not what bounds it.
-template <int NT, bool DUAL, bool BIG = false>
+// PAIR (16-wide chunks): every step consumes two consecutive 8-column blocks of
+// the window-even-padded pair stream (tcg_block_stream_pairs), so the per-step
+// costs (ring wait, id copies, cursor updates, loop) are paid once per 1 KB of
+// staged rows, as at 32-wide chunks.
+template <int NT, bool DUAL, bool BIG = false, bool PAIR = false>
 struct Cfg {
-  static constexpr int NB = 4;  // ring depth (blocks)
+  static constexpr int KB = PAIR ? 2 : 1;  // blocks per step
+  // ring depth in steps: 4 blocks of 32-wide rows in flight either way
+  static constexpr int NB = (PAIR && NT == 4) ? 2 : 4;
   // column-id ring: ids of block s + NI are requested at step s (NI >= 2 NB so
   // the ids of block s + NB have landed by then); power of two
   static constexpr int NI = 2 * NB;
@@ -143,8 +149,9 @@ struct Cfg {
   static constexpr int SLOT = 8 * 32 * NT;         // bytes of one operand's block
   static constexpr int OPS = DUAL ? 2 : 1;
   static constexpr int MB = (DUAL || BIG) ? 8 : 16;  // A-fragment blocks resident (one round)
-  static constexpr int RING = NB * SLOT * OPS;
-  static constexpr int IDX = NI * 32;              // column-id pairs of NI blocks
+  static constexpr int STEP = SLOT * OPS * KB;     // staged bytes of one step
+  static constexpr int RING = NB * STEP;
+  static constexpr int IDX = NI * 32 * KB;         // column ids of NI steps
   static constexpr int AFR = MB * 512 * OPS;
   // BIG: windows with more edges than the register prefetch holds (products:
   // ~400) stage the next window's edge slots and weights in shared memory
@@ -174,10 +181,11 @@ __device__ __forceinline__ int warp_lower_bound(const int32_t* __restrict__ a, i
   return lo + __popc(__ballot_sync(0xffffffffu, pr));
 }
 
-template <int NT, bool DUAL, bool BIG, bool MASK>
-__global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32, 1) spmm_stream(const Args a) {
-  using C = Cfg<NT, DUAL, BIG>;
-  constexpr int NB = C::NB, NI = C::NI, SLOT = C::SLOT, MB = C::MB;
+template <int NT, bool DUAL, bool BIG, bool MASK, bool PAIR = false>
+__global__ void __launch_bounds__(Cfg<NT, DUAL, BIG, PAIR>::WPC * 32, 1) spmm_stream(const Args a) {
+  using C = Cfg<NT, DUAL, BIG, PAIR>;
+  constexpr int NB = C::NB, NI = C::NI, SLOT = C::SLOT, MB = C::MB, KB = C::KB;
+  static_assert(!PAIR || (NT >= 2 && !DUAL && MB % 2 == 0), "pair steps: 16/32-wide, one operand");
   constexpr uint32_t RS = MB * 128;  // fragment slots of one round
   constexpr int CP = 4 * NT;  // bytes per lane per staged row
   extern __shared__ __align__(128) unsigned char smem[];
@@ -228,7 +236,21 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32, 1) spmm_stream(c
   const int q_vb = MASK ? max(0, min(16, (a.dv - 4 * qk) * 4)) : 16;
   const char* q_x = reinterpret_cast<const char*>(a.x + d0) + 16 * qk;
   const char* q_x2 = DUAL ? reinterpret_cast<const char*>(a.x2 + d0) + 16 * qk : nullptr;
-  auto issue_x = [&](uint32_t xo, uint32_t io) {
+  auto issue_block = [&](uint32_t xo, uint32_t io) {
+    if constexpr (PAIR && NT == 2) {  // x16 layout, both blocks of the step
+      const uint32_t id0 = *reinterpret_cast<const uint32_t*>(iring_p + io + q_id);
+      const uint32_t id1 = *reinterpret_cast<const uint32_t*>(iring_p + io + 32 + q_id);
+      const uint32_t d = ring + xo + q_dst;
+      if constexpr (masked) {
+        cp_async_n<16>(d, q_vb ? (const void*)(q_x + (uint64_t)id0 * xrow) : (const void*)a.x, q_vb);
+        cp_async_n<16>(d + SLOT, q_vb ? (const void*)(q_x + (uint64_t)id1 * xrow) : (const void*)a.x,
+                       q_vb);
+      } else {
+        cp_async<16>(d, q_x + (uint64_t)id0 * xrow);
+        cp_async<16>(d + SLOT, q_x + (uint64_t)id1 * xrow);
+      }
+      return;
+    }
     if (NT == 2 && a.x16) {
       const uint32_t id = *reinterpret_cast<const uint32_t*>(iring_p + io + q_id);
       const uint32_t d = ring + xo + q_dst;
@@ -264,19 +286,28 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32, 1) spmm_stream(c
       cp_async<CP>(xs + xo + SLOT + d1, xb2 + (uint64_t)id.y * xrow2);
     }
   };
-  if (lane < 2)
-    for (int s = 0; s < NI - NB; ++s) cp_async<16>(is + s * 32, csl + 32 * s);
+  auto issue_x = [&](uint32_t xo, uint32_t io) {
+    if constexpr (PAIR && NT == 4) {
+      issue_block(xo, io);
+      issue_block(xo + SLOT, io + 32);
+    } else {
+      issue_block(xo, io);
+    }
+  };
+  constexpr int IS = 32 * KB;  // id bytes per step (lanes 0 .. 2KB-1 copy 16 B each)
+  if (lane < 2 * KB)
+    for (int s = 0; s < NI - NB; ++s) cp_async<16>(is + s * IS, csl + IS * s);
   cp_commit();
   cp_wait<0>();
   __syncwarp();
   for (int s = 0; s < NB; ++s) {
-    issue_x(s * SLOT * C::OPS, s * 32);
-    if (lane < 2) cp_async<16>(is + (s + NI - NB) * 32, csl + 32 * (s + NI - NB));
+    issue_x(s * C::STEP, s * IS);
+    if (lane < 2 * KB) cp_async<16>(is + (s + NI - NB) * IS, csl + IS * (s + NI - NB));
     cp_commit();
   }
-  // ring cursors of the consumed block s: X slot, id slot of s + NB, id slot of s + NI
-  uint32_t xo = 0, io = NB * 32, iw = 0;
-  const char* cnext = csl + 32 * NI;
+  // ring cursors of the consumed step s: X slot, id slot of s + NB, id slot of s + NI
+  uint32_t xo = 0, io = NB * IS, iw = 0;
+  const char* cnext = csl + IS * NI;
 
   // ---- window metadata, rolled 3 windows ahead ----
   auto ptr_of = [&](int w) { return (int64_t)__ldg(a.ptr + min((int64_t)w * 16, a.n)); };
@@ -464,14 +495,15 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32, 1) spmm_stream(c
       }
       const int rend = min(nbw, r0 + MB);
       uint32_t fa = as;
-      for (int lb = r0; lb < rend; ++lb, fa += 512) {
+      for (int lb = r0; lb < rend; lb += KB, fa += 512 * KB) {
         cp_wait<NB - 1>();
         __syncwarp();  // ids copied by lanes 0-1 visible to the warp
-        {
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
           float x0[NT], x1[NT];
-          lds_slice<NT>(x0, xs + xo);
-          lds_slice<NT>(x1, xs + xo + d1);
-          const uint4 af = lds_frag(fa);
+          lds_slice<NT>(x0, xs + xo + kb * SLOT);
+          lds_slice<NT>(x1, xs + xo + kb * SLOT + d1);
+          const uint4 af = lds_frag(fa + kb * 512);
 #pragma unroll
           for (int j = 0; j < NT; ++j) mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
         }
@@ -490,12 +522,12 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG>::WPC * 32, 1) spmm_stream(c
           if (a.x16) __syncwarp();
         }
         issue_x(xo, io);
-        if (lane < 2) cp_async<16>(is + iw, cnext);
+        if (lane < 2 * KB) cp_async<16>(is + iw, cnext);
         cp_commit();
-        cnext += 32;
-        xo = (xo + SLOT * C::OPS) & (NB * SLOT * C::OPS - 1);
-        io = (io + 32) & (NI * 32 - 1);
-        iw = (iw + 32) & (NI * 32 - 1);
+        cnext += IS;
+        xo = (xo + C::STEP) & (NB * C::STEP - 1);
+        io = (io + IS) & (NI * IS - 1);
+        iw = (iw + IS) & (NI * IS - 1);
       }
     }
     store(w);
@@ -910,7 +942,7 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
   const int gb0 = __ldg(a.boff + ws);
 
   const char* xb = reinterpret_cast<const char*>(a.z + g * 4);
-  const uint64_t xrow = (uint64_t)a.ldz * 4;
+  const uint32_t xrow = (uint32_t)a.ldz * 4u;  // 32 x 32 -> 64-bit IMAD.WIDE per address
   const uint32_t so0 = agnn_off(t, g), so1 = agnn_off(t + 4, g);             // SpMM reads/writes
   const int pr = (g >> 1) + 4 * (g & 1);                                      // SDDMM row
   const uint32_t sd0 = agnn_off(pr, t), sd1 = agnn_off(pr, t + 4);
@@ -921,8 +953,8 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
   auto issue_x = [&](int s) {
     const uint2 id = *reinterpret_cast<const uint2*>(iring_p + (s & (NI - 1)) * 32 + 8 * t);
     const uint32_t sb = ring + (s & (NB - 1)) * 1024;
-    cp_async<16>(sb + so0, xb + id.x * xrow);
-    cp_async<16>(sb + so1, xb + id.y * xrow);
+    cp_async<16>(sb + so0, xb + (uint64_t)id.x * xrow);
+    cp_async<16>(sb + so1, xb + (uint64_t)id.y * xrow);
   };
   for (int s = 0; s < NB; ++s) issue_idx(s);
   cp_commit();
@@ -1037,7 +1069,7 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
         lds_slice<4>(b1, sb + sd1);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          mma_tf32(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], tf32_rn(b0[j]), tf32_rn(b1[j]));
+          mma_tf32_rb(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], b0[j], b1[j]);
       }
       // C (g, 2t) <-> A (g, t); C (g, 2t+1) <-> A (g, t+4): A slots are
       // (0: (g,t), 1: (g+8,t), 2: (g,t+4), 3: (g+8,t+4)); C regs are
@@ -1113,7 +1145,7 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
         lds_slice<4>(x1, sb + so1);
         const uint32_t a0 = tf32_rn(av[0]), a1 = tf32_rn(av[1]), a2 = tf32_rn(av[2]), a3 = tf32_rn(av[3]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) mma_tf32(acc[j], a0, a1, a2, a3, tf32_rn(x0[j]), tf32_rn(x1[j]));
+        for (int j = 0; j < 4; ++j) mma_tf32_rb(acc[j], a0, a1, a2, a3, x0[j], x1[j]);
       }
       __syncwarp();
       issue_x(s + NB);
@@ -1214,14 +1246,15 @@ int launch_agnn(AgnnArgs& a, cudaStream_t s) {
 // ---- tiling preprocessing ---------------------------------------------------
 
 // block_offsets[w] = sum of win_partition[0..w) (single CTA; once per tiling)
-__global__ void block_offsets_kernel(const uint32_t* __restrict__ wp, int64_t W, int32_t* boff) {
+__global__ void block_offsets_kernel(const uint32_t* __restrict__ wp, int64_t W, int32_t* boff,
+                                     int even) {
   __shared__ int scratch[33];
   __shared__ int carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (int64_t base = 0; base < W; base += 1024) {
     const int64_t i = base + threadIdx.x;
-    const int v = i < W ? (int)wp[i] : 0;
+    const int v = i < W ? (even ? (int)((wp[i] + 1) & ~1u) : (int)wp[i]) : 0;
     int total;
     const int ex = block_excl_scan<1024>(v, scratch, &total);
     if (i < W) boff[i] = carry + ex;
@@ -1256,10 +1289,10 @@ __global__ void stream_pad_kernel(const int32_t* __restrict__ boff, int64_t W, u
   for (int q = threadIdx.x; q < 8 * TCG_STREAM_PAD; q += blockDim.x) cs[8 * tb + q] = fill;
 }
 
-template <int NT, bool DUAL, bool BIG, bool MASK>
+template <int NT, bool DUAL, bool BIG, bool MASK, bool PAIR = false>
 int launch_t(Args& a, int nchunks, cudaStream_t s) {
-  using C = Cfg<NT, DUAL, BIG>;
-  auto kern = spmm_stream<NT, DUAL, BIG, MASK>;
+  using C = Cfg<NT, DUAL, BIG, PAIR>;
+  auto kern = spmm_stream<NT, DUAL, BIG, MASK, PAIR>;
   static int configured = -1;
   int dev = 0;
   TCG_CUDA(cudaGetDevice(&dev), "spmm_stream device");
@@ -1324,12 +1357,30 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
     // TMA tile::gather4 engine: opt-in (TCG_SPMM_ENGINE=tma), measured slower
     // than the cp.async ring on B200 (profiles/r02)
     static const char* eng = std::getenv("TCG_SPMM_ENGINE");
+    static const bool pair_off = std::getenv("TCG_NO_PAIRS") != nullptr;  // A/B: one block per step
     const bool use_tma = eng && std::strcmp(eng, "tma") == 0;
     if (use_tma && !dual && !big && !mk && nt == 4) {
       CUtensorMap tm;
       if (stream::make_row_map(&tm, q.x, q.n, q.dim, q.ldx)) {
         return stream::launch_tma<8, 8>(a, tm, nchunks, s);
       }
+    }
+    // 16-wide single-operand chunks: two blocks per step over the pair stream
+    // 32-wide single-operand chunks too (measured 34.8 -> 32.8 us at arxiv D=32, cold)
+    if (nt == 4 && !dual && !big && !mk && t->pair_offsets && t->pair_stream && !pair_off) {
+      stream::Args ap = a;
+      ap.boff = t->pair_offsets;
+      ap.cs = t->pair_stream;
+      return stream::launch_t<4, false, false, false, true>(ap, nchunks, s);
+    }
+    if (nt == 2 && !dual && a.x16 && t->pair_offsets && t->pair_stream && !pair_off) {
+      stream::Args ap = a;
+      ap.boff = t->pair_offsets;
+      ap.cs = t->pair_stream;
+      return big ? (mk ? stream::launch_t<2, false, true, true, true>(ap, nchunks, s)
+                       : stream::launch_t<2, false, true, false, true>(ap, nchunks, s))
+                 : (mk ? stream::launch_t<2, false, false, true, true>(ap, nchunks, s)
+                       : stream::launch_t<2, false, false, false, true>(ap, nchunks, s));
     }
 #define TCG_SL(NTV, MK)                                                                   \
   if (nt == NTV && mk == MK)                                                              \
@@ -1437,8 +1488,8 @@ extern "C" int tcg_invert_perm(const uint32_t* perm, int64_t n, uint32_t* inv, v
   return TCG_OK;
 }
 
-extern "C" int tcg_block_stream(const tcg_tiling* t, int32_t* block_offsets,
-                                uint32_t* col_stream, void* stream) {
+static int block_stream(const tcg_tiling* t, int32_t* block_offsets, uint32_t* col_stream, int even,
+                        void* stream) {
   TCG_REQUIRE(t != nullptr, "tcg_block_stream: null tiling");
   TCG_REQUIRE(t->blk_h == 16 && t->blk_w == 8,
               "tf32 mode requires the 16x8 tile shape, got %dx%d", t->blk_h, t->blk_w);
@@ -1452,7 +1503,7 @@ extern "C" int tcg_block_stream(const tcg_tiling* t, int32_t* block_offsets,
     return TCG_OK;
   }
   TCG_REQUIRE(t->win_partition && t->col_offsets, "tcg_block_stream: tiling arrays missing");
-  stream::block_offsets_kernel<<<1, 1024, 0, s>>>(t->win_partition, W, block_offsets);
+  stream::block_offsets_kernel<<<1, 1024, 0, s>>>(t->win_partition, W, block_offsets, even);
   TCG_LAUNCHED("block_offsets");
   if (col_stream == nullptr) return TCG_OK;  // offsets only (caller sizes the stream)
   if (t->num_unique > 0) {
@@ -1464,4 +1515,14 @@ extern "C" int tcg_block_stream(const tcg_tiling* t, int32_t* block_offsets,
   stream::stream_pad_kernel<<<1, 256, 0, s>>>(block_offsets, W, col_stream, t->col_to_node);
   TCG_LAUNCHED("stream_pad");
   return TCG_OK;
+}
+
+extern "C" int tcg_block_stream(const tcg_tiling* t, int32_t* block_offsets, uint32_t* col_stream,
+                                void* stream) {
+  return block_stream(t, block_offsets, col_stream, 0, stream);
+}
+
+extern "C" int tcg_block_stream_pairs(const tcg_tiling* t, int32_t* pair_offsets, uint32_t* pair_stream,
+                                      void* stream) {
+  return block_stream(t, pair_offsets, pair_stream, 1, stream);
 }

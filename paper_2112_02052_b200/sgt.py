@@ -218,6 +218,18 @@ class TiledGraph:
                 d["col_stream"] = cs
                 s.block_offsets = bo.data_ptr()
                 s.col_stream = cs.data_ptr()
+                # pair stream for the 16-wide SpMM (two blocks per step)
+                po = torch.empty(W + 1, dtype=torch.int32, device=self.device)
+                _lib.check(lib.tcg_block_stream_pairs(C.byref(s), po.data_ptr(), None,
+                                                      _stream_ptr()), "tcg_block_stream_pairs")
+                tp = int(po[W].item())
+                ps = torch.empty(8 * (tp + _lib.STREAM_PAD), dtype=torch.int32, device=self.device)
+                _lib.check(lib.tcg_block_stream_pairs(C.byref(s), po.data_ptr(), ps.data_ptr(),
+                                                      _stream_ptr()), "tcg_block_stream_pairs")
+                d["pair_offsets"] = po
+                d["pair_stream"] = ps
+                s.pair_offsets = po.data_ptr()
+                s.pair_stream = ps.data_ptr()
             self._aux["abi"] = s
         return s
 

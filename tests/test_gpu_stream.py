@@ -63,6 +63,60 @@ def test_block_stream_arrays(env, oracle):
                 want = nodes[c] if c < len(nodes) else nodes[0]
                 assert cs[8 * b + i] == want
     assert cs.size == 8 * (tb + 16)
+    # pair stream (16-wide SpMM, two blocks per step): windows padded to even
+    po = t.dev["pair_offsets"].cpu().numpy()
+    wp = t.win_partition.astype(np.int64)
+    assert np.array_equal(np.diff(po), wp + (wp & 1)) and po[0] == 0
+    ps = t.dev["pair_stream"].cpu().numpy().view(np.uint32)
+    for w in range(t.num_row_windows):
+        nodes = t.window_nodes(w)
+        for b in range(po[w], po[w + 1]):
+            for i in range(8):
+                c = (b - po[w]) * 8 + (i >> 1) + 4 * (i & 1)
+                assert ps[8 * b + i] == (nodes[c] if c < len(nodes) else nodes[0])
+    assert ps.size == 8 * (int(po[-1]) + 16)
+
+
+_PAIR_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import torch
+import paper_2112_02052_b200 as tcg
+from paper_2112_02052_b200.kernels import spmm_device
+out = []
+for n, deg, d, seed in ((3001, 7, 16, 1), (2000, 40, 16, 2), (777, 3, 12, 3), (1500, 9, 48, 4),
+                        (2500, 8, 32, 5), (1200, 11, 64, 6)):
+    g = tcg.synth.gen_uniform(n, deg, seed)
+    t = tcg.translate(g, tcg.BlockConfig())
+    rng = np.random.default_rng(seed)
+    x = torch.from_numpy(rng.standard_normal((n, d)).astype(np.float32)).cuda()
+    w = torch.from_numpy(rng.random(g.num_edges).astype(np.float32)).cuda()
+    out.append(spmm_device(t, x, w, mode="tf32").cpu().numpy())
+np.save(sys.argv[2], np.concatenate([o.ravel() for o in out]))
+"""
+
+
+def test_pair_steps_bitwise_equal_single_block_steps(tmp_path):
+    """The 16-wide two-blocks-per-step path (pair stream) is the same mma
+    sequence per window as the one-block-per-step path (TCG_NO_PAIRS=1): the
+    results are bitwise equal, incl. 40-edge windows (BIG staging), a masked
+    12-wide chunk, a 48-wide operand's 16-wide tail and 32 / 64-wide operands
+    (32-wide pair steps)."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    res = []
+    for k, env in enumerate(({}, {"TCG_NO_PAIRS": "1"})):
+        f = tmp_path / f"o{k}.npy"
+        r = subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, str(ROOT), str(f)],
+                           env=dict(os.environ, **env), capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(np.load(f))
+    assert np.array_equal(res[0], res[1])
 
 
 @pytest.mark.parametrize("dim", [3, 7, 8, 16, 22, 24, 32, 40, 47, 64, 100, 128])
