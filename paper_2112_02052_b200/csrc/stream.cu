@@ -185,7 +185,7 @@ template <int NT, bool DUAL, bool BIG, bool MASK, bool PAIR = false>
 __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG, PAIR>::WPC * 32, 1) spmm_stream(const Args a) {
   using C = Cfg<NT, DUAL, BIG, PAIR>;
   constexpr int NB = C::NB, NI = C::NI, SLOT = C::SLOT, MB = C::MB, KB = C::KB;
-  static_assert(!PAIR || (NT >= 2 && !DUAL && MB % 2 == 0), "pair steps: 16/32-wide, one operand");
+  static_assert(!PAIR || (NT >= 2 && (!DUAL || NT == 4) && MB % 2 == 0), "pair steps: 16/32-wide");
   constexpr uint32_t RS = MB * 128;  // fragment slots of one round
   constexpr int CP = 4 * NT;  // bytes per lane per staged row
   extern __shared__ __align__(128) unsigned char smem[];
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG, PAIR>::WPC * 32, 1) spmm_st
   auto issue_x = [&](uint32_t xo, uint32_t io) {
     if constexpr (PAIR && NT == 4) {
       issue_block(xo, io);
-      issue_block(xo + SLOT, io + 32);
+      issue_block(xo + SLOT * C::OPS, io + 32);
     } else {
       issue_block(xo, io);
     }
@@ -499,21 +499,23 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG, PAIR>::WPC * 32, 1) spmm_st
         cp_wait<NB - 1>();
         __syncwarp();  // ids copied by lanes 0-1 visible to the warp
 #pragma unroll
-        for (int kb = 0; kb < KB; ++kb) {
-          float x0[NT], x1[NT];
-          lds_slice<NT>(x0, xs + xo + kb * SLOT);
-          lds_slice<NT>(x1, xs + xo + kb * SLOT + d1);
-          const uint4 af = lds_frag(fa + kb * 512);
+        for (int kb = 0; kb < KB; ++kb) {  // block kb of the step at kb * SLOT * OPS
+          {
+            float x0[NT], x1[NT];
+            lds_slice<NT>(x0, xs + xo + kb * SLOT * C::OPS);
+            lds_slice<NT>(x1, xs + xo + kb * SLOT * C::OPS + d1);
+            const uint4 af = lds_frag(fa + kb * 512);
 #pragma unroll
-          for (int j = 0; j < NT; ++j) mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
-        }
-        if constexpr (DUAL) {
-          float x0[NT], x1[NT];
-          lds_slice<NT>(x0, xs + xo + SLOT);
-          lds_slice<NT>(x1, xs + xo + SLOT + d1);
-          const uint4 af = lds_frag(fa + MB * 512);
+            for (int j = 0; j < NT; ++j) mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
+          }
+          if constexpr (DUAL) {
+            float x0[NT], x1[NT];
+            lds_slice<NT>(x0, xs + xo + kb * SLOT * C::OPS + SLOT);
+            lds_slice<NT>(x1, xs + xo + kb * SLOT * C::OPS + SLOT + d1);
+            const uint4 af = lds_frag(fa + kb * 512 + MB * 512);
 #pragma unroll
-          for (int j = 0; j < NT; ++j) mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
+            for (int j = 0; j < NT; ++j) mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
+          }
         }
         // refill: X of block s + NB into this slot, ids of block s + 2NB. The
         // 16-wide path's lanes read slices copied by other lanes: all reads of
@@ -1367,11 +1369,12 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
     }
     // 16-wide single-operand chunks: two blocks per step over the pair stream
     // 32-wide single-operand chunks too (measured 34.8 -> 32.8 us at arxiv D=32, cold)
-    if (nt == 4 && !dual && !big && !mk && t->pair_offsets && t->pair_stream && !pair_off) {
+    if (nt == 4 && !big && !mk && t->pair_offsets && t->pair_stream && !pair_off) {
       stream::Args ap = a;
       ap.boff = t->pair_offsets;
       ap.cs = t->pair_stream;
-      return stream::launch_t<4, false, false, false, true>(ap, nchunks, s);
+      return dual ? stream::launch_t<4, true, false, false, true>(ap, nchunks, s)
+                  : stream::launch_t<4, false, false, false, true>(ap, nchunks, s);
     }
     if (nt == 2 && !dual && a.x16 && t->pair_offsets && t->pair_stream && !pair_off) {
       stream::Args ap = a;

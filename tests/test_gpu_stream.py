@@ -93,6 +93,10 @@ for n, deg, d, seed in ((3001, 7, 16, 1), (2000, 40, 16, 2), (777, 3, 12, 3), (1
     x = torch.from_numpy(rng.standard_normal((n, d)).astype(np.float32)).cuda()
     w = torch.from_numpy(rng.random(g.num_edges).astype(np.float32)).cuda()
     out.append(spmm_device(t, x, w, mode="tf32").cpu().numpy())
+    if d == 32:  # the dual form of the AGNN backward's A^T pass
+        x2 = torch.from_numpy(rng.standard_normal((n, d)).astype(np.float32)).cuda()
+        w2 = torch.from_numpy(rng.random(g.num_edges).astype(np.float32)).cuda()
+        out.append(spmm_device(t, x, w, x2=x2, weights2=w2, mode="tf32").cpu().numpy())
 np.save(sys.argv[2], np.concatenate([o.ravel() for o in out]))
 """
 
@@ -101,8 +105,8 @@ def test_pair_steps_bitwise_equal_single_block_steps(tmp_path):
     """The 16-wide two-blocks-per-step path (pair stream) is the same mma
     sequence per window as the one-block-per-step path (TCG_NO_PAIRS=1): the
     results are bitwise equal, incl. 40-edge windows (BIG staging), a masked
-    12-wide chunk, a 48-wide operand's 16-wide tail and 32 / 64-wide operands
-    (32-wide pair steps)."""
+    12-wide chunk, a 48-wide operand's 16-wide tail, 32 / 64-wide operands
+    (32-wide pair steps) and the two-operand (dual) form."""
     import os
     import subprocess
     import sys
