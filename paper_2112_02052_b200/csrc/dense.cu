@@ -466,6 +466,11 @@ int64_t slabs_for(int64_t n) {
 
 using namespace tcg;
 
+namespace tcg {
+int dense_tcgen05(const float* x, int64_t ldx, int64_t n, int ci, const float* m, int co, bool trans,
+                  const float* bias, int relu, const float* mask, float* y, int64_t ldy, cudaStream_t s);
+}
+
 extern "C" int tcg_dense(const float* x, int64_t ldx, int64_t n, int64_t ci, const float* m,
                          int64_t co, int32_t m_transposed, const float* bias, int32_t relu,
                          const float* mask, int64_t ldm, float* y, int64_t ldy, void* stream) {
@@ -474,6 +479,12 @@ extern "C" int tcg_dense(const float* x, int64_t ldx, int64_t n, int64_t ci, con
   if (n == 0) return TCG_OK;
   TCG_REQUIRE(x && m && y, "tcg_dense: null pointer");
   cudaStream_t s = as_stream(stream);
+  {
+    // tcgen05 3xTF32 GEMM (csrc/dense_tc.cu) for the wide input layers
+    const int rc = dense_tcgen05(x, ldx, n, (int)ci, m, (int)co, m_transposed != 0, bias, relu, mask, y,
+                                 ldy, s);
+    if (rc != 1) return rc;
+  }
   {
     const int rc = fast_dense(x, ldx, n, (int)ci, m, (int)co, m_transposed != 0, bias, relu, mask,
                               ldm, y, ldy, s);
