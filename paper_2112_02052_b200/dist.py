@@ -262,6 +262,20 @@ class Shard:
             self._bufs["at"] = got
         return got
 
+    def comm_stream(self):
+        """Side stream for collectives that overlap kernels (NCCL only: gloo
+        stages through the host synchronously); None when not overlapping."""
+        import torch
+        import torch.distributed as dist
+
+        if not dist.is_initialized() or dist.get_backend(self.group) != "nccl":
+            return None
+        st = self._bufs.get("comm_stream")
+        if st is None:
+            st = torch.cuda.Stream(device=self.t.device)
+            self._bufs["comm_stream"] = st
+        return st
+
     def allreduce_grads(self, params):
         """Sum the row-sharded weight gradients over the ranks (one collective
         over the flattened gradients)."""

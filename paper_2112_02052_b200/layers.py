@@ -261,7 +261,17 @@ class AgnnAggShard(torch.autograd.Function):
         _, yf, _ = sh.rows_buffer(("y", key), d)
         gbuf, gf, gmine = sh.rows_buffer("grad", d)
         gmine.copy_(g)
-        allgather_rows(gbuf, sh.plan, sh.group)
+        # The A-side kernel reads only this rank's rows of G (the SDDMM's own-row
+        # operand) and the already gathered Z, so under NCCL the G all-gather runs
+        # on a side stream beside it; the A^T pass below needs every row of G.
+        side = sh.comm_stream()
+        if side is not None:
+            cur = torch.cuda.current_stream()
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                allgather_rows(gbuf, sh.plan, sh.group)
+        else:
+            allgather_rows(gbuf, sh.plan, sh.group)
         ebuf, pv, dsv = sh.edge_buffer(key)
         wr = sh.plan.my_windows
         r0, r1 = sh.plan.my_rows
@@ -273,6 +283,8 @@ class AgnnAggShard(torch.autograd.Function):
             sddmm_device(sh.t, gf, zf, mode=mode, epilogue=_lib.EPI_SOFTMAX_BWD, aux=pv, out=dsv,
                          win_range=wr)
             spmm_device(sh.t, zf, dsv, mode=mode, out=out, win_range=wr, y_row0=r0)
+        if side is not None:
+            torch.cuda.current_stream().wait_stream(side)
         allgather_edges(ebuf, sh.plan, sh.group)
         pt, dst = sh.at_buffers()
         kb, ke = sh.t_edges
