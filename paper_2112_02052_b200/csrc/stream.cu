@@ -914,11 +914,12 @@ __device__ __forceinline__ uint32_t agnn_off(int r, int c) {
   return r * 128 + ((c ^ h) & 7) * 16;
 }
 
-template <int KIND>
+template <int KIND, bool PAIR = false>
 __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const AgnnArgs a) {
   using C = AgnnCfg<KIND>;
   constexpr bool BWD = KIND == 1;   // 0: forward, 1: backward A-side, 2: SDDMM only
   constexpr int NB = C::NB, NI = C::NI;
+  constexpr int KB = PAIR ? 2 : 1;  // blocks per step
   constexpr float kLog2e = 1.4426950408889634f;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1059,38 +1060,50 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
     float acc[4][4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-    for (int lb = 0; lb < nbw; ++lb, ++s) {
-      cp_wait<NB - 1>();
+    // KB blocks per step (PAIR: the window-even-padded pair stream): one ring
+    // wait, one row-max exchange and rescale check, and two independent
+    // SDDMM mma chains per step
+    for (int lb = 0; lb < nbw; lb += KB, s += KB) {
+      cp_wait<NB - KB>();
       __syncwarp();
-      const uint32_t sb = ring + (s & (NB - 1)) * 1024;
-      // SDDMM: sc = scores in SpMM-A layout (slot order: (g,t), (g+8,t), (g,t+4), (g+8,t+4))
-      float sc[4] = {0.f, 0.f, 0.f, 0.f};
-      {
+      // SDDMM: scores in SpMM-A layout (slot order: (g,t), (g+8,t), (g,t+4), (g+8,t+4))
+      float v[KB][4];
+      uint32_t mw[KB];
+#pragma unroll
+      for (int kb = 0; kb < KB; ++kb) {
+        const uint32_t sb = ring + ((s + kb) & (NB - 1)) * 1024;
+        float sc[4] = {0.f, 0.f, 0.f, 0.f};
         float b0[4], b1[4];
         lds_slice<4>(b0, sb + sd0);
         lds_slice<4>(b1, sb + sd1);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          mma_tf32_rb(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], b0[j], b1[j]);
+        for (int j = 0; j < 4; ++j) mma_tf32_rb(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], b0[j], b1[j]);
+        // C (g, 2t) <-> A (g, t); C (g, 2t+1) <-> A (g, t+4): A slots are
+        // (0: (g,t), 1: (g+8,t), 2: (g,t+4), 3: (g+8,t+4)); C regs are
+        // (0: (g,2t), 1: (g,2t+1), 2: (g+8,2t), 3: (g+8,2t+1))
+        v[kb][0] = sc[0], v[kb][1] = sc[2], v[kb][2] = sc[1], v[kb][3] = sc[3];
+        mw[kb] = lb + kb < kMapB ? map32[(lb + kb) * 32 + lane] : 0u;
       }
-      // C (g, 2t) <-> A (g, t); C (g, 2t+1) <-> A (g, t+4): A slots are
-      // (0: (g,t), 1: (g+8,t), 2: (g,t+4), 3: (g+8,t+4)); C regs are
-      // (0: (g,2t), 1: (g,2t+1), 2: (g+8,2t), 3: (g+8,2t+1))
-      const float v[4] = {sc[0], sc[2], sc[1], sc[3]};
-      const uint32_t mw = lb < kMapB ? map32[lb * 32 + lane] : 0u;
-      float av[4];
+      float av[KB][4];
       if constexpr (KIND == 2) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t ej = (mw >> (8 * q)) & 0xffu;
-          if (ej) esc[ej - 1] = v[q];
-        }
+        for (int kb = 0; kb < KB; ++kb)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t ej = (mw[kb] >> (8 * q)) & 0xffu;
+            if (ej) esc[ej - 1] = v[kb][q];
+          }
         (void)av;
       } else if constexpr (KIND == 0) {
-        // block row maxima (rows g, g+8) over the quad
-        float bm[2];
-        bm[0] = fmaxf((mw & 0xffu) ? v[0] : -INFINITY, (mw & 0xff0000u) ? v[2] : -INFINITY);
-        bm[1] = fmaxf((mw & 0xff00u) ? v[1] : -INFINITY, (mw & 0xff000000u) ? v[3] : -INFINITY);
+        // step row maxima (rows g, g+8) over the quad and the step's blocks
+        float bm[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+          bm[0] = fmaxf(bm[0], fmaxf((mw[kb] & 0xffu) ? v[kb][0] : -INFINITY,
+                                     (mw[kb] & 0xff0000u) ? v[kb][2] : -INFINITY));
+          bm[1] = fmaxf(bm[1], fmaxf((mw[kb] & 0xff00u) ? v[kb][1] : -INFINITY,
+                                     (mw[kb] & 0xff000000u) ? v[kb][3] : -INFINITY));
+        }
 #pragma unroll
         for (int rh = 0; rh < 2; ++rh) {
           bm[rh] = fmaxf(bm[rh], __shfl_xor_sync(0xffffffffu, bm[rh], 1));
@@ -1121,38 +1134,50 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
           }
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t ej = (mw >> (8 * q)) & 0xffu;
-          av[q] = ej ? ex2_approx(fmaf(v[q], kLog2e, -ml2[q & 1])) : 0.f;
-          lrow[q & 1] += av[q];
-          if (ej) esc[ej - 1] = v[q];
-        }
+        for (int kb = 0; kb < KB; ++kb)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t ej = (mw[kb] >> (8 * q)) & 0xffu;
+            av[kb][q] = ej ? ex2_approx(fmaf(v[kb][q], kLog2e, -ml2[q & 1])) : 0.f;
+            lrow[q & 1] += av[kb][q];
+            if (ej) esc[ej - 1] = v[kb][q];
+          }
       } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t ej = (mw >> (8 * q)) & 0xffu;
-          float d = 0.f;
-          if (ej) {
-            const float pv = esc[ej - 1];
-            d = pv * (v[q] - rs[q & 1]);
-            a.eout[e0 + ej - 1] = d;
+        for (int kb = 0; kb < KB; ++kb)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t ej = (mw[kb] >> (8 * q)) & 0xffu;
+            float d = 0.f;
+            if (ej) {
+              const float pv = esc[ej - 1];
+              d = pv * (v[kb][q] - rs[q & 1]);
+              a.eout[e0 + ej - 1] = d;
+            }
+            av[kb][q] = d;
           }
-          av[q] = d;
-        }
       }
       // SpMM: acc += A_av * Zc
       if constexpr (KIND != 2) {
-        float x0[4], x1[4];
-        lds_slice<4>(x0, sb + so0);
-        lds_slice<4>(x1, sb + so1);
-        const uint32_t a0 = tf32_rn(av[0]), a1 = tf32_rn(av[1]), a2 = tf32_rn(av[2]), a3 = tf32_rn(av[3]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) mma_tf32_rb(acc[j], a0, a1, a2, a3, x0[j], x1[j]);
+        for (int kb = 0; kb < KB; ++kb) {
+          const uint32_t sb = ring + ((s + kb) & (NB - 1)) * 1024;
+          float x0[4], x1[4];
+          lds_slice<4>(x0, sb + so0);
+          lds_slice<4>(x1, sb + so1);
+          const uint32_t a0 = tf32_rn(av[kb][0]), a1 = tf32_rn(av[kb][1]), a2 = tf32_rn(av[kb][2]),
+                         a3 = tf32_rn(av[kb][3]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) mma_tf32_rb(acc[j], a0, a1, a2, a3, x0[j], x1[j]);
+        }
       }
       __syncwarp();
-      issue_x(s + NB);
-      issue_idx(s + 2 * NB);
-      cp_commit();
+#pragma unroll
+      for (int kb = 0; kb < KB; ++kb) {
+        issue_x(s + kb + NB);
+        issue_idx(s + kb + 2 * NB);
+        cp_commit();
+      }
     }
     // ---- window epilogue ----
     float inv[2] = {1.f, 1.f};
@@ -1222,10 +1247,10 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
   cp_wait<0>();
 }
 
-template <int KIND>
+template <int KIND, bool PAIR = false>
 int launch_agnn(AgnnArgs& a, cudaStream_t s) {
   using C = AgnnCfg<KIND>;
-  auto kern = agnn_stream<KIND>;
+  auto kern = agnn_stream<KIND, PAIR>;
   static int configured = -1;
   int dev = 0;
   TCG_CUDA(cudaGetDevice(&dev), "agnn_stream device");
@@ -1447,6 +1472,14 @@ int stream_agnn(const tcg_tiling* t, bool bwd, const float* z, int64_t ldz, cons
   a.win_begin = (int)win_begin, a.win_end = (int)win_end;
   a.z = z, a.ldz = ldz, a.za = za, a.lda = lda, a.yf = yf, a.ldyf = ldyf, a.pin = pin;
   a.eout = eout, a.y = y, a.ldy = ldy, a.y_row0 = y_row0;
+  static const bool pair_off = std::getenv("TCG_NO_PAIRS") != nullptr;
+  // forward: two blocks per step (arxiv 59.4 -> 55.3 us cold); the backward was
+  // measured slower that way (59.5 -> 63.5 us: its per-edge dS stores and P
+  // loads double up per step) and keeps one block per step
+  if (!bwd && t->pair_offsets && t->pair_stream && !pair_off) {
+    a.boff = t->pair_offsets, a.cs = t->pair_stream;
+    return stream::launch_agnn<0, true>(a, s);
+  }
   return bwd ? stream::launch_agnn<1>(a, s) : stream::launch_agnn<0>(a, s);
 }
 
@@ -1466,6 +1499,11 @@ int stream_sddmm(const tcg_tiling* t, const float* xa, int64_t lda, const float*
   a.n = t->num_nodes;
   a.win_begin = (int)win_begin, a.win_end = (int)win_end;
   a.z = xb, a.ldz = ldb, a.za = xa, a.lda = lda, a.pin = aux, a.eout = out, a.epi = epi;
+  static const bool pair_off = std::getenv("TCG_NO_PAIRS") != nullptr;
+  if (t->pair_offsets && t->pair_stream && !pair_off) {
+    a.boff = t->pair_offsets, a.cs = t->pair_stream;
+    return stream::launch_agnn<2, true>(a, s);
+  }
   return stream::launch_agnn<2>(a, s);
 }
 
