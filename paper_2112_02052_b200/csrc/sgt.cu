@@ -127,10 +127,24 @@ __global__ void __launch_bounds__(kRankThreads)
 constexpr int kIdxBits = 9;
 constexpr int kWarpCap = 1 << kIdxBits;  // 512 edges: K = 16 keys per lane
 
+// Keys are kept complemented wherever the current merge level's block runs
+// descending, so every compare-exchange is a plain (min, max) pair -- intra-lane
+// two VIMNMX, inter-lane one SHFL and one VIMNMX with the lower lane keeping the
+// minimum -- and the direction bookkeeping is one XOR per key per level (the
+// last level is ascending everywhere, so the keys leave uncomplemented).
 template <int K>
 __device__ __forceinline__ void warp_bitonic(uint32_t (&v)[K], int lane) {
+  auto desc = [&](int r, int k) { return ((lane * K + r) & k) != 0; };
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+    if (desc(r, 2)) v[r] = ~v[r];
 #pragma unroll
   for (int k = 2; k <= 32 * K; k <<= 1) {
+    if (k > 2) {
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        if (desc(r, k >> 1) != desc(r, k)) v[r] = ~v[r];
+    }
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
       if (j >= K) {
@@ -139,17 +153,15 @@ __device__ __forceinline__ void warp_bitonic(uint32_t (&v)[K], int lane) {
 #pragma unroll
         for (int r = 0; r < K; ++r) {
           const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], lj);
-          const bool up = ((lane * K + r) & k) == 0;
-          v[r] = (lower == up) ? min(v[r], o) : max(v[r], o);
+          v[r] = lower ? min(v[r], o) : max(v[r], o);
         }
       } else {
 #pragma unroll
         for (int r = 0; r < K; ++r) {
           if ((r & j) == 0) {
-            const bool up = ((lane * K + r) & k) == 0;
-            const uint32_t a = v[r], b = v[r | j];
-            v[r] = up ? min(a, b) : max(a, b);
-            v[r | j] = up ? max(a, b) : min(a, b);
+            const uint32_t x = v[r], y = v[r | j];
+            v[r] = min(x, y);
+            v[r | j] = max(x, y);
           }
         }
       }
@@ -193,7 +205,7 @@ __device__ __forceinline__ int64_t warp_rank_window(const uint32_t* __restrict__
   return __shfl_sync(0xffffffffu, incl, 31);
 }
 
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, 2)
     sgt_rank_warp(const int64_t* __restrict__ ptr, const uint32_t* __restrict__ cols, int64_t n,
                   int64_t w0, int64_t num_windows, int bh, int bw, uint32_t* __restrict__ e2c,
                   int64_t* __restrict__ ucount, uint32_t* __restrict__ wp, int* __restrict__ mid_list,
