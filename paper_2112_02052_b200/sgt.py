@@ -301,15 +301,14 @@ def _sgt_device(ptr, cols, n: int, m: int, cfg: BlockConfig, graph) -> TiledGrap
     wsb = int(lib.tcg_sgt_workspace_bytes(n, m, cfg.blk_h))
     ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
     cp = cols.data_ptr() if m else None
-    # two phases, no host round trip between them: col_to_node is allocated at
-    # its upper bound M (U <= M) and U = col_offsets[W] is read lazily, on the
-    # first use that needs it as a host integer (TiledGraph.num_unique)
-    _lib.check(lib.tcg_sgt_count(ptr.data_ptr(), cp, n, m, cfg.blk_h, cfg.blk_w, e2c.data_ptr(),
-                                 offs.data_ptr(), ws.data_ptr(), wsb, _stream_ptr()), "tcg_sgt")
+    # one ABI call (count + scan + fill enqueued back to back from C), no host
+    # round trip: col_to_node is allocated at its upper bound M (U <= M) and
+    # U = col_offsets[W] is read lazily, on the first use that needs it as a
+    # host integer (TiledGraph.num_unique)
     c2n = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
-    _lib.check(lib.tcg_sgt_fill(ptr.data_ptr(), cp, n, m, cfg.blk_h, cfg.blk_w, e2c.data_ptr(),
-                                offs.data_ptr(), wp.data_ptr(), c2n.data_ptr(), _stream_ptr()),
-               "tcg_sgt")
+    _lib.check(lib.tcg_sgt(ptr.data_ptr(), cp, n, m, cfg.blk_h, cfg.blk_w, wp.data_ptr(),
+                           e2c.data_ptr(), offs.data_ptr(), c2n.data_ptr(), ws.data_ptr(), wsb,
+                           _stream_ptr()), "tcg_sgt")
     t = TiledGraph(graph, cfg, n, m, W)
     t.dev.update(node_ptr=ptr, edge_list=cols, win_partition=wp[:W], edge_to_col=e2c[:m],
                  col_offsets=offs, col_to_node=c2n)
