@@ -902,7 +902,8 @@ struct AgnnCfg {
   static constexpr int MAP = kMapB * 128;      // u8 per fragment slot: local edge + 1
   static constexpr int ESC = 256 * 4;          // per-edge scores (fwd) / P (bwd)
   static constexpr int ROW = 64 * 4;           // row stats
-  static constexpr int WARP = RING + IDX + MAP + ESC + ROW;
+  static constexpr int EROW = 256;             // fwd: window-local row of each edge (u8)
+  static constexpr int WARP = RING + IDX + MAP + ESC + ROW + EROW;
   static constexpr int WPC = 8;
   static constexpr int SMEM = WPC * WARP;
 };
@@ -934,6 +935,10 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
   float* rowm = esc + 256;   // [16] running max (fwd)
   float* rowl = rowm + 16;   // [16] 1 / row sum (fwd)
   float* rowrs = rowl + 16;  // [16] rs (bwd)
+  unsigned char* erow = reinterpret_cast<unsigned char*>(esc + 256 + 64);  // [256] fwd
+  // window-local row of fragment slot f: lane (g, t) = (f >> 2) & 31, register f & 3
+  // holds rows g (even) / g + 8 (odd)
+  auto slot_row = [](uint32_t f) { return (unsigned char)((((f >> 2) & 31u) >> 2) + 8u * (f & 1u)); };
 
   const int B0 = __ldg(a.boff + a.win_begin), B1 = __ldg(a.boff + a.win_end);
   const int64_t TBr = B1 - B0;
@@ -1013,13 +1018,19 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < kEPL; ++k) {
-      if (pf[k] < (uint32_t)(kMapB * 128)) map[pf[k]] = (unsigned char)(lane + 32 * k + 1);
+      if (pf[k] < (uint32_t)(kMapB * 128)) {
+        map[pf[k]] = (unsigned char)(lane + 32 * k + 1);
+        if constexpr (KIND == 0) erow[lane + 32 * k] = slot_row(pf[k]);
+      }
       if constexpr (BWD)
         if (lane + 32 * k < ne) esc[lane + 32 * k] = pp[k];
     }
     for (int j = 32 * kEPL + lane; j < ne; j += 32) {
       const uint32_t f = __ldg(a.efrag + e0 + j);
-      if (f < (uint32_t)(kMapB * 128)) map[f] = (unsigned char)(j + 1);
+      if (f < (uint32_t)(kMapB * 128)) {
+        map[f] = (unsigned char)(j + 1);
+        if constexpr (KIND == 0) erow[j] = slot_row(f);
+      }
       if constexpr (BWD) esc[j] = __ldg(a.pin + e0 + j);
     }
 #pragma unroll
@@ -1152,7 +1163,7 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
             if (ej) {
               const float pv = esc[ej - 1];
               d = pv * (v[kb][q] - rs[q & 1]);
-              a.eout[e0 + ej - 1] = d;
+              esc[ej - 1] = d;  // every edge once per window: dS replaces its P
             }
             av[kb][q] = d;
           }
@@ -1221,14 +1232,15 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
         rowl[g] = inv[0], rowl[g + 8] = inv[1];
       }
       __syncwarp();
-      // P_e = exp(S_e - m_i) / l_i, two lanes per row
-      const int r = lane >> 1, sub = lane & 1;
-      const int64_t rg = (int64_t)w * 16 + r;
-      if (rg < a.n) {
-        const int64_t rb = __ldg(a.ptr + rg) - e0, re = __ldg(a.ptr + rg + 1) - e0;
-        const float m = rowm[r], il = rowl[r];
-        for (int64_t j = rb + sub; j < re; j += 2) a.eout[e0 + j] = ex2_approx((esc[j] - m) * kLog2e) * il;
+      // P_e = exp(S_e - m_i) / l_i over the window's edges in order (coalesced)
+      for (int j = lane; j < ne; j += 32) {
+        const int r = erow[j];
+        a.eout[e0 + j] = ex2_approx((esc[j] - rowm[r]) * kLog2e) * rowl[r];
       }
+    } else if constexpr (KIND == 1) {
+      // dS of the window's edges, in order (coalesced)
+      __syncwarp();
+      for (int j = lane; j < ne; j += 32) a.eout[e0 + j] = esc[j];
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
