@@ -1485,9 +1485,9 @@ int stream_agnn(const tcg_tiling* t, bool bwd, const float* z, int64_t ldz, cons
   a.z = z, a.ldz = ldz, a.za = za, a.lda = lda, a.yf = yf, a.ldyf = ldyf, a.pin = pin;
   a.eout = eout, a.y = y, a.ldy = ldy, a.y_row0 = y_row0;
   static const bool pair_off = std::getenv("TCG_NO_PAIRS") != nullptr;
-  // forward: two blocks per step (arxiv 59.4 -> 55.3 us cold); the backward was
-  // measured slower that way (59.5 -> 63.5 us: its per-edge dS stores and P
-  // loads double up per step) and keeps one block per step
+  // forward: two blocks per step (arxiv 59.4 -> 55.3 us cold); the backward
+  // measured slower that way (55.3 -> 57.3 us with the coalesced dS writes,
+  // 59.5 -> 63.5 us before) and keeps one block per step
   if (!bwd && t->pair_offsets && t->pair_stream && !pair_off) {
     a.boff = t->pair_offsets, a.cs = t->pair_stream;
     return stream::launch_agnn<0, true>(a, s);
