@@ -902,7 +902,7 @@ struct AgnnCfg {
   static constexpr int MAP = kMapB * 128;      // u8 per fragment slot: local edge + 1
   static constexpr int ESC = 256 * 4;          // per-edge scores (fwd) / P (bwd)
   static constexpr int ROW = 64 * 4;           // row stats
-  static constexpr int EROW = 256;             // fwd: window-local row of each edge (u8)
+  static constexpr int EROW = 256;             // fwd / SDDMM: window-local row of each edge (u8)
   static constexpr int WARP = RING + IDX + MAP + ESC + ROW + EROW;
   static constexpr int WPC = 8;
   static constexpr int SMEM = WPC * WARP;
@@ -1020,7 +1020,7 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
     for (int k = 0; k < kEPL; ++k) {
       if (pf[k] < (uint32_t)(kMapB * 128)) {
         map[pf[k]] = (unsigned char)(lane + 32 * k + 1);
-        if constexpr (KIND == 0) erow[lane + 32 * k] = slot_row(pf[k]);
+        if constexpr (KIND != 1) erow[lane + 32 * k] = slot_row(pf[k]);
       }
       if constexpr (BWD)
         if (lane + 32 * k < ne) esc[lane + 32 * k] = pp[k];
@@ -1029,7 +1029,7 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
       const uint32_t f = __ldg(a.efrag + e0 + j);
       if (f < (uint32_t)(kMapB * 128)) {
         map[f] = (unsigned char)(j + 1);
-        if constexpr (KIND == 0) erow[j] = slot_row(f);
+        if constexpr (KIND != 1) erow[j] = slot_row(f);
       }
       if constexpr (BWD) esc[j] = __ldg(a.pin + e0 + j);
     }
@@ -1201,8 +1201,10 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
       const bool live = rg < a.n;  // every lane runs the same shuffles
       const int64_t rb = live ? __ldg(a.ptr + rg) - e0 : 0;
       const int64_t re = live ? __ldg(a.ptr + rg + 1) - e0 : 0;
+      // row statistics with two lanes per row, then the outputs in edge order
+      // (coalesced) through the per-edge row table
       if (a.epi == TCG_EPI_NONE) {
-        for (int64_t j = rb + sub; j < re; j += 2) a.eout[e0 + j] = esc[j];
+        for (int j = lane; j < ne; j += 32) a.eout[e0 + j] = esc[j];
       } else if (a.epi == TCG_EPI_SOFTMAX) {
         float mx = -INFINITY;
         for (int64_t j = rb + sub; j < re; j += 2) mx = fmaxf(mx, esc[j]);
@@ -1210,13 +1212,20 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
         float sm = 0.f;
         for (int64_t j = rb + sub; j < re; j += 2) sm += expf(esc[j] - mx);
         sm += __shfl_xor_sync(0xffffffffu, sm, 1);
-        for (int64_t j = rb + sub; j < re; j += 2) a.eout[e0 + j] = expf(esc[j] - mx) / sm;
+        if (sub == 0) rowm[r] = mx, rowl[r] = sm;
+        __syncwarp();
+        for (int j = lane; j < ne; j += 32) {
+          const int q = erow[j];
+          a.eout[e0 + j] = expf(esc[j] - rowm[q]) / rowl[q];
+        }
       } else {
         float rsum = 0.f;
         for (int64_t j = rb + sub; j < re; j += 2) rsum += __ldg(a.pin + e0 + j) * esc[j];
         rsum += __shfl_xor_sync(0xffffffffu, rsum, 1);
-        for (int64_t j = rb + sub; j < re; j += 2)
-          a.eout[e0 + j] = __ldg(a.pin + e0 + j) * (esc[j] - rsum);
+        if (sub == 0) rowrs[r] = rsum;
+        __syncwarp();
+        for (int j = lane; j < ne; j += 32)
+          a.eout[e0 + j] = __ldg(a.pin + e0 + j) * (esc[j] - rowrs[erow[j]]);
       }
     } else if constexpr (KIND == 0) {
 #pragma unroll
