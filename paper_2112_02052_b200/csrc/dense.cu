@@ -467,6 +467,10 @@ int64_t slabs_for(int64_t n) {
 using namespace tcg;
 
 namespace tcg {
+int dense_mma32(const float* x, int64_t ldx, int64_t n, int ci, const float* w, int co, bool trans,
+                const float* bias, int relu, const float* mask, float* y, int64_t ldy, cudaStream_t s);
+int dense_mma32_bwd(const float* x, int64_t ldx, const float* g, int64_t ldg, int64_t n, const float* w,
+                    float* dx, int64_t lddx, float* part, int64_t* slabs, cudaStream_t s);
 int dense_tcgen05(const float* x, int64_t ldx, int64_t n, int ci, const float* m, int co, bool trans,
                   const float* bias, int relu, const float* mask, float* y, int64_t ldy, cudaStream_t s);
 }
@@ -479,6 +483,11 @@ extern "C" int tcg_dense(const float* x, int64_t ldx, int64_t n, int64_t ci, con
   if (n == 0) return TCG_OK;
   TCG_REQUIRE(x && m && y, "tcg_dense: null pointer");
   cudaStream_t s = as_stream(stream);
+  {
+    // 32 x 32: mma.sync 3xTF32, ldmatrix-fed (csrc/dense_mma.cu)
+    const int rc = dense_mma32(x, ldx, n, (int)ci, m, (int)co, m_transposed != 0, bias, relu, mask, y, ldy, s);
+    if (rc != 1) return rc;
+  }
   {
     // tcgen05 3xTF32 GEMM (csrc/dense_tc.cu) for the wide input layers
     const int rc = dense_tcgen05(x, ldx, n, (int)ci, m, (int)co, m_transposed != 0, bias, relu, mask, y,
@@ -656,6 +665,17 @@ extern "C" int tcg_dense_backward(const float* x, int64_t ldx, const float* g, i
     if (rc != TCG_OK) return rc;
     return tcg_gemm_tn(x, ldx, g, ldg, nullptr, 0, n, ci, co, dw, nullptr, workspace,
                        workspace_bytes, stream);
+  }
+  {
+    int64_t slabs = 0;
+    float* part = static_cast<float*>(workspace);
+    const int rc = dense_mma32_bwd(x, ldx, g, ldg, n, w, dx, lddx, part, &slabs, s);
+    if (rc == TCG_OK) {
+      sum_slabs<<<(unsigned)((ci * co + 31) / 32), 1024, 0, s>>>(part, (int)slabs, ci * co, dw);
+      TCG_LAUNCHED("sum_slabs");
+      return TCG_OK;
+    }
+    if (rc != 1) return rc;
   }
   using Cfg = dr::BwdCfg<32, 32>;
   static int dev_done = -1, per_sm = 1;
