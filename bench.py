@@ -386,10 +386,9 @@ def run_ours(args):
 
     def train_step():
         opt.zero_grad(set_to_none=True)
-        if shard is None:
-            loss = layers.cross_entropy(net(x_dev, t), y_dev)
-        else:  # this rank's rows; weight gradients summed over the ranks
-            loss = layers.cross_entropy_sharded(net(x_dev, t, shard), y_dev, shard)
+        # the output layer runs inside the loss kernel (layers.*.loss); with a
+        # shard, this rank's rows and weight gradients summed over the ranks
+        loss = net.loss(x_dev, t, y_dev, shard)
         loss.backward()
         if shard is not None:
             shard.allreduce_grads(net.parameters())
@@ -688,7 +687,7 @@ def run_ours(args):
 
             def gstep():
                 gopt.zero_grad(set_to_none=True)
-                lo = layers.cross_entropy(gnet(x_dev, t), y_dev)
+                lo = gnet.loss(x_dev, t, y_dev)
                 lo.backward()
                 gopt.step()
                 return lo.detach()

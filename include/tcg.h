@@ -324,6 +324,33 @@ int tcg_softmax_xent_backward(const float* logits, int64_t ld, const int64_t* la
                               int64_t c, const float* grad_scale, float* dlogits, int64_t ldd,
                               void* stream);
 
+size_t tcg_linear_xent_workspace_bytes(int64_t n);
+/* The output layer fused with the loss: logits = x W + bias (x [n x kin], W
+ * [kin x c] row-major, bias may be null) on mma.sync 3xTF32 (fp32-class), then
+ * loss = sum_i -log_softmax(logits_i)[labels_i] / div and
+ * dlogits[n x c] (row stride ldd) = (softmax - onehot) / div (dlogits may be
+ * null: the loss only). The logits never reach memory. div = n for the mean;
+ * the global row count for a row shard.
+ * Covers kin a multiple of 4 up to 32, c <= 48, 16-B aligned x rows; other
+ * shapes return TCG_E_UNSUPPORTED (callers run tcg_dense + tcg_softmax_xent).
+ * The last layer and the training loss of the paper's GCN / AGNN models
+ * (PAPER.md:684-689). Deterministic. */
+int tcg_linear_xent(const float* x, int64_t ldx, int64_t n, int64_t kin, const float* w, int64_t c,
+                    const float* bias, const int64_t* labels, int64_t div, float* loss,
+                    float* dlogits, int64_t ldd, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
+size_t tcg_linear_xent_backward_workspace_bytes(int64_t n, int64_t kin, int64_t c);
+/* Backward of tcg_linear_xent for an incoming loss gradient g = *grad_scale
+ * (device scalar; null => 1), recomputing the logits instead of reading a
+ * stored dlogits: d = (softmax - onehot) * g / div, dx = d W^T (dx may be
+ * null), dw = x^T d, db = colsum d (db may be null). Same coverage as
+ * tcg_linear_xent (else TCG_E_UNSUPPORTED). Deterministic. */
+int tcg_linear_xent_backward(const float* x, int64_t ldx, int64_t n, int64_t kin, const float* w,
+                             int64_t c, const float* bias, const int64_t* labels, int64_t div,
+                             const float* grad_scale, float* dx, int64_t lddx, float* dw, float* db,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- TF32 operand rounding: reference tiles.quantize_tf32 (67-82) ------- */
 int tcg_quantize_tf32(const float* in, float* out, int64_t n, void* stream);
 

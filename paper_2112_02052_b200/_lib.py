@@ -14,6 +14,7 @@ _PKG = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("TCG_B200_LIB", _PKG / "libtcg_b200.so"))
 
 TCG_OK = 0
+TCG_E_UNSUPPORTED = -4
 PREC_F32 = 0
 PREC_TF32 = 1
 EPI_NONE = 0
@@ -112,6 +113,11 @@ SIGNATURES = {
     "tcg_colsum": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _SZ, _P]),
     "tcg_softmax_xent_workspace_bytes": (_SZ, [_I64]),
     "tcg_softmax_xent": (C.c_int, [_P, _I64, _P, _I64, _I64, _P, _P, _P, _SZ, _P]),
+    "tcg_linear_xent_workspace_bytes": (_SZ, [_I64]),
+    "tcg_linear_xent": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _SZ, _P]),
+    "tcg_linear_xent_backward_workspace_bytes": (_SZ, [_I64, _I64, _I64]),
+    "tcg_linear_xent_backward": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _P, _P, _I64,
+                                           _P, _P, _P, _SZ, _P]),
     "tcg_softmax_xent_backward": (C.c_int, [_P, _I64, _P, _I64, _I64, _P, _P, _I64, _P]),
 }
 

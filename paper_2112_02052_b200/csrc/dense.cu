@@ -142,8 +142,10 @@ __global__ void __launch_bounds__(256)
 // Fixed-order sum of the slab partials.
 // 32 outputs per CTA x 8 summers: summer j adds slabs j, j+8, ... in order,
 // then the 8 partial sums are combined in a fixed order (deterministic).
+// (outputs from `split` on go to out2: the dW | db partials of one slab)
 __global__ void __launch_bounds__(1024) sum_slabs(const float* __restrict__ part, int slabs,
-                                                  int64_t len, float* __restrict__ out) {
+                                                  int64_t len, float* __restrict__ out,
+                                                  int64_t split = INT64_MAX, float* __restrict__ out2 = nullptr) {
   // 32 outputs x 32 slab groups per CTA (the partial count is ~300-600, so
   // every thread keeps ~10-20 independent loads in flight); the groups are
   // combined in a fixed order (deterministic)
@@ -166,7 +168,8 @@ __global__ void __launch_bounds__(1024) sum_slabs(const float* __restrict__ part
     float tot = 0.f;
 #pragma unroll 8
     for (int q = 0; q < 32; ++q) tot += sh[q][o];
-    out[i] = tot;
+    if (i < split) out[i] = tot;
+    else if (out2) out2[i - split] = tot;
   }
 }
 
@@ -471,6 +474,14 @@ int dense_mma32(const float* x, int64_t ldx, int64_t n, int ci, const float* w, 
                 const float* bias, int relu, const float* mask, float* y, int64_t ldy, cudaStream_t s);
 int dense_mma32_bwd(const float* x, int64_t ldx, const float* g, int64_t ldg, int64_t n, const float* w,
                     float* dx, int64_t lddx, float* part, int64_t* slabs, cudaStream_t s);
+int linear_xent(const float* x, int64_t ldx, int64_t n, int kin, const float* w, int c, const float* bias,
+                const int64_t* labels, float inv_div, float* dl, int64_t ldd, float* lpart, int64_t cap_parts,
+                int64_t* nparts, cudaStream_t s);
+int64_t linear_xent_parts(int64_t n);
+int64_t linear_xent_bwd_slabs(int64_t n);
+int linear_xent_bwd(const float* x, int64_t ldx, int64_t n, int kin, const float* w, int c, const float* bias,
+                    const int64_t* labels, const float* gscale, float inv_div, float* dx, int64_t lddx, float* part,
+                    int64_t* slabs, cudaStream_t s);
 int dense_tcgen05(const float* x, int64_t ldx, int64_t n, int ci, const float* m, int co, bool trans,
                   const float* bias, int relu, const float* mask, float* y, int64_t ldy, cudaStream_t s);
 }
@@ -592,6 +603,62 @@ extern "C" int tcg_softmax_xent_backward(const float* logits, int64_t ld, const 
   softmax_xent<false, true><<<(unsigned)((n + 31) / 32), 256, 0, as_stream(stream)>>>(
       logits, ld, labels, n, (int)c, dlogits, ldd, grad_scale, nullptr, 0);
   TCG_LAUNCHED("softmax_xent_backward");
+  return TCG_OK;
+}
+
+extern "C" size_t tcg_linear_xent_workspace_bytes(int64_t n) {
+  return (size_t)(linear_xent_parts(n > 0 ? n : 1) + 1) * sizeof(float);
+}
+
+extern "C" int tcg_linear_xent(const float* x, int64_t ldx, int64_t n, int64_t kin, const float* w,
+                               int64_t c, const float* bias, const int64_t* labels, int64_t div,
+                               float* loss, float* dlogits, int64_t ldd, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  TCG_REQUIRE(n >= 1 && kin >= 1 && c >= 1 && ldx >= kin && (!dlogits || ldd >= c) && div >= 1,
+              "tcg_linear_xent: bad shape");
+  TCG_REQUIRE(x && w && labels && loss && workspace, "tcg_linear_xent: null pointer");
+  TCG_REQUIRE(workspace_bytes >= tcg_linear_xent_workspace_bytes(n), "tcg_linear_xent: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  float* lpart = static_cast<float*>(workspace);
+  int64_t parts = 0;
+  const int rc = linear_xent(x, ldx, n, (int)kin, w, (int)c, bias, labels, 1.f / (float)div, dlogits, ldd,
+                             lpart, (int64_t)(workspace_bytes / sizeof(float)), &parts, s);
+  if (rc < 0) return rc;
+  if (rc > 0) {
+    set_error("tcg_linear_xent: shape not covered (needs kin a multiple of 4 <= 32, c <= 48, 16-B rows)");
+    return TCG_E_UNSUPPORTED;
+  }
+  final_loss<<<1, 256, 0, s>>>(lpart, parts, div, loss);
+  TCG_LAUNCHED("final_loss");
+  return TCG_OK;
+}
+
+extern "C" size_t tcg_linear_xent_backward_workspace_bytes(int64_t n, int64_t kin, int64_t c) {
+  return (size_t)(linear_xent_bwd_slabs(n > 0 ? n : 1) * (kin * c + c)) * sizeof(float);
+}
+
+extern "C" int tcg_linear_xent_backward(const float* x, int64_t ldx, int64_t n, int64_t kin, const float* w,
+                                        int64_t c, const float* bias, const int64_t* labels, int64_t div,
+                                        const float* grad_scale, float* dx, int64_t lddx, float* dw, float* db,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
+  TCG_REQUIRE(n >= 1 && kin >= 1 && c >= 1 && ldx >= kin && div >= 1 && (!dx || lddx >= kin),
+              "tcg_linear_xent_backward: bad shape");
+  TCG_REQUIRE(x && w && labels && dw && workspace, "tcg_linear_xent_backward: null pointer");
+  TCG_REQUIRE(workspace_bytes >= tcg_linear_xent_backward_workspace_bytes(n, kin, c),
+              "tcg_linear_xent_backward: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  float* part = static_cast<float*>(workspace);
+  int64_t slabs = 0;
+  const int rc = linear_xent_bwd(x, ldx, n, (int)kin, w, (int)c, bias, labels, grad_scale, 1.f / (float)div, dx,
+                                 lddx, part, &slabs, s);
+  if (rc < 0) return rc;
+  if (rc > 0) {
+    set_error("tcg_linear_xent_backward: shape not covered (needs kin a multiple of 4 <= 32, c <= 48, 16-B rows)");
+    return TCG_E_UNSUPPORTED;
+  }
+  const int64_t len = kin * c + c;
+  sum_slabs<<<(unsigned)((len + 31) / 32), 1024, 0, s>>>(part, (int)slabs, len, dw, kin * c, db);
+  TCG_LAUNCHED("sum_slabs");
   return TCG_OK;
 }
 

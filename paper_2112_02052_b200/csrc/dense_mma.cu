@@ -27,6 +27,16 @@ namespace dm {
 constexpr int WPC = 4;  // warps per CTA
 
 __device__ __forceinline__ uint32_t su(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];\n" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ float tf32f(float x) { return __uint_as_float(tf32_rn(x)); }
 
 // staged tile: 16 rows x 32 floats, 16-B chunk c of row r at r * 128 + ((c ^ (r & 7)) * 16)
@@ -320,5 +330,476 @@ int dense_mma32_bwd(const float* x, int64_t ldx, const float* g, int64_t ldg, in
   *slabs = blocks;
   return TCG_OK;
 }
+
+}  // namespace tcg
+
+// ---- output layer fused with the softmax cross-entropy ----------------------
+//
+// logits = x W + b (x: [n x kin], kin <= 32; W: [kin x c], c <= 8 NTL) on mma.sync
+// 3xTF32, and in the epilogue -- each quad of lanes holds a whole row -- the
+// row's log-sum-exp, the NLL of its label and dlogits = (softmax - onehot) / div.
+// The logits never reach memory; dlogits does (the backward reads it), and the
+// per-warp loss partials are summed in row order (deterministic), then by
+// final_loss. Classes >= c are masked to -inf.
+namespace tcg {
+namespace dm {
+
+// rows [row0, row0 + 16) of a [n x kin] matrix (kin a multiple of 4, <= 8 KT) into a
+// staged 16 x 32 tile (its first 2 KT 16-B chunks per row), zero past kin and past n
+template <int KT>
+__device__ __forceinline__ void stage_rows_k(uint32_t tile, const float* __restrict__ x, int64_t ldx, int64_t n,
+                                             int kin, int64_t row0, int lane) {
+  constexpr int CH = 2 * KT;
+#pragma unroll
+  for (int i = 0; i < KT; ++i) {
+    const int q = lane + 32 * i, r = q / CH, c = q % CH;
+    const int64_t gr = row0 + r;
+    const bool ok = gr < n && 4 * c < kin;
+    cp16z(tile + sw(r, c), x + (ok ? gr : 0) * ldx + (ok ? 4 * c : 0), ok);
+  }
+}
+
+// The logits are carried in log2 units (W and the bias pre-scaled by log2 e),
+// so the softmax runs on MUFU ex2 / lg2 directly.
+constexpr float kLog2e = 1.4426950408889634f, kLn2 = 0.6931471805599453f;
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// W (kin x c) * log2 e as tf32 hi / lo in shared memory, [feature][class] with a
+// pitch that keeps both fragment reads conflict-free (row stride = 8 or 24 banks)
+constexpr int lx_pitch(int ntl) { return (ntl * 8) % 16 == 8 ? ntl * 8 : ntl * 8 + 8; }
+
+template <int NTL, int KT>
+struct LxW {
+  float v[2][KT * 8][lx_pitch(NTL)];
+};
+
+template <int NTL, int KT>
+__device__ __forceinline__ void lx_load_w(LxW<NTL, KT>& ws, const float* __restrict__ w, int kin, int c) {
+  constexpr int WP = lx_pitch(NTL);
+  for (int i = threadIdx.x; i < KT * 8 * WP; i += blockDim.x) {
+    const int k = i / WP, cl = i % WP;
+    const float v = (k < kin && cl < c) ? __ldg(w + (int64_t)k * c + cl) * kLog2e : 0.f;
+    const float hi = tf32f(v);
+    ws.v[0][k][cl] = hi;
+    ws.v[1][k][cl] = tf32f(v - hi);
+  }
+}
+
+// bias * log2 e per owned class (8 j + 2 t + e); -inf masks the padding classes
+template <int NTL>
+__device__ __forceinline__ void lx_bias(float (&bv)[NTL][2], const float* __restrict__ bias, int c, int t) {
+#pragma unroll
+  for (int j = 0; j < NTL; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int cl = 8 * j + 2 * t + e;
+      bv[j][e] = cl < c ? (bias ? __ldg(bias + cl) * kLog2e : 0.f) : -INFINITY;
+    }
+}
+
+// logits (log2 units) of the staged 16-row tile, 3xTF32: acc[j] = rows g / g + 8, classes 8 j + 2 t (+1)
+template <int NTL, int KT>
+__device__ __forceinline__ void lx_logits(float (&acc)[NTL][4], uint32_t cur, uint32_t wh, uint32_t wl, int lane) {
+  constexpr int WP = lx_pitch(NTL);
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int j = 0; j < NTL; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+#pragma unroll
+  for (int kc = 0; kc < KT; ++kc) {
+    uint32_t a[4], ah[4], al[4];
+    ldm_a(a, cur, kc, lane);
+    split(a, ah, al);
+#pragma unroll
+    for (int j = 0; j < NTL; ++j) {
+      const uint32_t o0 = ((8 * kc + t) * WP + 8 * j + g) * 4, o1 = o0 + 4 * WP * 4;
+      const uint32_t h0 = lds32(wh + o0), h1 = lds32(wh + o1), l0 = lds32(wl + o0), l1 = lds32(wl + o1);
+      mma(acc[j], al, h0, h1);
+      mma(acc[j], ah, l0, l1);
+      mma(acc[j], ah, h0, h1);
+    }
+  }
+}
+
+// adds the bias to row half h (rows g / g + 8) and returns its log2-sum-exp2 (quad-wide)
+template <int NTL>
+__device__ __forceinline__ float lx_lse(float (&v)[NTL][4], const float (&bv)[NTL][2], int h) {
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < NTL; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      v[j][2 * h + e] += bv[j][e];
+      mx = fmaxf(mx, v[j][2 * h + e]);
+    }
+  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+  float sm = 0.f;
+#pragma unroll
+  for (int j = 0; j < NTL; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) sm += ex2(v[j][2 * h + e] - mx);
+  sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+  sm += __shfl_xor_sync(0xffffffffu, sm, 2);
+  return mx + lg2(sm);
+}
+
+// labels of rows g, g + 8 of a tile (0 past n), loaded one tile ahead
+__device__ __forceinline__ void lx_labels(int64_t (&lab)[2], const int64_t* __restrict__ labels, int64_t n,
+                                          int64_t tile, int64_t tiles, int g) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t row = tile * 16 + g + 8 * h;
+    lab[h] = (tile < tiles && row < n) ? __ldg(labels + row) : 0;
+  }
+}
+
+template <int NTL, int KT>
+__global__ void __launch_bounds__(WPC * 32, 4) linear_xent(const float* __restrict__ x, int64_t ldx, int64_t n,
+                                                         int kin, const float* __restrict__ w, int c,
+                                                         const float* __restrict__ bias,
+                                                         const int64_t* __restrict__ labels, float inv_div,
+                                                         float* __restrict__ dl, int64_t ldd,
+                                                         float* __restrict__ lpart) {
+  constexpr int RD = 3;
+  __shared__ __align__(128) unsigned char sm[WPC][RD][2048];
+  __shared__ LxW<NTL, KT> ws;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t gw = (int64_t)blockIdx.x * WPC + wid, nw = (int64_t)gridDim.x * WPC;
+  const int64_t tiles = (n + 15) / 16;
+  const uint32_t tb = su(&sm[wid][0][0]);
+  int64_t tile = gw;
+#pragma unroll
+  for (int i = 0; i < RD - 1; ++i) {
+    if (tile + i * nw < tiles) stage_rows_k<KT>(tb + 2048 * i, x, ldx, n, kin, (tile + i * nw) * 16, lane);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  lx_load_w(ws, w, kin, c);
+  float bv[NTL][2];
+  lx_bias(bv, bias, c, t);
+  int64_t lab[2];
+  lx_labels(lab, labels, n, tile, tiles, g);
+  __syncthreads();
+  const uint32_t wh = su(&ws.v[0][0][0]), wl = su(&ws.v[1][0][0]);
+  float wsum = 0.f;  // this warp's loss, in row order
+  const float bad = __int_as_float(0x7fc00000);
+  for (int it = 0; tile < tiles; tile += nw, ++it) {
+    const uint32_t cur = tb + 2048 * (it % RD);
+    const int64_t ahead = tile + (RD - 1) * nw;
+    if (ahead < tiles) stage_rows_k<KT>(tb + 2048 * ((it + RD - 1) % RD), x, ldx, n, kin, ahead * 16, lane);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    int64_t labn[2];
+    lx_labels(labn, labels, n, tile + nw, tiles, g);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(RD - 1) : "memory");
+    __syncwarp();
+    float v[NTL][4];
+    lx_logits<NTL, KT>(v, cur, wh, wl, lane);
+    __syncwarp();  // the staging slot is refilled after every lane's ldmatrix
+    float tsum = 0.f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // rows g, g + 8 of the tile; the quad holds the row
+      const int64_t row = tile * 16 + g + 8 * h;
+      const float lse = lx_lse(v, bv, h);
+      const bool ok = lab[h] >= 0 && lab[h] < c;
+      float ly = 0.f;  // the label's logit (held by one lane of the quad)
+#pragma unroll
+      for (int j = 0; j < NTL; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (8 * j + 2 * t + e == lab[h]) ly = v[j][2 * h + e];
+      ly += __shfl_xor_sync(0xffffffffu, ly, 1);
+      ly += __shfl_xor_sync(0xffffffffu, ly, 2);
+      if (dl && row < n) {  // dl null: the loss only (the backward recomputes)
+        float* dr = dl + row * ldd;
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) {
+          const int cl = 8 * j + 2 * t;
+          float d[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            d[e] = ok ? (ex2(v[j][2 * h + e] - lse) - (cl + e == lab[h] ? 1.f : 0.f)) * inv_div : bad;
+          if (cl + 1 < c && (ldd % 2) == 0) *reinterpret_cast<float2*>(dr + cl) = make_float2(d[0], d[1]);
+          else {
+            if (cl < c) dr[cl] = d[0];
+            if (cl + 1 < c) dr[cl + 1] = d[1];
+          }
+        }
+      }
+      const float lrow = row < n ? (ok ? (lse - ly) * kLn2 : bad) : 0.f;
+      tsum += (t == 0) ? lrow : 0.f;  // rows g (h = 0) then g + 8 (h = 1)
+    }
+    // tile sum over g in a fixed tree order (lanes t = 0 hold the values)
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+    wsum += tsum;
+    lab[0] = labn[0];
+    lab[1] = labn[1];
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  if (lane == 0) lpart[gw] = wsum;
+}
+
+// The backward of linear_xent, recomputing instead of storing dlogits: per
+// 16-row tile the logits again (3xTF32), d = (softmax - onehot) * g / div in
+// registers, dx = d W^T (mma, the class index permuted so the accumulator
+// layout is the A fragment: k-slot t <-> class 2t, t + 4 <-> 2t + 1), and the
+// warp's running dW += x^T d (d through shared memory: its rows must move from
+// the g to the t lane index) and db += colsum d. Per CTA partials
+// [kin x c | c] in fixed warp order; sum_slabs finishes (deterministic).
+template <int NTL, int KT>
+__global__ void __launch_bounds__(WPC * 32, 3) linear_xent_bwd(
+    const float* __restrict__ x, int64_t ldx, int64_t n, int kin, const float* __restrict__ w, int c,
+    const float* __restrict__ bias, const int64_t* __restrict__ labels, const float* __restrict__ gscale,
+    float inv_div, float* __restrict__ dx, int64_t lddx, float* __restrict__ part) {
+  constexpr int RD = 2, WP = lx_pitch(NTL), MT = KT / 2, PW = KT * 8 * NTL * 8 + NTL * 8;
+  constexpr int RING = WPC * RD * 2048, DSM = WPC * 16 * WP * 4, RED = WPC * PW * 4;
+  constexpr int UNI = (RING + DSM) > RED ? (RING + DSM) : RED;
+  __shared__ __align__(128) unsigned char smu[UNI];
+  __shared__ LxW<NTL, KT> ws;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t gw = (int64_t)blockIdx.x * WPC + wid, nw = (int64_t)gridDim.x * WPC;
+  const int64_t tiles = (n + 15) / 16;
+  const uint32_t tb = su(smu + wid * RD * 2048);
+  int64_t tile = gw;
+#pragma unroll
+  for (int i = 0; i < RD - 1; ++i) {
+    if (tile + i * nw < tiles) stage_rows_k<KT>(tb + 2048 * i, x, ldx, n, kin, (tile + i * nw) * 16, lane);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  lx_load_w(ws, w, kin, c);
+  float bv[NTL][2];
+  lx_bias(bv, bias, c, t);
+  int64_t lab[2];
+  lx_labels(lab, labels, n, tile, tiles, g);
+  const float gs = (gscale ? __ldg(gscale) : 1.f) * inv_div;
+  __syncthreads();
+  float* dsm = reinterpret_cast<float*>(smu + RING) + wid * 16 * WP;
+  const uint32_t wh = su(&ws.v[0][0][0]), wl = su(&ws.v[1][0][0]);
+  float aw[MT][NTL][4] = {}, ab[NTL][2] = {};
+  const float bad = __int_as_float(0x7fc00000);
+  for (int it = 0; tile < tiles; tile += nw, ++it) {
+    const uint32_t cur = tb + 2048 * (it % RD);
+    const int64_t ahead = tile + (RD - 1) * nw;
+    if (ahead < tiles) stage_rows_k<KT>(tb + 2048 * ((it + RD - 1) % RD), x, ldx, n, kin, ahead * 16, lane);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    int64_t labn[2];
+    lx_labels(labn, labels, n, tile + nw, tiles, g);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(RD - 1) : "memory");
+    __syncwarp();
+    float d[NTL][4];
+    lx_logits<NTL, KT>(d, cur, wh, wl, lane);
+    // d = (softmax - onehot) * g / div; 0 on padding rows and classes
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t row = tile * 16 + g + 8 * h;
+      const float lse = lx_lse(d, bv, h);
+      const bool in = row < n;
+      const bool ok = lab[h] >= 0 && lab[h] < c;
+#pragma unroll
+      for (int j = 0; j < NTL; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cl = 8 * j + 2 * t + e;
+          const float p = (ex2(d[j][2 * h + e] - lse) - (cl == lab[h] ? 1.f : 0.f)) * gs;
+          d[j][2 * h + e] = !in || cl >= c ? 0.f : (ok ? p : bad);
+        }
+    }
+    lab[0] = labn[0];
+    lab[1] = labn[1];
+    // dx = d W^T
+    if (dx) {
+      float ax[KT][4] = {};
+#pragma unroll
+      for (int j = 0; j < NTL; ++j) {
+        const uint32_t a[4] = {__float_as_uint(d[j][0]), __float_as_uint(d[j][2]), __float_as_uint(d[j][1]),
+                               __float_as_uint(d[j][3])};
+        uint32_t ah[4], al[4];
+        split(a, ah, al);
+#pragma unroll
+        for (int nf = 0; nf < KT; ++nf) {
+          const uint32_t o = ((8 * nf + g) * WP + 8 * j + 2 * t) * 4;
+          const uint2 h = lds64(wh + o), l = lds64(wl + o);
+          mma(ax[nf], al, h.x, h.y);
+          mma(ax[nf], ah, l.x, l.y);
+          mma(ax[nf], ah, h.x, h.y);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t row = tile * 16 + g + 8 * h;
+        if (row >= n) continue;
+#pragma unroll
+        for (int nf = 0; nf < KT; ++nf) {
+          const int f = 8 * nf + 2 * t;
+          float* dr = dx + row * lddx + f;
+          // the staged W carries log2 e
+          const float v0 = ax[nf][2 * h] * kLn2, v1 = ax[nf][2 * h + 1] * kLn2;
+          if (f + 1 < kin && (lddx % 2) == 0)
+            *reinterpret_cast<float2*>(dr) = make_float2(v0, v1);
+          else {
+            if (f < kin) dr[0] = v0;
+            if (f + 1 < kin) dr[1] = v1;
+          }
+        }
+      }
+    }
+    // db += colsum d; d to shared memory, rows on the t index for dW += x^T d
+#pragma unroll
+    for (int j = 0; j < NTL; ++j) {
+      ab[j][0] += d[j][0] + d[j][2];
+      ab[j][1] += d[j][1] + d[j][3];
+      *reinterpret_cast<float2*>(dsm + g * WP + 8 * j + 2 * t) = make_float2(d[j][0], d[j][1]);
+      *reinterpret_cast<float2*>(dsm + (g + 8) * WP + 8 * j + 2 * t) = make_float2(d[j][2], d[j][3]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const int r0 = 8 * kk + t, r1 = r0 + 4;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int f0 = 16 * mt + g, f1 = f0 + 8;
+        const uint32_t a[4] = {lds32(cur + sw(r0, f0 >> 2) + (f0 & 3) * 4),
+                               lds32(cur + sw(r0, f1 >> 2) + (f1 & 3) * 4),
+                               lds32(cur + sw(r1, f0 >> 2) + (f0 & 3) * 4),
+                               lds32(cur + sw(r1, f1 >> 2) + (f1 & 3) * 4)};
+        uint32_t ah[4], al[4];
+        split(a, ah, al);
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) {
+          const float b0 = dsm[r0 * WP + 8 * j + g], b1 = dsm[r1 * WP + 8 * j + g];
+          const uint32_t bh0 = tf32_rn(b0), bh1 = tf32_rn(b1);
+          const uint32_t bl0 = tf32_rn(b0 - __uint_as_float(bh0)), bl1 = tf32_rn(b1 - __uint_as_float(bh1));
+          mma(aw[mt][j], al, bh0, bh1);
+          mma(aw[mt][j], ah, bl0, bl1);
+          mma(aw[mt][j], ah, bh0, bh1);
+        }
+      }
+    }
+    __syncwarp();  // the x slot and dsm are rewritten next tile
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  // db over the 8 row groups (fixed order)
+#pragma unroll
+  for (int j = 0; j < NTL; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) ab[j][e] += __shfl_xor_sync(0xffffffffu, ab[j][e], o);
+  __syncthreads();  // the ring / dsm become the reduction area
+  float* red = reinterpret_cast<float*>(smu) + wid * PW;
+  const int kw = KT * 8, cw = NTL * 8;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int j = 0; j < NTL; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red[(16 * mt + g + 8 * (q >> 1)) * cw + 8 * j + 2 * t + (q & 1)] = aw[mt][j][q];
+  if (g == 0)
+#pragma unroll
+    for (int j = 0; j < NTL; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) red[kw * cw + 8 * j + 2 * t + e] = ab[j][e];
+  __syncthreads();
+  // CTA partial [kin x c | c], warps summed in order
+  const float* r = reinterpret_cast<const float*>(smu);
+  float* out = part + (int64_t)blockIdx.x * (kin * c + c);
+  for (int i = threadIdx.x; i < kin * c + c; i += WPC * 32) {
+    const int src = i < kin * c ? (i / c) * cw + i % c : kw * cw + (i - kin * c);
+    float v = 0.f;
+#pragma unroll
+    for (int q = 0; q < WPC; ++q) v += r[q * PW + src];
+    out[i] = v;
+  }
+}
+
+}  // namespace dm
+
+// one resident wave of persistent warps per kernel instantiation
+template <typename K>
+int64_t lx_wave(K kern) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, dm::WPC * 32, 0) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  return (int64_t)num_sms() * std::min(per_sm, 8);
+}
+
+// the per-warp loss partials / per-CTA gradient slabs the workspaces hold (the
+// grid never exceeds 8 CTAs per SM)
+int64_t linear_xent_parts(int64_t n) {
+  return std::min<int64_t>(((n + 15) / 16 + dm::WPC - 1) / dm::WPC, (int64_t)num_sms() * 8) * dm::WPC;
+}
+int64_t linear_xent_bwd_slabs(int64_t n) {
+  return std::min<int64_t>(((n + 15) / 16 + dm::WPC - 1) / dm::WPC, (int64_t)num_sms() * 8);
+}
+
+static bool lx_covered(const float* x, int64_t ldx, int64_t n, int kin, int c) {
+  static const bool off = std::getenv("TCG_NO_FUSED_XENT") != nullptr;
+  return !off && n >= 1 && kin >= 4 && kin <= 32 && kin % 4 == 0 && c >= 1 && c <= 48 &&
+         (reinterpret_cast<uintptr_t>(x) & 15) == 0 && ldx % 4 == 0;
+}
+
+// dispatch on (class tiles, kin <= 16); F(NV, KV) launches one instantiation
+#define TCG_LX_DISPATCH(F)                  \
+  switch ((c + 7) / 8) {                    \
+    case 1: if (kin <= 16) F(1, 2) else F(1, 4) break; \
+    case 2: if (kin <= 16) F(2, 2) else F(2, 4) break; \
+    case 3: if (kin <= 16) F(3, 2) else F(3, 4) break; \
+    case 4: if (kin <= 16) F(4, 2) else F(4, 4) break; \
+    case 5: if (kin <= 16) F(5, 2) else F(5, 4) break; \
+    case 6: if (kin <= 16) F(6, 2) else F(6, 4) break; \
+  }
+
+int linear_xent_bwd(const float* x, int64_t ldx, int64_t n, int kin, const float* w, int c, const float* bias,
+                    const int64_t* labels, const float* gscale, float inv_div, float* dx, int64_t lddx, float* part,
+                    int64_t* slabs, cudaStream_t s) {
+  if (!lx_covered(x, ldx, n, kin, c)) return 1;
+  int64_t blocks = linear_xent_bwd_slabs(n);
+#define TCG_LXB(NV, KV)                                                                                  \
+  {                                                                                                      \
+    static const int64_t wave = lx_wave(dm::linear_xent_bwd<NV, KV>);                                    \
+    blocks = std::min(blocks, wave);                                                                     \
+    dm::linear_xent_bwd<NV, KV><<<(unsigned)blocks, dm::WPC * 32, 0, s>>>(x, ldx, n, kin, w, c, bias,    \
+                                                                         labels, gscale, inv_div, dx,   \
+                                                                         lddx, part);                    \
+  }
+  TCG_LX_DISPATCH(TCG_LXB)
+#undef TCG_LXB
+  TCG_LAUNCHED("linear_xent_bwd");
+  *slabs = blocks;
+  return TCG_OK;
+}
+
+// loss = sum_rows NLL / div into lpart (one partial per warp of the grid, *nparts);
+// dl = dlogits / div (dl may be null). 1 = shape not covered.
+int linear_xent(const float* x, int64_t ldx, int64_t n, int kin, const float* w, int c, const float* bias,
+                const int64_t* labels, float inv_div, float* dl, int64_t ldd, float* lpart, int64_t cap_parts,
+                int64_t* nparts, cudaStream_t s) {
+  if (!lx_covered(x, ldx, n, kin, c)) return 1;
+  int64_t blocks = std::min(linear_xent_parts(n), cap_parts) / dm::WPC;
+  if (blocks < 1) return 1;
+#define TCG_LXF(NV, KV)                                                                                  \
+  {                                                                                                      \
+    static const int64_t wave = lx_wave(dm::linear_xent<NV, KV>);                                        \
+    blocks = std::min(blocks, wave);                                                                     \
+    dm::linear_xent<NV, KV><<<(unsigned)blocks, dm::WPC * 32, 0, s>>>(x, ldx, n, kin, w, c, bias, labels, \
+                                                                     inv_div, dl, ldd, lpart);          \
+  }
+  TCG_LX_DISPATCH(TCG_LXF)
+#undef TCG_LXF
+  TCG_LAUNCHED("linear_xent");
+  *nparts = blocks * dm::WPC;
+  return TCG_OK;
+}
+#undef TCG_LX_DISPATCH
 
 }  // namespace tcg

@@ -204,3 +204,98 @@ class Linear(nn.Module):
 
 def cross_entropy(logits, labels):
     return SoftmaxXentFn.apply(logits, labels)
+
+
+def linear_xent(x, w, bias, labels, div=None, grad=True):
+    """(sum NLL / div, dlogits = (softmax - onehot) / div or None) of logits =
+    x w + bias, fused (csrc/dense_mma.cu linear_xent; the logits never reach
+    memory), or None when the shape is outside the fused kernel's coverage."""
+    lib = _lib.load()
+    n, kin = x.shape
+    c = w.shape[1]
+    labels = _labels(labels, n, x.device)
+    div = n if div is None else int(div)
+    loss = torch.empty((), dtype=torch.float32, device=x.device)
+    dl = rows_empty(n, c, x.device) if grad else None
+    wsb = int(lib.tcg_linear_xent_workspace_bytes(n))
+    ws = torch.empty(max(wsb // 4, 1), dtype=torch.float32, device=x.device)
+    rc = lib.tcg_linear_xent(x.data_ptr(), x.stride(0), n, kin, w.data_ptr(), c, _p(bias),
+                             labels.data_ptr(), div, loss.data_ptr(), _p(dl),
+                             dl.stride(0) if grad else 0, ws.data_ptr(), wsb, _stream())
+    if rc == _lib.TCG_E_UNSUPPORTED:
+        return None
+    _lib.check(rc, "tcg_linear_xent")
+    return loss, dl
+
+
+def linear_xent_backward(x, w, bias, labels, div=None, grad_scale=None, need_dx=True):
+    """(dx, dw, db) of linear_xent's loss for an incoming gradient grad_scale
+    (device scalar), recomputing the logits (no stored dlogits); None outside
+    the fused coverage."""
+    lib = _lib.load()
+    n, kin = x.shape
+    c = w.shape[1]
+    labels = _labels(labels, n, x.device)
+    div = n if div is None else int(div)
+    dx = rows_empty(n, kin, x.device) if need_dx else None
+    dw = torch.empty((kin, c), dtype=torch.float32, device=x.device)
+    db = torch.empty(c, dtype=torch.float32, device=x.device) if bias is not None else None
+    gs = None if grad_scale is None else grad_scale.float().contiguous()
+    wsb = int(lib.tcg_linear_xent_backward_workspace_bytes(n, kin, c))
+    ws = torch.empty(max(wsb // 4, 1), dtype=torch.float32, device=x.device)
+    rc = lib.tcg_linear_xent_backward(x.data_ptr(), x.stride(0), n, kin, w.data_ptr(), c, _p(bias),
+                                      labels.data_ptr(), div, _p(gs), _p(dx),
+                                      dx.stride(0) if need_dx else 0, dw.data_ptr(), _p(db),
+                                      ws.data_ptr(), wsb, _stream())
+    if rc == _lib.TCG_E_UNSUPPORTED:
+        return None
+    _lib.check(rc, "tcg_linear_xent_backward")
+    return dx, dw, db
+
+
+class LinearXentFn(torch.autograd.Function):
+    """loss = sum_i NLL(x_i w + b, label_i) / div, the output layer and the loss
+    in one kernel; the backward recomputes the logits in the kernel that
+    produces dx, dw and db (no dlogits in memory). Shapes outside the fused
+    coverage run the two-kernel form (dense, then softmax_xent with dlogits
+    kept for the dense backward)."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, labels, div):
+        x = rows_ok(x)
+        w = w.contiguous()
+        n = x.shape[0]
+        labels = _labels(labels, n, x.device)
+        r = linear_xent(x, w, b, labels, div, grad=False)
+        ctx.dl = None
+        if r is None:  # outside the fused coverage: the two-kernel form, same maths
+            logits = dense(x, w, bias=b)
+            loss, dl = softmax_xent(logits, labels, grad=True)
+            if div != n:
+                loss, dl = loss * (n / div), dl * (n / div)
+            ctx.dl = dl
+        else:
+            loss = r[0]
+        ctx.div = div
+        ctx.has_b = b is not None
+        ctx.save_for_backward(x, w, b, labels)
+        return loss
+
+    @staticmethod
+    def backward(ctx, g):
+        x, w, b, labels = ctx.saved_tensors
+        need_dx = ctx.needs_input_grad[0]
+        if ctx.dl is None:
+            dx, dw, db = linear_xent_backward(x, w, b, labels, ctx.div, g, need_dx)
+            return dx, dw, db, None, None
+        dl = rows_empty(*ctx.dl.shape, ctx.dl.device)  # keeps the 16-B row stride
+        torch.mul(ctx.dl, g, out=dl)
+        dx = dense(dl, w, transposed=True) if need_dx else None
+        dw, db = gemm_tn(x, dl, colsum=ctx.has_b)
+        return dx, dw, db, None, None
+
+
+def linear_cross_entropy(x, weight, bias, labels, div=None):
+    """F.cross_entropy(x @ weight + bias, labels) (mean; sum / div with `div`)
+    with the output layer fused into the loss."""
+    return LinearXentFn.apply(x, weight, bias, labels, x.shape[0] if div is None else int(div))

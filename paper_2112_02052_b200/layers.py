@@ -38,7 +38,9 @@ from .dense import (  # noqa: F401  (re-exported)
     Linear,
     SoftmaxXentFn,
     colsum,
+    LinearXentFn,
     cross_entropy,
+    linear_cross_entropy,
     rows_empty,
     rows_ok,
 )
@@ -337,6 +339,20 @@ class GCNConv(nn.Module):
         h = DenseFn.apply(x, self.weight, None, False)
         return GcnAggregate.apply(h, self.bias, t, self.mode)
 
+    def loss(self, x, t: TiledGraph, labels, shard: Shard | None = None, key=None, div=None):
+        """cross_entropy(self(x, t), labels) (sum / div with `div`); aggregate-first,
+        the dense step runs inside the loss kernel (logits never stored)."""
+        if not self.aggregate_first:
+            logits = self(x, t, shard, key)
+            n = logits.shape[0]
+            ce = SoftmaxXentFn.apply(logits, labels)
+            return ce if div is None or div == n else ce * (n / div)
+        if shard is not None:
+            h = GcnAggShard.apply(x, None, shard, key, self.mode)
+        else:
+            h = GcnAggregate.apply(x, None, t, self.mode)
+        return linear_cross_entropy(h, self.weight, self.bias, labels, div)
+
 
 class AGNNConv(nn.Module):
     """TC-GNN AGNNConv: agnn_layer(t, X W) (kernels.py:586-601 + a linear map)."""
@@ -355,7 +371,8 @@ class AGNNConv(nn.Module):
 
 class GCN(nn.Module):
     """X -> GCNConv(F,h) -> ReLU -> GCNConv(h,C) -> logits (PAPER.md:684);
-    train with `cross_entropy` (log_softmax + NLL fused)."""
+    train with `GCN.loss` (the last dense step fused into the loss) or
+    `cross_entropy` of the logits."""
 
     def __init__(self, f_in, hidden, classes, mode="tf32", seed=3):
         super().__init__()
@@ -370,10 +387,23 @@ class GCN(nn.Module):
             x = x[r0:r1]
         return self.c2(F.relu(self.c1(x, t, shard, 1)), t, shard, 2)
 
+    def loss(self, x, t, labels, shard=None):
+        """Mean cross-entropy of the logits against labels (all N rows), the last
+        dense step fused into the loss; with a Shard, this rank's share (its
+        rows' NLL / N: the sum over ranks is the loss)."""
+        if shard is not None:
+            r0, r1 = shard.plan.my_rows
+            x, labels = x[r0:r1], labels[r0:r1]
+            div = shard.plan.num_nodes
+        else:
+            div = None
+        return self.c2.loss(F.relu(self.c1(x, t, shard, 1)), t, labels, shard, 2, div)
+
 
 class AGNN(nn.Module):
     """X -> Linear(F,h) -> ReLU -> L x AGNNConv(h,h) -> Linear(h,C) -> logits
-    (PAPER.md:688-689); train with `cross_entropy`."""
+    (PAPER.md:688-689); train with `AGNN.loss` (lin_out fused into the loss)
+    or `cross_entropy` of the logits."""
 
     def __init__(self, f_in, hidden, classes, layers=4, mode="tf32", seed=3):
         super().__init__()
@@ -391,6 +421,23 @@ class AGNN(nn.Module):
         for i, c in enumerate(self.convs):
             h = c(h, t, shard, i)
         return self.lin_out(h)
+
+    def loss(self, x, t, labels, shard=None):
+        """Mean cross-entropy of the logits against labels with lin_out fused
+        into the loss; with a Shard, this rank's share (see GCN.loss)."""
+        div = None
+        if shard is not None:
+            r0, r1 = shard.plan.my_rows
+            x, labels = x[r0:r1], labels[r0:r1]
+            div = shard.plan.num_nodes
+        h = self.lin_in(x)
+        for i, c in enumerate(self.convs):
+            h = c(h, t, shard, i)
+        lo = self.lin_out
+        if lo.relu:
+            return cross_entropy(lo(h), labels) if div is None else \
+                SoftmaxXentFn.apply(lo(h), labels) * (h.shape[0] / div)
+        return linear_cross_entropy(h, lo.weight, lo.bias, labels, div)
 
 
 def cross_entropy_sharded(logits_local, labels, shard: Shard):

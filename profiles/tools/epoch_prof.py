@@ -16,7 +16,7 @@ net = (layers.AGNN(feats, 32, classes, layers=4) if kind == "agnn" else layers.G
 opt = torch.optim.Adam(net.parameters(), lr=0.01, capturable=True, fused=True)
 def step():
     opt.zero_grad(set_to_none=True)
-    lo = layers.cross_entropy(net(x, t), y); lo.backward(); opt.step()
+    lo = net.loss(x, t, y); lo.backward(); opt.step()
 for _ in range(3): step()
 torch.cuda.synchronize()
 torch.cuda.profiler.start(); step(); torch.cuda.synchronize(); torch.cuda.profiler.stop()

@@ -128,6 +128,56 @@ def test_softmax_xent(env):
     assert rel_l2(lt.grad.cpu().numpy(), 3.0 * lg.grad.cpu().numpy()) < 1e-5
 
 
+@pytest.mark.parametrize("n,kin,c", [(169343, 32, 40), (1000, 16, 47), (37, 32, 1), (50, 20, 9),
+                                     (5003, 32, 48), (100, 12, 7), (16, 4, 2), (1, 32, 40),
+                                     (700, 64, 40), (300, 32, 64), (200, 30, 10)])
+def test_linear_xent(env, n, kin, c):
+    """Output layer fused with the loss (and the two-kernel form for the shapes
+    the fused kernel declines: kin 64, c 64, kin not a multiple of 4) against
+    float64 torch: loss, dx, dW, db; bitwise deterministic."""
+    _, dense, _, torch = env
+    gen = torch.Generator(device="cuda").manual_seed(n + kin + c)
+    x = torch.randn(n, kin, device="cuda", generator=gen)
+    w = torch.randn(kin, c, device="cuda", generator=gen) / kin ** 0.5 * 3
+    b = torch.randn(c, device="cuda", generator=gen)
+    labels = torch.randint(0, c, (n,), device="cuda", generator=gen)
+    fused = dense.linear_xent(x, w, b, labels)
+    assert (fused is None) == (kin > 32 or kin % 4 != 0 or c > 48)
+    xd, wd, bd = (v.double().requires_grad_(True) for v in (x, w, b))
+    ref = torch.nn.functional.cross_entropy(xd @ wd + bd, labels)
+    ref.backward()
+    tol = 2e-6
+    for div in (None, 3 * n):
+        xs, ws, bs = (v.clone().requires_grad_(True) for v in (x, w, b))
+        loss = dense.linear_cross_entropy(xs, ws, bs, labels, div)
+        (2.0 * loss).backward()
+        sc = 1.0 if div is None else n / div
+        assert abs(float(loss) - sc * float(ref)) <= tol * max(1.0, abs(float(ref)))
+        for got, want in ((xs.grad, xd.grad), (ws.grad, wd.grad), (bs.grad, bd.grad)):
+            assert rel_l2(got.cpu().numpy(), 2.0 * sc * want.cpu().numpy()) < tol
+    if fused is not None:
+        loss, dl = fused
+        again = dense.linear_xent(x, w, b, labels)
+        assert torch.equal(loss, again[0]) and torch.equal(dl, again[1])
+        lg = (xd @ wd + bd).detach().requires_grad_(True)
+        torch.nn.functional.cross_entropy(lg, labels).backward()
+        assert rel_l2(dl.cpu().numpy(), lg.grad.cpu().numpy()) < tol
+        # a label outside [0, c) poisons the loss and its row
+        bad = labels.clone()
+        bad[n // 2] = c
+        lb, db_ = dense.linear_xent(x, w, b, bad)
+        assert torch.isnan(lb) and torch.isnan(db_[n // 2]).all()
+        assert not torch.isnan(db_[:n // 2]).any()
+        # the backward alone: no bias, no dx, a device grad scale; deterministic
+        gsc = torch.tensor(0.5, device="cuda")
+        dx0, dw0, db0 = dense.linear_xent_backward(x, w, None, labels, None, gsc, need_dx=False)
+        assert dx0 is None and db0 is None
+        wd2 = w.double().requires_grad_(True)
+        torch.nn.functional.cross_entropy(x.double() @ wd2, labels).backward()
+        assert rel_l2(dw0.cpu().numpy(), 0.5 * wd2.grad.cpu().numpy()) < tol
+        assert torch.equal(dw0, dense.linear_xent_backward(x, w, None, labels, None, gsc, False)[1])
+
+
 def _copy_weights_agnn(net, cpu):
     cpu.w_in[...] = net.lin_in.weight.detach().cpu().numpy()
     cpu.b_in[...] = net.lin_in.bias.detach().cpu().numpy()
@@ -137,7 +187,8 @@ def _copy_weights_agnn(net, cpu):
     cpu.b_out[...] = net.lin_out.bias.detach().cpu().numpy()
 
 
-def test_agnn_train_step_vs_oracle(env, oracle):
+@pytest.mark.parametrize("fused", [False, True])
+def test_agnn_train_step_vs_oracle(env, oracle, fused):
     tcg, _, layers, torch = env
     n, f, h, c = 3000, 64, 32, 10
     g = tcg.synth.gen_uniform(n, 6, 5)
@@ -148,8 +199,8 @@ def test_agnn_train_step_vs_oracle(env, oracle):
     cpu = oracle.AgnnModelCPU(f, h, c, layers=2)
     _copy_weights_agnn(net, cpu)
     params0 = [p.copy() for p in cpu.params]
-    loss = layers.cross_entropy(net(torch.from_numpy(x).cuda(), t),
-                                torch.from_numpy(lab).cuda())
+    xg, lg = torch.from_numpy(x).cuda(), torch.from_numpy(lab).cuda()
+    loss = net.loss(xg, t, lg) if fused else layers.cross_entropy(net(xg, t), lg)
     loss.backward()
     cpu_loss = cpu.epoch(g.node_pointer, g.edge_list, x, lab, mode="tf32")
     assert abs(float(loss) - cpu_loss) <= TF32_REL_L2 * abs(cpu_loss)
@@ -164,7 +215,8 @@ def test_agnn_train_step_vs_oracle(env, oracle):
     assert all(not np.array_equal(a, b) for a, b in zip(params0, cpu.params))
 
 
-def test_gcn_train_step_vs_oracle(env, oracle):
+@pytest.mark.parametrize("fused", [False, True])
+def test_gcn_train_step_vs_oracle(env, oracle, fused):
     tcg, _, layers, torch = env
     n, f, h, c = 2000, 100, 16, 7
     g = tcg.synth.gen_uniform(n, 5, 8)
@@ -175,7 +227,8 @@ def test_gcn_train_step_vs_oracle(env, oracle):
     cpu = oracle.GcnModelCPU(f, h, c)
     cpu.w1[...] = net.c1.weight.detach().cpu().numpy()
     cpu.w2[...] = net.c2.weight.detach().cpu().numpy()
-    loss = layers.cross_entropy(net(torch.from_numpy(x).cuda(), t), torch.from_numpy(lab).cuda())
+    xg, lg = torch.from_numpy(x).cuda(), torch.from_numpy(lab).cuda()
+    loss = net.loss(xg, t, lg) if fused else layers.cross_entropy(net(xg, t), lg)
     loss.backward()
     cpu_loss = cpu.epoch(g.node_pointer, g.edge_list, x, lab, mode="tf32")
     assert abs(float(loss) - cpu_loss) <= TF32_REL_L2 * abs(cpu_loss)

@@ -68,7 +68,9 @@ def _worker(rank, world, port, out_dir):
                 loss.backward()
                 lv = float(loss)
             else:
-                loss = layers.cross_entropy_sharded(net(x, t, sh), lab, sh)
+                # logits + sharded loss, and the output layer fused into the loss
+                loss = (layers.cross_entropy_sharded(net(x, t, sh), lab, sh) if kind == "gcn"
+                        else net.loss(x, t, lab, sh))
                 loss.backward()
                 sh.allreduce_grads(net.parameters())
                 lt = loss.detach().cpu().reshape(1)
@@ -147,7 +149,7 @@ for kind in ("agnn", "gcn"):
 
     def step():
         opt.zero_grad(set_to_none=False)
-        lo = layers.cross_entropy_sharded(net(x, t, shard), y, shard)
+        lo = net.loss(x, t, y, shard)
         lo.backward()
         shard.allreduce_grads(net.parameters())
         opt.step()
