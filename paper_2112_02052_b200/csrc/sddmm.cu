@@ -160,8 +160,8 @@ extern "C" int tcg_sddmm(const tcg_tiling* t, const float* xa, int64_t lda, cons
   TCG_REQUIRE(t->edge_frag, "tcg_sddmm: tf32 needs edge_frag (tcg_edge_frag)");
   {
     static const bool no_stream = std::getenv("TCG_NO_STREAM") != nullptr;
-    if (!no_stream && dim == 32) {
-      const int rc = stream_sddmm(t, xa, lda, xb, ldb, aux, out, epilogue, win_begin, win_end, s);
+    if (!no_stream && dim <= 32 && dim % 4 == 0) {
+      const int rc = stream_sddmm(t, (int)dim, xa, lda, xb, ldb, aux, out, epilogue, win_begin, win_end, s);
       if (rc != TCG_E_UNSUPPORTED) return rc;
     }
   }
@@ -214,8 +214,9 @@ extern "C" int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz
               "tcg_agnn_forward: y_row0 %lld beyond first output row", (long long)y_row0);
   const int nt = win::nt_for(dim);
   static const bool no_stream = std::getenv("TCG_NO_STREAM") != nullptr;
-  if (!no_stream && dim == 32 && t->num_edges > 0 && win_begin < win_end && z && p && y) {
-    const int rc = stream_agnn(t, false, z, ldz, z, ldz, nullptr, 0, nullptr, p, y, ldy, y_row0,
+  if (!no_stream && dim <= 32 && dim % 4 == 0 && t->num_edges > 0 && win_begin < win_end && z && p &&
+      y) {
+    const int rc = stream_agnn(t, false, (int)dim, z, ldz, z, ldz, nullptr, 0, nullptr, p, y, ldy, y_row0,
                                win_begin, win_end, as_stream(stream));
     if (rc != TCG_E_UNSUPPORTED) return rc;
   }
@@ -266,9 +267,9 @@ extern "C" int tcg_agnn_backward_fused(const tcg_tiling* t, const float* z, int6
               "tcg_agnn_backward_fused: dz_row0 %lld beyond first output row",
               (long long)dz_row0);
   static const bool no_stream = std::getenv("TCG_NO_STREAM") != nullptr;
-  if (!no_stream && dim == 32 && t->num_edges > 0 && win_begin < win_end) {
+  if (!no_stream && dim <= 32 && dim % 4 == 0 && t->num_edges > 0 && win_begin < win_end) {
     TCG_REQUIRE(z && gy && y_fwd && p && ds && dz, "tcg_agnn_backward_fused: null pointer");
-    const int rc = stream_agnn(t, true, z, ldz, gy, ldg, y_fwd, ld_yfwd, p, ds, dz, lddz, dz_row0,
+    const int rc = stream_agnn(t, true, (int)dim, z, ldz, gy, ldg, y_fwd, ld_yfwd, p, ds, dz, lddz, dz_row0,
                                win_begin, win_end, as_stream(stream));
     if (rc != TCG_E_UNSUPPORTED) {
       if (rc != TCG_OK || !ds_t || !inv_perm) return rc;

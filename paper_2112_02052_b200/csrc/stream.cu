@@ -880,6 +880,7 @@ struct AgnnArgs {
   float* y;          // fwd: Y, bwd: dZ (A-side)
   int64_t ldy, y_row0;
   int epi;           // SDDMM-only launches: TCG_EPI_*
+  int dv;            // MASK launches: valid features (a multiple of 4, < 32); the rest read as 0
 };
 
 constexpr float kTau = 8.f;  // lazy-rescale threshold of the online softmax (natural log)
@@ -915,7 +916,10 @@ __device__ __forceinline__ uint32_t agnn_off(int r, int c) {
   return r * 128 + ((c ^ h) & 7) * 16;
 }
 
-template <int KIND, bool PAIR = false>
+// MASK: D < 32 (a multiple of 4) run in the D = 32 layout with the missing
+// features zero-filled by the copies (src-size 0) and never stored: the scores,
+// softmax and products are those of the D-wide rows.
+template <int KIND, bool PAIR = false, bool MASK = false>
 __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const AgnnArgs a) {
   using C = AgnnCfg<KIND>;
   constexpr bool BWD = KIND == 1;   // 0: forward, 1: backward A-side, 2: SDDMM only
@@ -958,11 +962,18 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
   auto issue_idx = [&](int s) {
     if (lane < 2) cp_async<16>(iring + (s & (NI - 1)) * 32 + lane * 16, csw + 8 * (int64_t)s + 4 * lane);
   };
+  const int xvb = MASK ? (4 * g < a.dv ? 16 : 0) : 16;  // this lane's bytes of a row
   auto issue_x = [&](int s) {
     const uint2 id = *reinterpret_cast<const uint2*>(iring_p + (s & (NI - 1)) * 32 + 8 * t);
     const uint32_t sb = ring + (s & (NB - 1)) * 1024;
-    cp_async<16>(sb + so0, xb + (uint64_t)id.x * xrow);
-    cp_async<16>(sb + so1, xb + (uint64_t)id.y * xrow);
+    if constexpr (MASK) {
+      const void* z0 = a.z;  // any valid address when nothing is copied
+      cp_async_n<16>(sb + so0, xvb ? (const void*)(xb + (uint64_t)id.x * xrow) : z0, xvb);
+      cp_async_n<16>(sb + so1, xvb ? (const void*)(xb + (uint64_t)id.y * xrow) : z0, xvb);
+    } else {
+      cp_async<16>(sb + so0, xb + (uint64_t)id.x * xrow);
+      cp_async<16>(sb + so1, xb + (uint64_t)id.y * xrow);
+    }
   };
   for (int s = 0; s < NB; ++s) issue_idx(s);
   cp_commit();
@@ -986,7 +997,7 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
     for (int h = 0; h < 4; ++h) {
       const int64_t r = (int64_t)w * 16 + g + 8 * (h & 1);
       const int f = 4 * (t + 4 * (h >> 1));
-      const bool ok = w < a.win_end && r < a.n;
+      const bool ok = w < a.win_end && r < a.n && (!MASK || f < a.dv);
       o[h] = ok ? __ldg(reinterpret_cast<const float4*>(a.za + r * a.lda + f)) : make_float4(0.f, 0.f, 0.f, 0.f);
       if constexpr (BWD)
         yv[h] = ok ? __ldg(reinterpret_cast<const float4*>(a.yf + r * a.ldyf + f)) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1257,10 +1268,12 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
       const int64_t r = (int64_t)w * 16 + g + 8 * h;
       if (r >= a.n) continue;
       float4* yr = reinterpret_cast<float4*>(a.y + (r - a.y_row0) * a.ldy + 8 * t);
-      yr[0] = make_float4(acc[0][2 * h] * inv[h], acc[1][2 * h] * inv[h], acc[2][2 * h] * inv[h],
-                          acc[3][2 * h] * inv[h]);
-      yr[1] = make_float4(acc[0][2 * h + 1] * inv[h], acc[1][2 * h + 1] * inv[h],
-                          acc[2][2 * h + 1] * inv[h], acc[3][2 * h + 1] * inv[h]);
+      if (!MASK || 8 * t < a.dv)
+        yr[0] = make_float4(acc[0][2 * h] * inv[h], acc[1][2 * h] * inv[h], acc[2][2 * h] * inv[h],
+                            acc[3][2 * h] * inv[h]);
+      if (!MASK || 8 * t + 4 < a.dv)
+        yr[1] = make_float4(acc[0][2 * h + 1] * inv[h], acc[1][2 * h + 1] * inv[h],
+                            acc[2][2 * h + 1] * inv[h], acc[3][2 * h + 1] * inv[h]);
     }
     cb0 = cb1, cb1 = nb2, nb2 = nb3, nb3 = blk_of(w + 4);
     e0 = e1, e1 = e2, e2 = e3, e3 = ptr_of(w + 4);
@@ -1268,10 +1281,10 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
   cp_wait<0>();
 }
 
-template <int KIND, bool PAIR = false>
+template <int KIND, bool PAIR = false, bool MASK = false>
 int launch_agnn(AgnnArgs& a, cudaStream_t s) {
   using C = AgnnCfg<KIND>;
-  auto kern = agnn_stream<KIND, PAIR>;
+  auto kern = agnn_stream<KIND, PAIR, MASK>;
   static int configured = -1;
   int dev = 0;
   TCG_CUDA(cudaGetDevice(&dev), "agnn_stream device");
@@ -1476,10 +1489,11 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
 
 // Fused AGNN forward / backward on the block stream; TCG_E_UNSUPPORTED when
 // the shape does not fit (D != 32, misaligned, windows wider than the slot map).
-int stream_agnn(const tcg_tiling* t, bool bwd, const float* z, int64_t ldz, const float* za,
+int stream_agnn(const tcg_tiling* t, bool bwd, int dim, const float* z, int64_t ldz, const float* za,
                 int64_t lda, const float* yf, int64_t ldyf, const float* pin, float* eout,
                 float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
                 cudaStream_t s) {
+  if (dim < 4 || dim > 32 || dim % 4) return TCG_E_UNSUPPORTED;
   if (!t->block_offsets || !t->col_stream || !t->edge_frag) return TCG_E_UNSUPPORTED;
   if (t->max_window_edges <= 0 || t->max_window_edges > stream::kMaxE ||
       t->max_window_unique > 8 * stream::kMapB)
@@ -1493,21 +1507,26 @@ int stream_agnn(const tcg_tiling* t, bool bwd, const float* z, int64_t ldz, cons
   a.win_begin = (int)win_begin, a.win_end = (int)win_end;
   a.z = z, a.ldz = ldz, a.za = za, a.lda = lda, a.yf = yf, a.ldyf = ldyf, a.pin = pin;
   a.eout = eout, a.y = y, a.ldy = ldy, a.y_row0 = y_row0;
+  a.dv = dim;
+  const bool mk = dim < 32;
   static const bool pair_off = std::getenv("TCG_NO_PAIRS") != nullptr;
   // forward: two blocks per step (arxiv 59.4 -> 55.3 us cold); the backward
   // measured slower that way (55.3 -> 57.3 us with the coalesced dS writes,
   // 59.5 -> 63.5 us before) and keeps one block per step
   if (!bwd && t->pair_offsets && t->pair_stream && !pair_off) {
     a.boff = t->pair_offsets, a.cs = t->pair_stream;
-    return stream::launch_agnn<0, true>(a, s);
+    return mk ? stream::launch_agnn<0, true, true>(a, s) : stream::launch_agnn<0, true>(a, s);
   }
-  return bwd ? stream::launch_agnn<1>(a, s) : stream::launch_agnn<0>(a, s);
+  if (bwd) return mk ? stream::launch_agnn<1, false, true>(a, s) : stream::launch_agnn<1>(a, s);
+  return mk ? stream::launch_agnn<0, false, true>(a, s) : stream::launch_agnn<0>(a, s);
 }
 
-// SDDMM (+ softmax / softmax-backward row epilogue) on the block stream, D = 32
-int stream_sddmm(const tcg_tiling* t, const float* xa, int64_t lda, const float* xb, int64_t ldb,
+// SDDMM (+ softmax / softmax-backward row epilogue) on the block stream, D <= 32
+// (a multiple of 4; D < 32 runs masked)
+int stream_sddmm(const tcg_tiling* t, int dim, const float* xa, int64_t lda, const float* xb, int64_t ldb,
                  const float* aux, float* out, int epi, int64_t win_begin, int64_t win_end,
                  cudaStream_t s) {
+  if (dim < 4 || dim > 32 || dim % 4) return TCG_E_UNSUPPORTED;
   if (!t->block_offsets || !t->col_stream || !t->edge_frag) return TCG_E_UNSUPPORTED;
   if (t->max_window_edges <= 0 || t->max_window_edges > stream::kMaxE ||
       t->max_window_unique > 8 * stream::kMapB)
@@ -1520,12 +1539,14 @@ int stream_sddmm(const tcg_tiling* t, const float* xa, int64_t lda, const float*
   a.n = t->num_nodes;
   a.win_begin = (int)win_begin, a.win_end = (int)win_end;
   a.z = xb, a.ldz = ldb, a.za = xa, a.lda = lda, a.pin = aux, a.eout = out, a.epi = epi;
+  a.dv = dim;
+  const bool mk = dim < 32;
   static const bool pair_off = std::getenv("TCG_NO_PAIRS") != nullptr;
   if (t->pair_offsets && t->pair_stream && !pair_off) {
     a.boff = t->pair_offsets, a.cs = t->pair_stream;
-    return stream::launch_agnn<2, true>(a, s);
+    return mk ? stream::launch_agnn<2, true, true>(a, s) : stream::launch_agnn<2, true>(a, s);
   }
-  return stream::launch_agnn<2>(a, s);
+  return mk ? stream::launch_agnn<2, false, true>(a, s) : stream::launch_agnn<2>(a, s);
 }
 
 }  // namespace tcg

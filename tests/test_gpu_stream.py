@@ -2,7 +2,7 @@
 
 The stream engine takes every TF32 SpMM whose feature chunks are multiples of
 8 (NT = 4 / 2 / 1 launches), the dual A^T form of the AGNN backward, and the
-fused AGNN forward / one-pass backward at D = 32. These cases pin it: chunk
+fused AGNN forward / one-pass backward / SDDMM at D <= 32 (multiples of 4). These cases pin it: chunk
 splits (8 ... 128 features), bias / accumulate / shard row offsets, graphs
 with hub windows (> 16 blocks: the fragment re-load path; > 255 edges: the
 fused kernels hand over to the window engine), empty windows, the block
@@ -274,6 +274,54 @@ def test_stream_sddmm_epilogues(env, oracle, kind):
                               aux=torch.from_numpy(p_ref).cuda())
     ds_ref = oracle.softmax_backward(p_ref, s_ref, ptr)
     assert rel_l2(ds.cpu().numpy(), ds_ref) <= TF32_REL_L2
+
+
+def _kernel_names(torch, fn):
+    from torch.profiler import ProfilerActivity, profile
+
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    return {e.name for e in prof.events()}
+
+
+@pytest.mark.parametrize("dim", [4, 8, 16, 20, 28])
+@pytest.mark.parametrize("kind", ["uniform", "hub"])
+def test_stream_agnn_masked_dims(env, oracle, dim, kind):
+    """D < 32 (multiples of 4) on the fused AGNN / SDDMM kernels: the D = 32
+    layout with the missing features zero-filled by the copies and never
+    stored. Forward, one-pass backward and the SDDMM epilogues against the
+    oracle; the launches are the stream kernels (not the window engine)."""
+    tcg, kernels, layers, torch = env
+    from paper_2112_02052_b200 import _lib
+
+    g = _graph(tcg, kind, 3000, 7, 30 + dim)
+    t = tcg.translate(g, tcg.BlockConfig())
+    rng = np.random.default_rng(dim)
+    z = rng.standard_normal((g.num_nodes, dim)).astype(np.float32)
+    gy = rng.standard_normal((g.num_nodes, dim)).astype(np.float32)
+    ptr, cols = g.node_pointer, g.edge_list
+    zt, gyt = torch.from_numpy(z).cuda(), torch.from_numpy(gy).cuda()
+    res = {}
+    names = _kernel_names(torch, lambda: res.update(fwd=kernels.agnn_forward_device(t, zt)))
+    y, p = res["fwd"]
+    if kind == "uniform":  # the hub graph's > 255-edge windows go to the window engine
+        assert any("agnn_stream" in n for n in names), names
+    p_ref = oracle.segment_softmax(oracle.sddmm(ptr, cols, z), ptr)
+    assert rel_l2(p.cpu().numpy()[: g.num_edges], p_ref) <= TF32_REL_L2
+    assert rel_l2(y.cpu().numpy(), oracle.spmm(ptr, cols, z, f=p_ref)) <= TF32_REL_L2
+    dz_a, ds = kernels.agnn_backward_device(t, zt, gyt, p, y_fwd=y)
+    ds_ref = oracle.softmax_backward(p_ref, oracle.sddmm(ptr, cols, gy, z), ptr)
+    assert rel_l2(ds.cpu().numpy()[: g.num_edges], ds_ref) <= TF32_REL_L2
+    assert rel_l2(dz_a.cpu().numpy(), oracle.spmm(ptr, cols, z, f=ds_ref)) <= TF32_REL_L2
+    zg = zt.clone().requires_grad_(True)
+    layers.AgnnAggregate.apply(zg, t, "tf32").backward(gyt)
+    assert rel_l2(zg.grad.cpu().numpy(), oracle.agnn_backward(ptr, cols, z, p_ref, gy)) <= TF32_REL_L2
+    s = kernels.sddmm_device(t, zt, gyt)
+    s_ref = oracle.sddmm(ptr, cols, z, gy)
+    assert rel_l2(s.cpu().numpy(), s_ref) <= TF32_REL_L2
+    ps = kernels.sddmm_device(t, zt, epilogue=_lib.EPI_SOFTMAX)
+    assert rel_l2(ps.cpu().numpy(), p_ref) <= TF32_REL_L2
 
 
 @pytest.mark.parametrize("dim", [16, 32, 40, 47])
