@@ -140,8 +140,8 @@ __global__ void __launch_bounds__(256)
 }
 
 // Fixed-order sum of the slab partials.
-// 32 outputs per CTA x 8 summers: summer j adds slabs j, j+8, ... in order,
-// then the 8 partial sums are combined in a fixed order (deterministic).
+// 32 outputs per CTA x 32 summers: summer j adds slabs j, j+32, ... in a fixed
+// order, then the 32 partial sums are combined in a fixed order (deterministic).
 // (outputs from `split` on go to out2: the dW | db partials of one slab)
 __global__ void __launch_bounds__(1024) sum_slabs(const float* __restrict__ part, int slabs,
                                                   int64_t len, float* __restrict__ out,
@@ -152,15 +152,21 @@ __global__ void __launch_bounds__(1024) sum_slabs(const float* __restrict__ part
   __shared__ float sh[32][33];
   const int o = threadIdx.x & 31, j = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * 32 + o;
-  // 8 independent partials: a slab group's loads are all in flight at once
+  // up to 24 loads per thread issued as one batch (one L2 round trip for the
+  // usual <= 768 slabs), folded into 8 partials in a fixed order
+  constexpr int U = 24;
   float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (i < len) {
-    int q = j;
-    for (; q + 7 * 32 < slabs; q += 8 * 32) {
+    for (int q0 = j; q0 < slabs; q0 += 32 * U) {
+      float v[U];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) sp[u] += part[(int64_t)(q + 32 * u) * len + i];
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + 32 * u;
+        v[u] = q < slabs ? __ldg(part + (int64_t)q * len + i) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) sp[u & 7] += v[u];
     }
-    for (; q < slabs; q += 32) sp[0] += part[(int64_t)q * len + i];
   }
   sh[j][o] = ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
   __syncthreads();
@@ -478,6 +484,9 @@ int linear_xent(const float* x, int64_t ldx, int64_t n, int kin, const float* w,
                 const int64_t* labels, float inv_div, float* dl, int64_t ldd, float* lpart, int64_t cap_parts,
                 int64_t* nparts, cudaStream_t s);
 int64_t linear_xent_parts(int64_t n);
+int gemm_tn_mma(const float* a, int64_t lda, const float* b, int64_t ldb, const float* mask, int64_t ldm,
+                int64_t n, int k, int c, float* part, float* colpart, int64_t cap_slabs, int64_t* used,
+                cudaStream_t s);
 int64_t linear_xent_bwd_slabs(int64_t n);
 int linear_xent_bwd(const float* x, int64_t ldx, int64_t n, int kin, const float* w, int c, const float* bias,
                     const int64_t* labels, const float* gscale, float inv_div, float* dx, int64_t lddx, float* part,
@@ -542,8 +551,13 @@ extern "C" int tcg_gemm_tn(const float* a, int64_t lda, const float* b, int64_t 
   }
   {
     int64_t used = 0;
-    const int rc = fast_gemm_tn(a, lda, b, ldb, mask, ldm, n, (int)k, (int)c, part,
-                                colsum ? colpart : nullptr, slabs, &used, s);
+    // the wide input layers (k 33..128 -> 16 / 32) on the tensor cores (3xTF32),
+    // then the FFMA2 tile kernels
+    int rc = gemm_tn_mma(a, lda, b, ldb, mask, ldm, n, (int)k, (int)c, part, colsum ? colpart : nullptr,
+                         slabs, &used, s);
+    if (rc == 1)
+      rc = fast_gemm_tn(a, lda, b, ldb, mask, ldm, n, (int)k, (int)c, part, colsum ? colpart : nullptr,
+                        slabs, &used, s);
     if (rc == TCG_OK) {
       sum_slabs<<<(unsigned)((k * c + 31) / 32), 1024, 0, s>>>(part, (int)used, k * c, out);
       TCG_LAUNCHED("sum_slabs");

@@ -722,6 +722,139 @@ __global__ void __launch_bounds__(WPC * 32, 3) linear_xent_bwd(
   }
 }
 
+
+// ---- weight gradients of the wide input layers: dW = A^T (B .* [M > 0]) --------
+//
+// A [n x k] (k <= 128, a multiple of 4), B / M [n x CO] (CO 16 or 32): one CTA of
+// 8 warps per 32-row chunk, warp w owning features 16 w .. 16 w + 15 (the M
+// dimension of m16n8k8, with the chunk's rows as K), 3xTF32. A, B and M stream
+// through a 3-stage cp.async ring shared by the CTA (A rows padded to 136
+// floats: the t / t + 4 row reads land 8 banks apart). Per-CTA partials of dW
+// and of the column sums of B .* [M > 0]; sum_slabs finishes (deterministic).
+namespace gt {
+constexpr int R = 32, S = 3, AP = 136;
+template <int CO>
+struct Smem {
+  static constexpr int BP = CO + 8;
+  float a[S][R][AP];
+  float b[S][R][BP];
+  float m[S][R][BP];
+  float bh[R][BP], bl[R][BP];  // the chunk's B .* [M > 0], tf32 hi / lo (split once per CTA)
+  float cs[256 / CO][CO];      // column-sum partials per row residue
+};
+}  // namespace gt
+
+template <int CO>
+__global__ void __launch_bounds__(256, 2) gemm_tn_mma(const float* __restrict__ a, int64_t lda,
+                                                       const float* __restrict__ b, int64_t ldb,
+                                                       const float* __restrict__ mk, int64_t ldm, int64_t n,
+                                                       int k, float* __restrict__ part,
+                                                       float* __restrict__ colpart) {
+  using namespace gt;
+  using Sm = Smem<CO>;
+  constexpr int BP = Sm::BP, NJ = CO / 8;
+  extern __shared__ __align__(128) unsigned char gsm[];
+  Sm& sm = *reinterpret_cast<Sm*>(gsm);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t chunks = (n + R - 1) / R;
+  const int kc = k / 4;  // 16-B chunks per A row
+  auto stage = [&](int slot, int64_t ch) {
+    const int64_t r0 = ch * R;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // A: 32 rows x 32 chunks
+      const int q = tid + 256 * i, r = q >> 5, c = q & 31;
+      const bool ok = r0 + r < n && c < kc;
+      cp16z(su(&sm.a[slot][r][4 * c]), a + (ok ? (r0 + r) * lda + 4 * c : 0), ok);
+    }
+    if (tid < R * CO / 4) {  // B (and M): 32 rows x CO / 4 chunks
+      const int r = tid / (CO / 4), c = tid % (CO / 4);
+      const bool ok = r0 + r < n;
+      cp16z(su(&sm.b[slot][r][4 * c]), b + (ok ? (r0 + r) * ldb + 4 * c : 0), ok);
+      if (mk) cp16z(su(&sm.m[slot][r][4 * c]), mk + (ok ? (r0 + r) * ldm + 4 * c : 0), ok);
+    }
+  };
+  int64_t ch = blockIdx.x;
+#pragma unroll
+  for (int i = 0; i < S - 1; ++i) {
+    if (ch + i * (int64_t)gridDim.x < chunks) stage(i, ch + i * (int64_t)gridDim.x);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  float acc[NJ][4] = {};
+  float csum[R * CO / 256] = {};  // this thread's column (tid % CO) over its rows, in order
+  const bool active = 16 * w < k;
+  const int f0 = 16 * w + g, f1 = f0 + 8;
+  for (int it = 0; ch < chunks; ch += gridDim.x, ++it) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 2) : "memory");
+    __syncthreads();
+    const int slot = it % S;
+    {  // the slot computed last iteration is free for the chunk S - 1 ahead
+      const int64_t ahead = ch + (int64_t)(S - 1) * gridDim.x;
+      if (ahead < chunks) stage((it + S - 1) % S, ahead);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    // B .* [M > 0] split once for all warps, column sums on the way
+#pragma unroll
+    for (int i = 0; i < R * CO / 256; ++i) {
+      const int e = tid + 256 * i, r = e / CO, c = e % CO;
+      float v = sm.b[slot][r][c];
+      if (mk) v = sm.m[slot][r][c] > 0.f ? v : 0.f;
+      csum[i] += v;
+      const float hi = tf32f(v);
+      sm.bh[r][c] = hi;
+      sm.bl[r][c] = tf32f(v - hi);
+    }
+    __syncthreads();
+    if (!active) continue;
+    // the chunk's products start from zero and are folded into acc with FADD
+    // (RNE): the tensor-core accumulation chain stays 12 deep, not the whole slab
+    float ca[NJ][4] = {};
+#pragma unroll
+    for (int ks = 0; ks < R / 8; ++ks) {
+      const int r0 = 8 * ks + t, r1 = r0 + 4;
+      const uint32_t av[4] = {__float_as_uint(sm.a[slot][r0][f0]), __float_as_uint(sm.a[slot][r0][f1]),
+                              __float_as_uint(sm.a[slot][r1][f0]), __float_as_uint(sm.a[slot][r1][f1])};
+      uint32_t ah[4], al[4];
+      split(av, ah, al);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const uint32_t bh0 = __float_as_uint(sm.bh[r0][8 * j + g]), bh1 = __float_as_uint(sm.bh[r1][8 * j + g]);
+        const uint32_t bl0 = __float_as_uint(sm.bl[r0][8 * j + g]), bl1 = __float_as_uint(sm.bl[r1][8 * j + g]);
+        mma(ca[j], al, bh0, bh1);
+        mma(ca[j], ah, bl0, bl1);
+        mma(ca[j], ah, bh0, bh1);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[j][q] += ca[j][q];
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  float* pp = part + (int64_t)blockIdx.x * k * CO;
+  if (active) {
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int c = 8 * j + 2 * t;
+      if (f0 < k) *reinterpret_cast<float2*>(pp + (int64_t)f0 * CO + c) = make_float2(acc[j][0], acc[j][1]);
+      if (f1 < k) *reinterpret_cast<float2*>(pp + (int64_t)f1 * CO + c) = make_float2(acc[j][2], acc[j][3]);
+    }
+  }
+  if (colpart) {  // rows r = tid / CO + (256 / CO) i: fold the row residues in order
+    float v = 0.f;
+#pragma unroll
+    for (int i = 0; i < R * CO / 256; ++i) v += csum[i];
+    __syncthreads();
+    sm.cs[tid / CO][tid % CO] = v;
+    __syncthreads();
+    if (tid < CO) {
+      float tot = 0.f;
+#pragma unroll
+      for (int q = 0; q < 256 / CO; ++q) tot += sm.cs[q][tid];
+      colpart[(int64_t)blockIdx.x * CO + tid] = tot;
+    }
+  }
+}
 }  // namespace dm
 
 // one resident wave of persistent warps per kernel instantiation
@@ -801,5 +934,39 @@ int linear_xent(const float* x, int64_t ldx, int64_t n, int kin, const float* w,
   return TCG_OK;
 }
 #undef TCG_LX_DISPATCH
+
+
+// dW = A^T (B .* [M > 0]) partials (and column-sum partials) on the tensor cores;
+// 1 = shape not covered. *used = CTAs (slabs) written, <= cap_slabs.
+int gemm_tn_mma(const float* a, int64_t lda, const float* b, int64_t ldb, const float* mask, int64_t ldm,
+                int64_t n, int k, int c, float* part, float* colpart, int64_t cap_slabs, int64_t* used,
+                cudaStream_t s) {
+  static const bool off = std::getenv("TCG_NO_GEMM_TN_MMA") != nullptr;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (off || n < 4096 || k < 33 || k > 128 || k % 4 || (c != 16 && c != 32) || !al(a) || !al(b) ||
+      lda % 4 || ldb % 4 || (mask && (!al(mask) || ldm % 4)))
+    return 1;
+  const int64_t chunks = (n + dm::gt::R - 1) / dm::gt::R;
+#define TCG_GTM(CV)                                                                                    \
+  {                                                                                                    \
+    auto kern = dm::gemm_tn_mma<CV>;                                                                   \
+    const int smem = (int)sizeof(dm::gt::Smem<CV>);                                                    \
+    static int per_sm = 0;                                                                             \
+    if (per_sm == 0) {                                                                                 \
+      TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),         \
+               "gemm_tn_mma attr");                                                                    \
+      TCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem),               \
+               "gemm_tn_mma occupancy");                                                               \
+      if (per_sm < 1) per_sm = 1;                                                                      \
+    }                                                                                                  \
+    const int64_t grid = std::min<int64_t>(std::min<int64_t>((int64_t)num_sms() * per_sm, chunks), cap_slabs); \
+    kern<<<(unsigned)grid, 256, smem, s>>>(a, lda, b, ldb, mask, ldm, n, k, part, colpart);           \
+    *used = grid;                                                                                      \
+  }
+  if (c == 16) TCG_GTM(16) else TCG_GTM(32)
+#undef TCG_GTM
+  TCG_LAUNCHED("gemm_tn_mma");
+  return TCG_OK;
+}
 
 }  // namespace tcg
