@@ -484,6 +484,8 @@ int linear_xent(const float* x, int64_t ldx, int64_t n, int kin, const float* w,
                 const int64_t* labels, float inv_div, float* dl, int64_t ldd, float* lpart, int64_t cap_parts,
                 int64_t* nparts, cudaStream_t s);
 int64_t linear_xent_parts(int64_t n);
+int dense_in_mma(const float* x, int64_t ldx, int64_t n, int ci, const float* w, int co, bool trans,
+                 const float* bias, int relu, const float* mask, float* y, int64_t ldy, cudaStream_t s);
 int gemm_tn_mma(const float* a, int64_t lda, const float* b, int64_t ldb, const float* mask, int64_t ldm,
                 int64_t n, int k, int c, float* part, float* colpart, int64_t cap_slabs, int64_t* used,
                 cudaStream_t s);
@@ -509,9 +511,17 @@ extern "C" int tcg_dense(const float* x, int64_t ldx, int64_t n, int64_t ci, con
     if (rc != 1) return rc;
   }
   {
-    // tcgen05 3xTF32 GEMM (csrc/dense_tc.cu) for the wide input layers
-    const int rc = dense_tcgen05(x, ldx, n, (int)ci, m, (int)co, m_transposed != 0, bias, relu, mask, y,
-                                 ldy, s);
+    // the wide input layers (33..128 -> 16 / 32) on mma.sync 3xTF32 (csrc/dense_mma.cu
+    // dense_in_mma): arxiv 128 -> 32 38.9 us cold (tcgen05 dense_tc 43.0, FFMA2 53.2),
+    // 128 -> 16 30.7 (36.9), 96 -> 16 46.1 (55.3), products 100 -> 16 242 (328).
+    // TCG_DENSE_TC=1 puts the tcgen05 kernel (csrc/dense_tc.cu) first for 96..128 -> 32.
+    static const bool tc_first = std::getenv("TCG_DENSE_TC") && std::atoi(std::getenv("TCG_DENSE_TC")) == 1;
+    if (tc_first) {
+      const int rc = dense_tcgen05(x, ldx, n, (int)ci, m, (int)co, m_transposed != 0, bias, relu, mask, y,
+                                   ldy, s);
+      if (rc != 1) return rc;
+    }
+    const int rc = dense_in_mma(x, ldx, n, (int)ci, m, (int)co, m_transposed != 0, bias, relu, mask, y, ldy, s);
     if (rc != 1) return rc;
   }
   {

@@ -855,6 +855,118 @@ __global__ void __launch_bounds__(256, 2) gemm_tn_mma(const float* __restrict__ 
     }
   }
 }
+
+// ---- the wide input layers: Y = act(X W + b), X [n x ci] (ci <= 128), W [ci x CO] ----
+//
+// One CTA of 4 warps per 64-row chunk through a 2-stage cp.async ring (rows of
+// 512 B, 16-B chunk c of row r at r * 512 + ((c ^ (r & 7)) << 4): ldmatrix
+// conflict-free); warp w computes rows 16 w .. + 15 of the chunk for every
+// n-tile (each A fragment is split into tf32 hi / lo once), 3xTF32 with W
+// (tf32 hi / lo) in shared memory.
+namespace di {
+constexpr int R = 64, S = 2;
+template <int CO>
+struct Smem {
+  static constexpr int WP = CO + 8;  // B fragment reads: rows t / t + 4 land 8 banks apart
+  unsigned char x[S][R * 512];
+  float wh[128][WP], wl[128][WP];
+};
+}  // namespace di
+
+template <int CO>
+__global__ void __launch_bounds__(128, 2) dense_in_mma(const float* __restrict__ x, int64_t ldx, int64_t n, int ci,
+                                                        const float* __restrict__ w, const float* __restrict__ bias,
+                                                        int relu, float* __restrict__ y, int64_t ldy) {
+  using namespace di;
+  using Sm = Smem<CO>;
+  constexpr int WP = Sm::WP, NJ = CO / 8, NT = 128;
+  extern __shared__ __align__(128) unsigned char dsm_[];
+  Sm& sm = *reinterpret_cast<Sm*>(dsm_);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int rg = wid, j0 = 0;  // warp w: rows 16 w .. 16 w + 15 of the chunk, every n-tile
+  const int64_t chunks = (n + R - 1) / R;
+  const int kc4 = ci / 4, kc8 = (ci + 7) / 8;
+  auto stage = [&](int slot, int64_t ch) {
+    const uint32_t base = su(&sm.x[slot][0]);
+    const int64_t r0 = ch * R;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {  // 64 rows x 32 chunks
+      const int q = tid + NT * i, r = q >> 5, c = q & 31;
+      const bool ok = r0 + r < n && c < kc4;
+      cp16z(base + r * 512 + ((c ^ (r & 7)) << 4), x + (ok ? (r0 + r) * ldx + 4 * c : 0), ok);
+    }
+  };
+  int64_t ch = blockIdx.x;
+  if (ch < chunks) stage(0, ch);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  for (int i = tid; i < 128 * CO; i += NT) {
+    const int k = i / CO, c = i % CO;
+    const float v = k < ci ? __ldg(w + (int64_t)k * CO + c) : 0.f;
+    const float hi = tf32f(v);
+    sm.wh[k][c] = hi;
+    sm.wl[k][c] = tf32f(v - hi);
+  }
+  float bv[NJ][2];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) bv[j][e] = bias ? __ldg(bias + 8 * (j0 + j) + 2 * t + e) : 0.f;
+  const uint32_t wh = su(&sm.wh[0][0]), wl = su(&sm.wl[0][0]);
+  for (int it = 0; ch < chunks; ch += gridDim.x, ++it) {
+    const int slot = it & 1;
+    {
+      const int64_t ahead = ch + gridDim.x;
+      if (ahead < chunks) stage(slot ^ 1, ahead);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncthreads();
+    const uint32_t tile = su(&sm.x[slot][0]);
+    // two accumulator sets (k chunks even / odd), added at the end: the
+    // tensor-core accumulation chains stay half as deep
+    float acc[2][NJ][4] = {};
+    const int m = lane >> 3, rr = lane & 7;
+    const int ar = 16 * rg + rr + 8 * (m & 1);
+    auto kstep = [&](int kc, float (&ac)[NJ][4]) {
+      uint32_t a[4], ah[4], al[4];
+      const int c = 2 * kc + (m >> 1);
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                   : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+                   : "r"(tile + ar * 512 + ((c ^ (ar & 7)) << 4)));
+      split(a, ah, al);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const uint32_t o0 = ((8 * kc + t) * WP + 8 * (j0 + j) + g) * 4, o1 = o0 + 4 * WP * 4;
+        const uint32_t h0 = lds32(wh + o0), h1 = lds32(wh + o1), l0 = lds32(wl + o0), l1 = lds32(wl + o1);
+        mma(ac[j], al, h0, h1);
+        mma(ac[j], ah, l0, l1);
+        mma(ac[j], ah, h0, h1);
+      }
+    };
+    int kc = 0;
+#pragma unroll 2
+    for (; kc + 1 < kc8; kc += 2) {
+      kstep(kc, acc[0]);
+      kstep(kc + 1, acc[1]);
+    }
+    if (kc < kc8) kstep(kc, acc[0]);
+    __syncthreads();  // the slot is restaged next iteration
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t row = ch * R + 16 * rg + g + 8 * h;
+      if (row >= n) continue;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        float v0 = acc[0][j][2 * h] + acc[1][j][2 * h] + bv[j][0];
+        float v1 = acc[0][j][2 * h + 1] + acc[1][j][2 * h + 1] + bv[j][1];
+        if (relu) v0 = fmaxf(v0, 0.f), v1 = fmaxf(v1, 0.f);
+        *reinterpret_cast<float2*>(y + row * ldy + 8 * (j0 + j) + 2 * t) = make_float2(v0, v1);
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
 }  // namespace dm
 
 // one resident wave of persistent warps per kernel instantiation
@@ -966,6 +1078,38 @@ int gemm_tn_mma(const float* a, int64_t lda, const float* b, int64_t ldb, const 
   if (c == 16) TCG_GTM(16) else TCG_GTM(32)
 #undef TCG_GTM
   TCG_LAUNCHED("gemm_tn_mma");
+  return TCG_OK;
+}
+
+
+// Y = act(X W + b) for the wide input layers (ci 33..128 -> 16 / 32, n >= 4096) on
+// mma.sync 3xTF32; 1 = shape not covered.
+int dense_in_mma(const float* x, int64_t ldx, int64_t n, int ci, const float* w, int co, bool trans,
+                 const float* bias, int relu, const float* mask, float* y, int64_t ldy, cudaStream_t s) {
+  static const bool off = std::getenv("TCG_NO_DENSE_IN_MMA") != nullptr;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (off || trans || mask || n < 4096 || ci < 33 || ci > 128 || ci % 4 || (co != 16 && co != 32) || !al(x) ||
+      ldx % 4 || (reinterpret_cast<uintptr_t>(y) & 7) || ldy % 2)
+    return 1;
+  const int64_t chunks = (n + dm::di::R - 1) / dm::di::R;
+#define TCG_DIM(CV)                                                                                     \
+  {                                                                                                     \
+    auto kern = dm::dense_in_mma<CV>;                                                                   \
+    const int smem = (int)sizeof(dm::di::Smem<CV>);                                                     \
+    static int per_sm = 0;                                                                              \
+    if (per_sm == 0) {                                                                                  \
+      TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),          \
+               "dense_in_mma attr");                                                                    \
+      TCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem),                \
+               "dense_in_mma occupancy");                                                               \
+      if (per_sm < 1) per_sm = 1;                                                                       \
+    }                                                                                                   \
+    const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm, chunks);                        \
+    kern<<<(unsigned)grid, 128, smem, s>>>(x, ldx, n, ci, w, bias, relu, y, ldy);                       \
+  }
+  if (co == 16) TCG_DIM(16) else TCG_DIM(32)
+#undef TCG_DIM
+  TCG_LAUNCHED("dense_in_mma");
   return TCG_OK;
 }
 
