@@ -459,8 +459,10 @@ __global__ void __launch_bounds__(256)
 }
 
 int64_t colsum_slabs(int64_t n) {
-  const int64_t s = (n + 1023) / 1024;
-  const int64_t cap = 2LL * num_sms();
+  // 256 rows per slab: ~4 CTAs of 256 threads per SM and one round of loads each
+  // (1024-row slabs at <= 2 per SM ran arxiv 169343 x 16 at 1 TB/s)
+  const int64_t s = (n + 255) / 256;
+  const int64_t cap = 8LL * num_sms();
   return s < 1 ? 1 : (s > cap ? cap : s);
 }
 
