@@ -488,6 +488,8 @@ int linear_xent(const float* x, int64_t ldx, int64_t n, int kin, const float* w,
 int64_t linear_xent_parts(int64_t n);
 int dense_in_mma(const float* x, int64_t ldx, int64_t n, int ci, const float* w, int co, bool trans,
                  const float* bias, int relu, const float* mask, float* y, int64_t ldy, cudaStream_t s);
+int dense_wide_mma(const float* x, int64_t ldx, int64_t n, int ci, const float* w, int co, bool trans,
+                   const float* bias, int relu, const float* mask, float* y, int64_t ldy, cudaStream_t s);
 int gemm_tn_mma(const float* a, int64_t lda, const float* b, int64_t ldb, const float* mask, int64_t ldm,
                 int64_t n, int k, int c, float* part, float* colpart, int64_t cap_slabs, int64_t* used,
                 cudaStream_t s);
@@ -524,6 +526,11 @@ extern "C" int tcg_dense(const float* x, int64_t ldx, int64_t n, int64_t ci, con
       if (rc != 1) return rc;
     }
     const int rc = dense_in_mma(x, ldx, n, (int)ci, m, (int)co, m_transposed != 0, bias, relu, mask, y, ldy, s);
+    if (rc != 1) return rc;
+  }
+  {
+    // inputs wider than 128 features (Cora 1433, Pubmed 500) in 128-feature K panels
+    const int rc = dense_wide_mma(x, ldx, n, (int)ci, m, (int)co, m_transposed != 0, bias, relu, mask, y, ldy, s);
     if (rc != 1) return rc;
   }
   {

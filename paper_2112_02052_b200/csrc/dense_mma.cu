@@ -45,6 +45,10 @@ __device__ __forceinline__ uint32_t sw(int r, int c) { return r * 128 + ((c ^ (r
 __device__ __forceinline__ void cp16z(uint32_t d, const void* s, bool ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(s), "r"(ok ? 16 : 0) : "memory");
 }
+// 16-B copy of the first `bytes` (0..16) bytes, zero-filling the rest
+__device__ __forceinline__ void cp16n(uint32_t d, const void* s, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(s), "r"(bytes) : "memory");
+}
 
 // rows [row0, row0 + 16) of a [n x 32] matrix into a staged tile (zero past n)
 __device__ __forceinline__ void stage_rows(uint32_t tile, const float* __restrict__ x, int64_t ldx, int64_t n,
@@ -758,14 +762,17 @@ __global__ void __launch_bounds__(256, 2) gemm_tn_mma(const float* __restrict__ 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int64_t chunks = (n + R - 1) / R;
-  const int kc = k / 4;  // 16-B chunks per A row
+  // blockIdx.y: 128-feature panel of A (k > 128); the partial rows k0 .. k0 + kp
+  const int k0 = 128 * blockIdx.y, kp = min(128, k - k0);
+  a += k0;
+  const int kc = (kp + 3) / 4;  // 16-B chunks per A row (a partial last one zero-filled)
   auto stage = [&](int slot, int64_t ch) {
     const int64_t r0 = ch * R;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {  // A: 32 rows x 32 chunks
       const int q = tid + 256 * i, r = q >> 5, c = q & 31;
       const bool ok = r0 + r < n && c < kc;
-      cp16z(su(&sm.a[slot][r][4 * c]), a + (ok ? (r0 + r) * lda + 4 * c : 0), ok);
+      cp16n(su(&sm.a[slot][r][4 * c]), a + (ok ? (r0 + r) * lda + 4 * c : 0), ok ? 4 * min(4, kp - 4 * c) : 0);
     }
     if (tid < R * CO / 4) {  // B (and M): 32 rows x CO / 4 chunks
       const int r = tid / (CO / 4), c = tid % (CO / 4);
@@ -782,7 +789,7 @@ __global__ void __launch_bounds__(256, 2) gemm_tn_mma(const float* __restrict__ 
   }
   float acc[NJ][4] = {};
   float csum[R * CO / 256] = {};  // this thread's column (tid % CO) over its rows, in order
-  const bool active = 16 * w < k;
+  const bool active = 16 * w < kp;
   const int f0 = 16 * w + g, f1 = f0 + 8;
   for (int it = 0; ch < chunks; ch += gridDim.x, ++it) {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 2) : "memory");
@@ -831,16 +838,16 @@ __global__ void __launch_bounds__(256, 2) gemm_tn_mma(const float* __restrict__ 
       for (int q = 0; q < 4; ++q) acc[j][q] += ca[j][q];
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  float* pp = part + (int64_t)blockIdx.x * k * CO;
+  float* pp = part + (int64_t)blockIdx.x * k * CO + (int64_t)k0 * CO;
   if (active) {
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
       const int c = 8 * j + 2 * t;
-      if (f0 < k) *reinterpret_cast<float2*>(pp + (int64_t)f0 * CO + c) = make_float2(acc[j][0], acc[j][1]);
-      if (f1 < k) *reinterpret_cast<float2*>(pp + (int64_t)f1 * CO + c) = make_float2(acc[j][2], acc[j][3]);
+      if (f0 < kp) *reinterpret_cast<float2*>(pp + (int64_t)f0 * CO + c) = make_float2(acc[j][0], acc[j][1]);
+      if (f1 < kp) *reinterpret_cast<float2*>(pp + (int64_t)f1 * CO + c) = make_float2(acc[j][2], acc[j][3]);
     }
   }
-  if (colpart) {  // rows r = tid / CO + (256 / CO) i: fold the row residues in order
+  if (colpart && blockIdx.y == 0) {  // rows r = tid / CO + (256 / CO) i: fold the row residues in order
     float v = 0.f;
 #pragma unroll
     for (int i = 0; i < R * CO / 256; ++i) v += csum[i];
@@ -886,15 +893,16 @@ __global__ void __launch_bounds__(128, 2) dense_in_mma(const float* __restrict__
   const int g = lane >> 2, t = lane & 3;
   const int rg = wid, j0 = 0;  // warp w: rows 16 w .. 16 w + 15 of the chunk, every n-tile
   const int64_t chunks = (n + R - 1) / R;
-  const int kc4 = ci / 4, kc8 = (ci + 7) / 8;
+  const int kc8 = (ci + 7) / 8;
   auto stage = [&](int slot, int64_t ch) {
     const uint32_t base = su(&sm.x[slot][0]);
     const int64_t r0 = ch * R;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {  // 64 rows x 32 chunks
       const int q = tid + NT * i, r = q >> 5, c = q & 31;
-      const bool ok = r0 + r < n && c < kc4;
-      cp16z(base + r * 512 + ((c ^ (r & 7)) << 4), x + (ok ? (r0 + r) * ldx + 4 * c : 0), ok);
+      const bool ok = r0 + r < n && 4 * c < ci;  // a partial last chunk is zero-filled past ci
+      cp16n(base + r * 512 + ((c ^ (r & 7)) << 4), x + (ok ? (r0 + r) * ldx + 4 * c : 0),
+            ok ? 4 * min(4, ci - 4 * c) : 0);
     }
   };
   int64_t ch = blockIdx.x;
@@ -963,6 +971,130 @@ __global__ void __launch_bounds__(128, 2) dense_in_mma(const float* __restrict__
         if (relu) v0 = fmaxf(v0, 0.f), v1 = fmaxf(v1, 0.f);
         *reinterpret_cast<float2*>(y + row * ldy + 8 * (j0 + j) + 2 * t) = make_float2(v0, v1);
       }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// ---- input layers wider than 128 features (Cora 1433, Pubmed 500): K panels ----
+//
+// dense_in_mma's layout with the K dimension walked in 128-feature panels: the
+// ring stages (row chunk, panel) items, X rows and the raw W panel together,
+// and W is split into tf32 hi / lo at the fragment load. The accumulators of a
+// row chunk live across its panels (even / odd panels in separate sets).
+namespace dw {
+constexpr int R = 64, S = 2;
+template <int CO>
+struct Smem {
+  static constexpr int WP = CO + 8;
+  unsigned char x[S][R * 512];
+  float w[S][128][WP];
+};
+}  // namespace dw
+
+template <int CO>
+__global__ void __launch_bounds__(128, 2) dense_wide_mma(const float* __restrict__ x, int64_t ldx, int64_t n,
+                                                          int ci, const float* __restrict__ w,
+                                                          const float* __restrict__ bias, int relu,
+                                                          float* __restrict__ y, int64_t ldy) {
+  using namespace dw;
+  using Sm = Smem<CO>;
+  constexpr int WP = Sm::WP, NJ = CO / 8, NT = 128;
+  extern __shared__ __align__(128) unsigned char wsm_[];
+  Sm& sm = *reinterpret_cast<Sm*>(wsm_);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t chunks = (n + R - 1) / R;
+  const int panels = (ci + 127) / 128;
+  const int64_t mine = chunks > blockIdx.x ? (chunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t items = mine * panels;
+  auto stage = [&](int slot, int64_t item) {
+    const int64_t ch = blockIdx.x + (item / panels) * gridDim.x;
+    const int k0 = (int)(item % panels) * 128;
+    const int kv = min(128, ci - k0);  // features of this panel
+    const uint32_t base = su(&sm.x[slot][0]);
+    const int64_t r0 = ch * R;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {  // 64 rows x 32 chunks
+      const int q = tid + NT * i, r = q >> 5, c = q & 31;
+      const bool ok = r0 + r < n && 4 * c < kv;  // a partial last chunk is zero-filled past kv
+      cp16n(base + r * 512 + ((c ^ (r & 7)) << 4), x + (ok ? (r0 + r) * ldx + k0 + 4 * c : 0),
+            ok ? 4 * min(4, kv - 4 * c) : 0);
+    }
+    // the W panel: 128 rows x CO (CO / 4 chunks per row)
+    for (int q = tid; q < 128 * CO / 4; q += NT) {
+      const int r = q / (CO / 4), c = q % (CO / 4);
+      const bool ok = r < kv;
+      cp16z(su(&sm.w[slot][r][4 * c]), w + (ok ? (int64_t)(k0 + r) * CO + 4 * c : 0), ok);
+    }
+  };
+  float bv[NJ][2];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) bv[j][e] = bias ? __ldg(bias + 8 * j + 2 * t + e) : 0.f;
+  if (items > 0) stage(0, 0);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  float acc[NJ][4] = {};
+  const int m = lane >> 3, rr = lane & 7;
+  const int ar = 16 * wid + rr + 8 * (m & 1);
+  for (int64_t it = 0; it < items; ++it) {
+    const int slot = (int)(it & 1);
+    if (it + 1 < items) stage(slot ^ 1, it + 1);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncthreads();
+    const uint32_t tile = su(&sm.x[slot][0]);
+    const int p = (int)(it % panels);
+    const int kc8 = (min(128, ci - 128 * p) + 7) / 8;
+    // per panel: even / odd k chunks in fresh accumulators (24-deep tensor-core
+    // chains), folded into acc with FADD (RNE) -- K = 1433 stays fp32-class
+    float c0[NJ][4] = {}, c1[NJ][4] = {};
+    auto kstep = [&](int kc, float (&ac)[NJ][4]) {
+      uint32_t a[4], ah[4], al[4];
+      const int c = 2 * kc + (m >> 1);
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                   : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+                   : "r"(tile + ar * 512 + ((c ^ (ar & 7)) << 4)));
+      split(a, ah, al);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const float w0 = sm.w[slot][8 * kc + t][8 * j + g], w1 = sm.w[slot][8 * kc + t + 4][8 * j + g];
+        const uint32_t h0 = tf32_rn(w0), h1 = tf32_rn(w1);
+        const uint32_t l0 = tf32_rn(w0 - __uint_as_float(h0)), l1 = tf32_rn(w1 - __uint_as_float(h1));
+        mma(ac[j], al, h0, h1);
+        mma(ac[j], ah, l0, l1);
+        mma(ac[j], ah, h0, h1);
+      }
+    };
+    int kc = 0;
+    for (; kc + 1 < kc8; kc += 2) {
+      kstep(kc, c0);
+      kstep(kc + 1, c1);
+    }
+    if (kc < kc8) kstep(kc, c0);
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[j][q] += c0[j][q] + c1[j][q];
+    __syncthreads();  // the slot is restaged next iteration
+    if (p == panels - 1) {  // the row chunk is complete
+      const int64_t ch = blockIdx.x + (it / panels) * gridDim.x;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t row = ch * R + 16 * wid + g + 8 * h;
+        if (row < n) {
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
+            float v0 = acc[j][2 * h] + bv[j][0];
+            float v1 = acc[j][2 * h + 1] + bv[j][1];
+            if (relu) v0 = fmaxf(v0, 0.f), v1 = fmaxf(v1, 0.f);
+            *reinterpret_cast<float2*>(y + row * ldy + 8 * j + 2 * t) = make_float2(v0, v1);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -1055,9 +1187,10 @@ int gemm_tn_mma(const float* a, int64_t lda, const float* b, int64_t ldb, const 
                 cudaStream_t s) {
   static const bool off = std::getenv("TCG_NO_GEMM_TN_MMA") != nullptr;
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (off || n < 4096 || k < 33 || k > 128 || k % 4 || (c != 16 && c != 32) || !al(a) || !al(b) ||
-      lda % 4 || ldb % 4 || (mask && (!al(mask) || ldm % 4)))
+  if (off || n < 1024 || k < 33 || (c != 16 && c != 32) || !al(a) || !al(b) || lda % 4 || ldb % 4 ||
+      (mask && (!al(mask) || ldm % 4)))
     return 1;
+  const unsigned panels = (unsigned)((k + 127) / 128);
   const int64_t chunks = (n + dm::gt::R - 1) / dm::gt::R;
 #define TCG_GTM(CV)                                                                                    \
   {                                                                                                    \
@@ -1072,7 +1205,7 @@ int gemm_tn_mma(const float* a, int64_t lda, const float* b, int64_t ldb, const 
       if (per_sm < 1) per_sm = 1;                                                                      \
     }                                                                                                  \
     const int64_t grid = std::min<int64_t>(std::min<int64_t>((int64_t)num_sms() * per_sm, chunks), cap_slabs); \
-    kern<<<(unsigned)grid, 256, smem, s>>>(a, lda, b, ldb, mask, ldm, n, k, part, colpart);           \
+    kern<<<dim3((unsigned)grid, panels), 256, smem, s>>>(a, lda, b, ldb, mask, ldm, n, k, part, colpart); \
     *used = grid;                                                                                      \
   }
   if (c == 16) TCG_GTM(16) else TCG_GTM(32)
@@ -1088,7 +1221,7 @@ int dense_in_mma(const float* x, int64_t ldx, int64_t n, int ci, const float* w,
                  const float* bias, int relu, const float* mask, float* y, int64_t ldy, cudaStream_t s) {
   static const bool off = std::getenv("TCG_NO_DENSE_IN_MMA") != nullptr;
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (off || trans || mask || n < 4096 || ci < 33 || ci > 128 || ci % 4 || (co != 16 && co != 32) || !al(x) ||
+  if (off || trans || mask || n < 4096 || ci < 33 || ci > 128 || (co != 16 && co != 32) || !al(x) ||
       ldx % 4 || (reinterpret_cast<uintptr_t>(y) & 7) || ldy % 2)
     return 1;
   const int64_t chunks = (n + dm::di::R - 1) / dm::di::R;
@@ -1110,6 +1243,38 @@ int dense_in_mma(const float* x, int64_t ldx, int64_t n, int ci, const float* w,
   if (co == 16) TCG_DIM(16) else TCG_DIM(32)
 #undef TCG_DIM
   TCG_LAUNCHED("dense_in_mma");
+  return TCG_OK;
+}
+
+
+// Y = act(X W + b) for inputs wider than 128 features (-> 16 / 32) on mma.sync
+// 3xTF32, K in 128-feature panels; 1 = shape not covered.
+int dense_wide_mma(const float* x, int64_t ldx, int64_t n, int ci, const float* w, int co, bool trans,
+                   const float* bias, int relu, const float* mask, float* y, int64_t ldy, cudaStream_t s) {
+  static const bool off = std::getenv("TCG_NO_DENSE_IN_MMA") != nullptr;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (off || trans || mask || n < 256 || ci <= 128 || (co != 16 && co != 32) || !al(x) || !al(w) ||
+      ldx % 4 || (reinterpret_cast<uintptr_t>(y) & 7) || ldy % 2)
+    return 1;
+  const int64_t chunks = (n + dm::dw::R - 1) / dm::dw::R;
+#define TCG_DWM(CV)                                                                                     \
+  {                                                                                                     \
+    auto kern = dm::dense_wide_mma<CV>;                                                                 \
+    const int smem = (int)sizeof(dm::dw::Smem<CV>);                                                     \
+    static int per_sm = 0;                                                                              \
+    if (per_sm == 0) {                                                                                  \
+      TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),          \
+               "dense_wide_mma attr");                                                                  \
+      TCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem),                \
+               "dense_wide_mma occupancy");                                                             \
+      if (per_sm < 1) per_sm = 1;                                                                       \
+    }                                                                                                   \
+    const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm, chunks);                        \
+    kern<<<(unsigned)grid, 128, smem, s>>>(x, ldx, n, ci, w, bias, relu, y, ldy);                       \
+  }
+  if (co == 16) TCG_DWM(16) else TCG_DWM(32)
+#undef TCG_DWM
+  TCG_LAUNCHED("dense_wide_mma");
   return TCG_OK;
 }
 

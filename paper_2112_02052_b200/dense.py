@@ -45,6 +45,21 @@ def rows_ok(x):
     return x if x.dim() == 2 and x.stride(1) == 1 else x.contiguous()
 
 
+def rows16(x):
+    """x with 16-B aligned rows (a padded-stride copy when they are not): the
+    tensor-core dense kernels stage rows in 16-B pieces. Used for the wide input
+    layers (Cora's 1433 features), where the copy is small next to the GEMM."""
+    x = rows_ok(x)
+    if x.stride(0) % 4 == 0 and x.data_ptr() % 16 == 0:
+        return x
+    out = rows_empty(x.shape[0], x.shape[1], x.device) if x.shape[1] > 16 else None
+    if out is None or out.stride(0) % 4:
+        buf = torch.empty((x.shape[0], (x.shape[1] + 3) // 4 * 4), dtype=x.dtype, device=x.device)
+        out = buf[:, :x.shape[1]]
+    out.copy_(x)
+    return out
+
+
 def dense(x, w, bias=None, relu=False, mask=None, transposed=False, out=None):
     """y = act((x .* [mask>0]) M + bias), M = w ([ci x co]) or w^T when
     `transposed` (w then [co x ci])."""
@@ -149,7 +164,7 @@ def softmax_xent_backward(logits, labels, grad_scale=None):
 class DenseFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, b, relu: bool):
-        x = rows_ok(x)
+        x = rows16(x) if x.shape[1] > 128 and w.shape[1] in (16, 32) else rows_ok(x)
         y = dense(x, w.contiguous(), bias=b, relu=relu)
         ctx.relu = relu
         ctx.has_b = b is not None

@@ -7,7 +7,8 @@ import paper_2112_02052_b200 as tcg
 from paper_2112_02052_b200 import layers
 kind = sys.argv[1] if len(sys.argv) > 1 else "agnn"
 shape = sys.argv[2] if len(sys.argv) > 2 else "arxiv"
-feats, classes = {"arxiv": (128, 40), "products": (100, 47), "amazon0601": (96, 22)}[shape]
+feats, classes = {"arxiv": (128, 40), "products": (100, 47), "amazon0601": (96, 22), "cora": (1433, 7),
+                  "pubmed": (500, 3)}[shape]
 g, x_np, lab_np = bench.make_inputs(shape, feats, classes)
 t = tcg.translate(g, tcg.BlockConfig(), device="cuda")
 t.transpose()
