@@ -30,6 +30,9 @@ extern "C" {
 #define TCG_E_WORKSPACE (-3) /* workspace too small                        */
 #define TCG_E_UNSUPPORTED (-4)
 
+#define TCG_ACT_NONE 0
+#define TCG_ACT_RELU 1 /* tcg_spmm_act: ReLU on the stored output */
+
 #define TCG_PREC_F32 0  /* exact f32: CSR-order fold, bitwise = reference f32 */
 #define TCG_PREC_TF32 1 /* tensor cores: RNE-to-tf32 operands, f32 accumulate */
 
@@ -219,6 +222,14 @@ int tcg_spmm(const tcg_tiling* t, const float* x, int64_t ldx, int64_t dim,
              const float* weights2, const uint32_t* weight_idx2, const float* bias,
              float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
              int32_t precision, int32_t accumulate, void* stream);
+/* tcg_spmm (single operand) with an activation on the stored rows: act =
+ * TCG_ACT_RELU gives Y = relu(A_w X + bias (+ Y)), fused into the stream
+ * engine's epilogue (a separate pass for the other engines). GCN's first
+ * layer, relu(gcn_layer(...)). */
+int tcg_spmm_act(const tcg_tiling* t, const float* x, int64_t ldx, int64_t dim,
+                 const float* weights, const uint32_t* weight_idx, const float* bias, float* y,
+                 int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
+                 int32_t precision, int32_t accumulate, int32_t act, void* stream);
 
 /* ---- SDDMM: reference kernels.sddmm (kernels.py:377-538, Alg. 3) --------- */
 /* out[e] = <xa[row e], xb[col e]> for the edges e of windows
@@ -311,6 +322,12 @@ size_t tcg_colsum_workspace_bytes(int64_t n, int64_t c);
  * reduction (deterministic). The bias gradient of gcn_layer's `+ b`. */
 int tcg_colsum(const float* x, int64_t ld, int64_t n, int64_t c, float* out, void* workspace,
                size_t workspace_bytes, void* stream);
+/* ReLU backward fused with the bias gradient: gout = x .* [gate > 0] (gate =
+ * the layer's ReLU output) and out[c] = column sums of gout, fixed order
+ * (deterministic); workspace as tcg_colsum. */
+int tcg_colsum_gate(const float* x, int64_t ld, const float* gate, int64_t ldg, int64_t n, int64_t c,
+                    float* gout, int64_t ldo, float* out, void* workspace, size_t workspace_bytes,
+                    void* stream);
 size_t tcg_softmax_xent_workspace_bytes(int64_t n);
 /* loss = mean_i -log_softmax(logits_i)[labels_i]; dlogits = (softmax - onehot)/n
  * (dlogits may be null: loss only) */

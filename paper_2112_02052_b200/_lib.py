@@ -14,6 +14,7 @@ _PKG = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("TCG_B200_LIB", _PKG / "libtcg_b200.so"))
 
 TCG_OK = 0
+ACT_NONE, ACT_RELU = 0, 1
 TCG_E_UNSUPPORTED = -4
 PREC_F32 = 0
 PREC_TF32 = 1
@@ -111,6 +112,9 @@ SIGNATURES = {
                                      _SZ, _P]),
     "tcg_colsum_workspace_bytes": (_SZ, [_I64, _I64]),
     "tcg_colsum": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _SZ, _P]),
+    "tcg_colsum_gate": (C.c_int, [_P, _I64, _P, _I64, _I64, _I64, _P, _I64, _P, _P, _SZ, _P]),
+    "tcg_spmm_act": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _I64,
+                               _I64, _I32, _I32, _I32, _P]),
     "tcg_softmax_xent_workspace_bytes": (_SZ, [_I64]),
     "tcg_softmax_xent": (C.c_int, [_P, _I64, _P, _I64, _I64, _P, _P, _P, _SZ, _P]),
     "tcg_linear_xent_workspace_bytes": (_SZ, [_I64]),

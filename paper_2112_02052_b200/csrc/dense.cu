@@ -416,10 +416,11 @@ int fast_gemm_tn(const float* a, int64_t lda, const float* b, int64_t ldb, const
 // r+RL, ... of its V columns (V = 4: float4 loads when c, ld are multiples of
 // 4) with 8 independent partials in flight; the RL lane partials are then added
 // in lane order, so the result is deterministic.
-template <int V>
+template <int V, bool GATE = false>
 __global__ void __launch_bounds__(256)
     colsum_part(const float* __restrict__ x, int64_t ld, int64_t n, int c, int64_t rows,
-                float* __restrict__ part) {
+                float* __restrict__ part, const float* __restrict__ gate = nullptr, int64_t ldg = 0,
+                float* __restrict__ gout = nullptr, int64_t ldo = 0) {
   using VT = typename std::conditional<V == 4, float4, float>::type;
   __shared__ VT sh[256];
   const int units = c / V;
@@ -427,6 +428,16 @@ __global__ void __launch_bounds__(256)
   auto add = [](VT& a, const VT& b) {
     if constexpr (V == 4) a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
     else a += b;
+  };
+  // GATE: the value is x .* [gate > 0] (the ReLU backward), also written to gout
+  auto gated = [](VT v, VT m) {
+    if constexpr (V == 4) {
+      v.x = m.x > 0.f ? v.x : 0.f, v.y = m.y > 0.f ? v.y : 0.f;
+      v.z = m.z > 0.f ? v.z : 0.f, v.w = m.w > 0.f ? v.w : 0.f;
+      return v;
+    } else {
+      return m > 0.f ? v : 0.f;
+    }
   };
   for (int ub = 0; ub < units; ub += 256) {
     const int uw = min(256, units - ub);
@@ -437,13 +448,26 @@ __global__ void __launch_bounds__(256)
     for (int u = 0; u < 8; ++u) sp[u] = VT{};
     if (lane_r < rl) {
       const VT* col = reinterpret_cast<const VT*>(x) + ub + j;
-      const int64_t ldv = ld / V;
+      const VT* gcol = GATE ? reinterpret_cast<const VT*>(gate) + ub + j : nullptr;
+      VT* ocol = GATE ? reinterpret_cast<VT*>(gout) + ub + j : nullptr;
+      const int64_t ldv = ld / V, ldgv = ldg / V, ldov = ldo / V;
+      auto val = [&](int64_t r) {
+        VT v = __ldg(col + r * ldv);
+        if constexpr (GATE) {
+          v = gated(v, __ldg(gcol + r * ldgv));
+          ocol[r * ldov] = v;
+        }
+        return v;
+      };
       int64_t r = r0 + lane_r;
       for (; r + 7 * rl < r1; r += 8 * rl) {
+        VT v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) add(sp[u], __ldg(col + (r + u * rl) * ldv));
+        for (int u = 0; u < 8; ++u) v[u] = val(r + u * rl);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) add(sp[u], v[u]);
       }
-      for (; r < r1; r += rl) add(sp[0], __ldg(col + r * ldv));
+      for (; r < r1; r += rl) add(sp[0], val(r));
     }
     add(sp[0], sp[1]), add(sp[2], sp[3]), add(sp[4], sp[5]), add(sp[6], sp[7]);
     add(sp[0], sp[2]), add(sp[4], sp[6]), add(sp[0], sp[4]);
@@ -733,6 +757,32 @@ extern "C" int tcg_colsum(const float* x, int64_t ld, int64_t n, int64_t c, floa
     TCG_LAUNCHED("colsum_part");
     sum_slabs<<<(unsigned)((c + 31) / 32), 1024, 0, s>>>(part, (int)slabs, c, out);
   }
+  TCG_LAUNCHED("sum_slabs");
+  return TCG_OK;
+}
+
+extern "C" int tcg_colsum_gate(const float* x, int64_t ld, const float* gate, int64_t ldg, int64_t n,
+                               int64_t c, float* gout, int64_t ldo, float* out, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  TCG_REQUIRE(n >= 0 && c >= 1 && ld >= c && ldg >= c && ldo >= c, "tcg_colsum_gate: bad shape");
+  TCG_REQUIRE(workspace_bytes >= tcg_colsum_workspace_bytes(n, c), "tcg_colsum_gate: workspace too small");
+  TCG_REQUIRE(out && workspace && (n == 0 || (x && gate && gout)), "tcg_colsum_gate: null pointer");
+  cudaStream_t s = as_stream(stream);
+  if (n == 0) {
+    TCG_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * c, s), "tcg_colsum_gate memset");
+    return TCG_OK;
+  }
+  const int64_t slabs = colsum_slabs(n);
+  const int64_t rows = (n + slabs - 1) / slabs;
+  float* part = static_cast<float*>(workspace);
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool v4 = c % 4 == 0 && ld % 4 == 0 && ldg % 4 == 0 && ldo % 4 == 0 && al(x) && al(gate) && al(gout);
+  if (v4)
+    colsum_part<4, true><<<(unsigned)slabs, 256, 0, s>>>(x, ld, n, (int)c, rows, part, gate, ldg, gout, ldo);
+  else
+    colsum_part<1, true><<<(unsigned)slabs, 256, 0, s>>>(x, ld, n, (int)c, rows, part, gate, ldg, gout, ldo);
+  TCG_LAUNCHED("colsum_gate");
+  sum_slabs<<<(unsigned)((c + 31) / 32), 1024, 0, s>>>(part, (int)slabs, c, out);
   TCG_LAUNCHED("sum_slabs");
   return TCG_OK;
 }

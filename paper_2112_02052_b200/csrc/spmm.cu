@@ -11,6 +11,8 @@
 //    (test_acceptance.py:76-98).
 //  * TCG_PREC_TF32: the tensor-core row-window engine (window.cu, modes SPMM
 //    and SPMM_DUAL).
+#include <algorithm>
+
 #include "common.cuh"
 #include "window.cuh"
 
@@ -113,12 +115,59 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 using namespace tcg;
 
+namespace tcg {
+// ReLU over output rows [r0, r1) (absolute; stored at y[r - y_row0]), for the
+// engines that do not fuse it
+__global__ void spmm_relu_rows(float* __restrict__ y, int64_t ldy, int64_t r0, int64_t r1, int64_t y_row0, int dim) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t rows = r1 - r0;
+  if (i >= rows * dim) return;
+  const int64_t r = r0 + i / dim;
+  float* p = y + (r - y_row0) * ldy + i % dim;
+  *p = fmaxf(*p, 0.f);
+}
+}  // namespace tcg
+
+static int spmm_run(const tcg_tiling* t, const float* x, int64_t ldx, int64_t dim, const float* weights,
+                    const uint32_t* weight_idx, const float* x2, int64_t ldx2, const float* weights2,
+                    const uint32_t* weight_idx2, const float* bias, float* y, int64_t ldy, int64_t y_row0,
+                    int64_t win_begin, int64_t win_end, int32_t precision, int32_t accumulate, int relu,
+                    bool* fused, void* stream);
+
 extern "C" int tcg_spmm(const tcg_tiling* t, const float* x, int64_t ldx, int64_t dim,
                         const float* weights, const uint32_t* weight_idx, const float* x2,
                         int64_t ldx2, const float* weights2, const uint32_t* weight_idx2,
                         const float* bias, float* y, int64_t ldy, int64_t y_row0,
                         int64_t win_begin, int64_t win_end, int32_t precision, int32_t accumulate,
                         void* stream) {
+  bool fused = false;
+  return spmm_run(t, x, ldx, dim, weights, weight_idx, x2, ldx2, weights2, weight_idx2, bias, y, ldy, y_row0,
+                  win_begin, win_end, precision, accumulate, 0, &fused, stream);
+}
+
+extern "C" int tcg_spmm_act(const tcg_tiling* t, const float* x, int64_t ldx, int64_t dim,
+                            const float* weights, const uint32_t* weight_idx, const float* bias, float* y,
+                            int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
+                            int32_t precision, int32_t accumulate, int32_t act, void* stream) {
+  TCG_REQUIRE(act == TCG_ACT_NONE || act == TCG_ACT_RELU, "tcg_spmm_act: unknown activation %d", act);
+  bool fused = false;
+  const int rc = spmm_run(t, x, ldx, dim, weights, weight_idx, nullptr, 0, nullptr, nullptr, bias, y, ldy,
+                          y_row0, win_begin, win_end, precision, accumulate, act == TCG_ACT_RELU, &fused, stream);
+  if (rc != TCG_OK || act != TCG_ACT_RELU || fused || win_begin == win_end || t->num_nodes == 0) return rc;
+  const int64_t r0 = win_begin * t->blk_h, r1 = std::min<int64_t>(win_end * (int64_t)t->blk_h, t->num_nodes);
+  if (r1 <= r0) return TCG_OK;
+  const int64_t total = (r1 - r0) * dim;
+  tcg::spmm_relu_rows<<<(unsigned)((total + 255) / 256), 256, 0, as_stream(stream)>>>(y, ldy, r0, r1, y_row0,
+                                                                                   (int)dim);
+  TCG_LAUNCHED("relu_rows");
+  return TCG_OK;
+}
+
+static int spmm_run(const tcg_tiling* t, const float* x, int64_t ldx, int64_t dim, const float* weights,
+                    const uint32_t* weight_idx, const float* x2, int64_t ldx2, const float* weights2,
+                    const uint32_t* weight_idx2, const float* bias, float* y, int64_t ldy, int64_t y_row0,
+                    int64_t win_begin, int64_t win_end, int32_t precision, int32_t accumulate, int relu,
+                    bool* fused, void* stream) {
   TCG_REQUIRE(t != nullptr, "tcg_spmm: null tiling");
   TCG_REQUIRE(dim >= 1, "tcg_spmm: embedding dimension must be >= 1, got %lld", (long long)dim);
   TCG_REQUIRE(ldx >= dim && ldy >= dim, "tcg_spmm: leading dimension < dim");
@@ -210,10 +259,15 @@ extern "C" int tcg_spmm(const tcg_tiling* t, const float* x, int64_t ldx, int64_
   q.x = x, q.ldx = ldx, q.x2 = x2, q.ldx2 = ldx2;
   q.w = weights, q.widx = weight_idx, q.w2 = weights2, q.widx2 = weight_idx2;
   q.bias = bias, q.y = y, q.ldy = ldy, q.y_row0 = y_row0, q.accumulate = accumulate;
+  q.relu = relu;
   static const bool no_stream = std::getenv("TCG_NO_STREAM") != nullptr;
   if (!no_stream) {
     const int rc = stream_spmm(t, q, s);
-    if (rc != TCG_E_UNSUPPORTED) return rc;
+    if (rc != TCG_E_UNSUPPORTED) {
+      *fused = relu != 0;
+      return rc;
+    }
   }
+  q.relu = 0;
   return win::launch(x2 ? win::MODE_SPMM_DUAL : win::MODE_SPMM, nt, q, s);
 }

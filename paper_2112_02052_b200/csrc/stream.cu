@@ -125,6 +125,7 @@ struct Args {
   int accumulate;
   int vec_out;           // 16-B aligned output rows
   int x16;               // NT = 2: operand rows 16-B aligned (one 16-B copy per lane)
+  int relu;              // ReLU on the stored output (after bias / accumulate)
 };
 
 constexpr int kEPL = 5;    // edges per lane prefetched for the next window (160)
@@ -430,6 +431,10 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG, PAIR>::WPC * 32, 1) spmm_st
 #pragma unroll
         for (int q = 0; q < 2 * NT; ++q)
           if (!MASK || 2 * t * NT + q < a.dv) o[q] += yr[q];
+      }
+      if (a.relu) {
+#pragma unroll
+        for (int q = 0; q < 2 * NT; ++q) o[q] = fmaxf(o[q], 0.f);
       }
       if (MASK || !a.vec_out) {
         // lane t holds chunk features 2t NT .. 2t NT + 2NT
@@ -1404,6 +1409,7 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
   a.ldx = (int)q.ldx, a.ldx2 = (int)q.ldx2;
   a.x = q.x, a.x2 = q.x2, a.w = q.w, a.widx = q.widx, a.w2 = q.w2, a.widx2 = q.widx2;
   a.bias = q.bias, a.y = q.y, a.ldy = q.ldy, a.y_row0 = q.y_row0, a.accumulate = q.accumulate;
+  a.relu = q.relu;
   // big windows (products: ~400 edges each) stage their edges in shared memory
 #ifndef TCG_BIG_EPW
 #define TCG_BIG_EPW 256  // measured: amazon0601 (134 edges per window) is faster without staging
@@ -1420,7 +1426,7 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
     static const char* eng = std::getenv("TCG_SPMM_ENGINE");
     static const bool pair_off = std::getenv("TCG_NO_PAIRS") != nullptr;  // A/B: one block per step
     const bool use_tma = eng && std::strcmp(eng, "tma") == 0;
-    if (use_tma && !dual && !big && !mk && nt == 4) {
+    if (use_tma && !dual && !big && !mk && nt == 4 && !q.relu) {
       CUtensorMap tm;
       if (stream::make_row_map(&tm, q.x, q.n, q.dim, q.ldx)) {
         return stream::launch_tma<8, 8>(a, tm, nchunks, s);

@@ -55,6 +55,7 @@ struct Params {
   int64_t ldy;
   int64_t y_row0;
   int accumulate;
+  int relu;  // ReLU on the stored output (stream engine epilogue only)
   // SDDMM A operand (window rows) and edge outputs
   const float* xa;
   int64_t lda;

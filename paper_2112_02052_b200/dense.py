@@ -119,6 +119,23 @@ def colsum(x):
     return out
 
 
+def colsum_gate(x, gate):
+    """(x .* [gate > 0], its column sums): the ReLU backward fused with the bias
+    gradient (tcg_colsum_gate; fixed-order, deterministic)."""
+    lib = _lib.load()
+    n, c = x.shape
+    x = rows_ok(x)
+    gate = rows_ok(gate)
+    gout = rows_empty(n, c, x.device)
+    out = torch.empty(c, dtype=torch.float32, device=x.device)
+    wsb = int(lib.tcg_colsum_workspace_bytes(n, c))
+    ws = torch.empty(max(wsb // 4, 1), dtype=torch.float32, device=x.device)
+    _lib.check(lib.tcg_colsum_gate(x.data_ptr(), x.stride(0), gate.data_ptr(), gate.stride(0), n, c,
+                                   gout.data_ptr(), gout.stride(0), out.data_ptr(), ws.data_ptr(), wsb,
+                                   _stream()), "tcg_colsum_gate")
+    return gout, out
+
+
 def _labels(labels, n: int, device):
     """Class labels as the kernel reads them: int64, contiguous, 1-D of length
     n on the logits' device (int32 / host labels are converted, anything

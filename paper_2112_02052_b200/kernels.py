@@ -235,8 +235,9 @@ def _sddmm_counters(t: TiledGraph, d: int) -> Counters:
 
 def spmm_device(t: TiledGraph, x, weights=None, *, mode="tf32", out=None, bias=None,
                 accumulate=False, weight_idx=None, x2=None, weights2=None, weight_idx2=None,
-                win_range=None, y_row0=None):
-    """Raw SpMM launch: Y = A_w X (+ A_w2 X2) (+ bias), rows of `win_range`."""
+                win_range=None, y_row0=None, relu=False):
+    """Raw SpMM launch: Y = A_w X (+ A_w2 X2) (+ bias), rows of `win_range`;
+    relu=True (single operand) stores relu(Y) (tcg_spmm_act)."""
     import torch
 
     lib = _lib.load()
@@ -247,6 +248,15 @@ def spmm_device(t: TiledGraph, x, weights=None, *, mode="tf32", out=None, bias=N
         y_row0 = 0
     elif y_row0 is None:
         y_row0 = 0
+    if relu:
+        if x2 is not None:
+            raise ValueError("relu is supported for single-operand SpMM only")
+        _lib.check(lib.tcg_spmm_act(
+            C.byref(t.abi()), x.data_ptr(), x.stride(0), d, _ptr(weights), _ptr(weight_idx), _ptr(bias),
+            out.data_ptr(), out.stride(0), y_row0, wb, we,
+            _lib.PREC_TF32 if mode == "tf32" else _lib.PREC_F32, int(bool(accumulate)), _lib.ACT_RELU,
+            _stream()), "tcg_spmm_act")
+        return out
     _lib.check(lib.tcg_spmm(
         C.byref(t.abi()), x.data_ptr(), x.stride(0), d, _ptr(weights), _ptr(weight_idx),
         _ptr(x2), x2.stride(0) if x2 is not None else 0, _ptr(weights2), _ptr(weight_idx2),

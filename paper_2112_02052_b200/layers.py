@@ -39,6 +39,7 @@ from .dense import (  # noqa: F401  (re-exported)
     SoftmaxXentFn,
     colsum,
     LinearXentFn,
+    colsum_gate,
     cross_entropy,
     linear_cross_entropy,
     rows_empty,
@@ -82,26 +83,36 @@ def _rows16(x):
 
 
 class GcnAggregate(torch.autograd.Function):
-    """Y = A_w H + b, w = stored edge values (or 1)."""
+    """Y = A_w H + b, w = stored edge values (or 1); relu=True gives relu(Y)
+    with the ReLU in the SpMM epilogue and its backward fused with the bias
+    gradient (tcg_colsum_gate)."""
 
     @staticmethod
-    def forward(ctx, h, bias, t: TiledGraph, mode: str):
+    def forward(ctx, h, bias, t: TiledGraph, mode: str, relu: bool = False):
         h = _rows16(h) if mode == "tf32" else h.contiguous()
         out = _rows_out(t, h.shape[1], h)
-        spmm_device(t, h, _edge_weights(t), mode=mode, out=out, bias=bias)
-        ctx.t, ctx.mode = t, mode
+        spmm_device(t, h, _edge_weights(t), mode=mode, out=out, bias=bias, relu=relu)
+        ctx.t, ctx.mode, ctx.relu = t, mode, relu
         ctx.has_bias = bias is not None
+        if relu:
+            ctx.save_for_backward(out)
         return out
 
     @staticmethod
     def backward(ctx, g):
         t = ctx.t
+        db = None
+        if ctx.relu:  # g .* [Y > 0] and its column sums in one pass
+            (y,) = ctx.saved_tensors
+            g, cs = colsum_gate(g, y)
+            db = cs if ctx.has_bias else None
         g = _rows16(g) if ctx.mode == "tf32" else g.contiguous()
         tt = t.transpose()
         out = _rows_out(t, g.shape[1], g)
         spmm_device(tt.tiled, g, _edge_weights_t(t, tt.perm), mode=ctx.mode, out=out)
-        db = colsum(g) if ctx.has_bias else None
-        return out, db, None, None
+        if ctx.has_bias and not ctx.relu:
+            db = colsum(g)
+        return out, db, None, None, None
 
 
 def _edge_weights_t(t: TiledGraph, perm):
@@ -326,18 +337,20 @@ class GCNConv(nn.Module):
         self.aggregate_first = (order == "aggregate_first"
                                 or (order == "auto" and in_dim < out_dim))
 
-    def forward(self, x, t: TiledGraph, shard: Shard | None = None, key=None):
+    def forward(self, x, t: TiledGraph, shard: Shard | None = None, key=None, relu: bool = False):
+        """The layer's output (relu=True: relu of it, fused into the last kernel)."""
         if shard is not None:  # x: this rank's rows
             if self.aggregate_first:
                 h = GcnAggShard.apply(x, None, shard, key, self.mode)
-                return DenseFn.apply(h, self.weight, self.bias, False)
+                return DenseFn.apply(h, self.weight, self.bias, relu)
             h = DenseFn.apply(x, self.weight, None, False)
-            return GcnAggShard.apply(h, self.bias, shard, key, self.mode)
+            y = GcnAggShard.apply(h, self.bias, shard, key, self.mode)
+            return F.relu(y) if relu else y
         if self.aggregate_first:
-            h = GcnAggregate.apply(x, None, t, self.mode)
-            return DenseFn.apply(h, self.weight, self.bias, False)
+            h = GcnAggregate.apply(x, None, t, self.mode, False)
+            return DenseFn.apply(h, self.weight, self.bias, relu)
         h = DenseFn.apply(x, self.weight, None, False)
-        return GcnAggregate.apply(h, self.bias, t, self.mode)
+        return GcnAggregate.apply(h, self.bias, t, self.mode, relu)
 
     def loss(self, x, t: TiledGraph, labels, shard: Shard | None = None, key=None, div=None):
         """cross_entropy(self(x, t), labels) (sum / div with `div`); aggregate-first,
@@ -350,7 +363,7 @@ class GCNConv(nn.Module):
         if shard is not None:
             h = GcnAggShard.apply(x, None, shard, key, self.mode)
         else:
-            h = GcnAggregate.apply(x, None, t, self.mode)
+            h = GcnAggregate.apply(x, None, t, self.mode, False)
         return linear_cross_entropy(h, self.weight, self.bias, labels, div)
 
 
@@ -385,7 +398,7 @@ class GCN(nn.Module):
         if shard is not None:
             r0, r1 = shard.plan.my_rows
             x = x[r0:r1]
-        return self.c2(F.relu(self.c1(x, t, shard, 1)), t, shard, 2)
+        return self.c2(self.c1(x, t, shard, 1, relu=True), t, shard, 2)
 
     def loss(self, x, t, labels, shard=None):
         """Mean cross-entropy of the logits against labels (all N rows), the last
@@ -397,7 +410,7 @@ class GCN(nn.Module):
             div = shard.plan.num_nodes
         else:
             div = None
-        return self.c2.loss(F.relu(self.c1(x, t, shard, 1)), t, labels, shard, 2, div)
+        return self.c2.loss(self.c1(x, t, shard, 1, relu=True), t, labels, shard, 2, div)
 
 
 class AGNN(nn.Module):

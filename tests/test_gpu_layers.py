@@ -70,7 +70,7 @@ def test_gcn_backward_vs_oracle(env, oracle, weighted):
     gy = rng.standard_normal((2000, 16)).astype(np.float32)
     ht = torch.from_numpy(h).cuda().requires_grad_(True)
     bt = torch.from_numpy(b).cuda().requires_grad_(True)
-    y = layers.GcnAggregate.apply(ht, bt, t, "f32")
+    y = layers.GcnAggregate.apply(ht, bt, t, "f32", False)
     y.backward(torch.from_numpy(gy).cuda())
     ptr, cols = g.node_pointer, g.edge_list
     assert np.array_equal(y.detach().cpu().numpy(),
@@ -78,6 +78,31 @@ def test_gcn_backward_vs_oracle(env, oracle, weighted):
     dh = oracle.spmm_transpose(ptr, cols, gy, f=vals)
     assert np.array_equal(ht.grad.cpu().numpy(), dh)  # exact mode: same fold order
     np.testing.assert_allclose(bt.grad.cpu().numpy(), gy.sum(0), rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("mode", ["tf32", "f32"])
+@pytest.mark.parametrize("d", [16, 32])
+def test_gcn_aggregate_fused_relu(env, mode, d):
+    """relu=True (the ReLU in the SpMM epilogue, its backward fused with the bias
+    gradient in tcg_colsum_gate; f32 mode takes the separate ReLU pass) is
+    bitwise equal to F.relu of the plain layer, forward and backward."""
+    tcg, layers, torch = env
+    g = tcg.synth.gen_uniform(3000, 6, 9)
+    t = tcg.translate(g, tcg.BlockConfig())
+    gen = torch.Generator(device="cuda").manual_seed(d)
+    h = torch.randn(3000, d, device="cuda", generator=gen)
+    b = torch.randn(d, device="cuda", generator=gen)
+    gy = torch.randn(3000, d, device="cuda", generator=gen)
+    outs = []
+    for fused in (True, False):
+        ht, bt = h.clone().requires_grad_(True), b.clone().requires_grad_(True)
+        y = (layers.GcnAggregate.apply(ht, bt, t, mode, True) if fused
+             else torch.nn.functional.relu(layers.GcnAggregate.apply(ht, bt, t, mode, False)))
+        y.backward(gy)
+        outs.append((y.detach(), ht.grad, bt.grad))
+    for a, b_ in zip(*outs):
+        assert torch.equal(a, b_)
+    assert (outs[0][0] == 0).any() and (outs[0][0] > 0).any()
 
 
 def test_models_train_and_graph_capture(env):
