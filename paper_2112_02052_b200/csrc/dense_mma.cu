@@ -514,12 +514,19 @@ __global__ void __launch_bounds__(WPC * 32, 4) linear_xent(const float* __restri
       const int64_t row = tile * 16 + g + 8 * h;
       const float lse = lx_lse(v, bv, h);
       const bool ok = lab[h] >= 0 && lab[h] < c;
-      float ly = 0.f;  // the label's logit (held by one lane of the quad)
+      // the label's logit, held by lane t = (lab >> 1) & 3 of the quad: a select
+      // tree over the n-tiles (lab >> 3) instead of a compare per class
+      const int lb = (int)lab[h];
+      float cand[8];
 #pragma unroll
-      for (int j = 0; j < NTL; ++j)
+      for (int j = 0; j < 8; ++j) cand[j] = j < NTL ? ((lb & 1) ? v[j < NTL ? j : 0][2 * h + 1] : v[j < NTL ? j : 0][2 * h]) : 0.f;
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (8 * j + 2 * t + e == lab[h]) ly = v[j][2 * h + e];
+      for (int lvl = 0; lvl < 3; ++lvl) {
+        const bool bit = (lb >> (3 + lvl)) & 1;
+#pragma unroll
+        for (int i = 0; i < (4 >> lvl); ++i) cand[i] = bit ? cand[2 * i + 1] : cand[2 * i];
+      }
+      float ly = ((lb >> 1) & 3) == t ? cand[0] : 0.f;
       ly += __shfl_xor_sync(0xffffffffu, ly, 1);
       ly += __shfl_xor_sync(0xffffffffu, ly, 2);
       if (dl && row < n) {  // dl null: the loss only (the backward recomputes)
