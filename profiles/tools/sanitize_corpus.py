@@ -43,14 +43,31 @@ for g in graphs:
         worst = max(worst, float(np.linalg.norm(y.cpu().numpy() - yr) / np.linalg.norm(yr)))
         spmm_device(t, x, w, mode="f32")
         sddmm_device(t, x, mode="tf32")
+    for d in (32, 16, 12):  # masked D < 32 on the fused AGNN kernels (round 2)
+        z = torch.randn(n, d, device="cuda")
+        y, p = agnn_forward_device(t, z)
+        agnn_backward_device(t, z, torch.randn_like(z), p, y_fwd=y)
     z = torch.randn(n, 32, device="cuda")
-    y, p = agnn_forward_device(t, z)
-    agnn_backward_device(t, z, torch.randn_like(z), p, y_fwd=y)
     net = layers.AGNN(32, 32, 5, layers=2).cuda()
     lab = torch.randint(0, 5, (n,), device="cuda")
     layers.cross_entropy(net(z, t), lab).backward()
+    net.loss(z, t, lab).backward()  # fused output layer + loss (linear_xent, _bwd)
     gnet = layers.GCN(32, 16, 5).cuda()
     layers.cross_entropy(gnet(z, t), lab).backward()
+    gnet.loss(z, t, lab).backward()  # fused ReLU epilogue, tcg_colsum_gate, linear_xent
+# the round-2 dense tensor-core kernels at shapes that take them (n >= 4096 / wide inputs)
+from paper_2112_02052_b200 import dense  # noqa: E402
+for n, ci, co in ((4100, 128, 32), (4100, 100, 16), (1500, 300, 16), (1300, 1433, 32)):
+    x = dense.rows16(torch.randn(n, ci, device="cuda"))
+    wt = torch.randn(ci, co, device="cuda", requires_grad=True)
+    b = torch.randn(co, device="cuda", requires_grad=True)
+    dense.DenseFn.apply(x, wt, b, True).sum().backward()
+for n, kin, c in ((5000, 32, 47), (4097, 16, 40), (33, 12, 3)):
+    x = torch.randn(n, kin, device="cuda", requires_grad=True)
+    wt = torch.randn(kin, c, device="cuda", requires_grad=True)
+    b = torch.randn(c, device="cuda", requires_grad=True)
+    lab = torch.randint(0, c, (n,), device="cuda")
+    dense.linear_cross_entropy(x, wt, b, lab).backward()
 torch.cuda.synchronize()
 print(f"corpus ok, worst tf32 rel-L2 {worst:.2e}")
 assert worst <= 5e-3
