@@ -57,6 +57,30 @@ __global__ void __launch_bounds__(256) ldg_gather(const float4* __restrict__ x, 
   if (acc == 1234.5f) out[threadIdx.x] = acc;
 }
 
+// 64-B rows (D = 16): 4 lanes per row, 8 rows per warp instruction
+template <int UNR>
+__global__ void __launch_bounds__(256) ldg64_gather(const float4* __restrict__ x, const int* __restrict__ idx,
+                                                    long m, float* out) {
+  const int lane = threadIdx.x & 31;
+  const long gw = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((long)gridDim.x * blockDim.x) >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  float acc = 0.f;
+  for (long c = gw; c * 8 * UNR < m; c += nw) {
+    int id[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const long i = c * 8 * UNR + 8 * u + r;
+      id[u] = i < m ? __ldg(idx + i) : 0;
+    }
+    float4 v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) v[u] = __ldg(x + (size_t)id[u] * 4 + q);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  if (acc == 1234.5f) out[threadIdx.x] = acc;
+}
+
 // 96-B rows: lanes 0..29 -> 5 rows x 6 pieces of 16 B
 template <int UNR>
 __global__ void __launch_bounds__(256) ldg96_gather(const float4* __restrict__ x, const int* __restrict__ idx,
@@ -234,6 +258,40 @@ static float timeit(F f, int mode, int reps = 30) {
 }
 
 int main() {
+  if (getenv("GC_PRODUCTS")) {
+    // products-scale D = 16: 61.86 M random 64-B rows out of a 2.45 M-row (157 MB) X
+    const long N = 2449029, M = 61858832;
+    std::mt19937 rng(1);
+    std::vector<int> idx(M);
+    for (auto& v : idx) v = rng() % N;
+    float *x, *out;
+    int* di;
+    CK(cudaMalloc(&x, (size_t)N * 64));
+    CK(cudaMalloc(&di, 4 * M));
+    CK(cudaMalloc(&out, 1 << 24));
+    CK(cudaMalloc(&g_fl, 1024ull << 20));
+    g_out = out;
+    CK(cudaMemset(x, 0, (size_t)N * 64));
+    CK(cudaMemcpy(di, idx.data(), 4 * M, cudaMemcpyHostToDevice));
+    cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, 0);
+    const char* mn[3] = {"warm", "dirty", "clean"};
+    for (int cps : {4, 8}) {
+      for (int unr : {4, 8}) {
+        printf("ldg64 U=%d ctas/sm=%d (rows %.2f GB + ids %.2f GB)", unr, cps, M * 64 / 1e9, M * 4 / 1e9);
+        for (int mode = 0; mode < 3; ++mode) {
+          auto f = [&] {
+            if (unr == 4) ldg64_gather<4><<<g_nsm * cps, 256>>>((const float4*)x, di, M, out);
+            else ldg64_gather<8><<<g_nsm * cps, 256>>>((const float4*)x, di, M, out);
+          };
+          const float us = timeit(f, mode);
+          printf("  %s %7.1f us", mn[mode], us);
+        }
+        printf("\n");
+        CK(cudaGetLastError());
+      }
+    }
+    return 0;
+  }
   const int N = 169343, M = 1165855;
   std::mt19937 rng(1);
   std::vector<int> idx(M);
