@@ -293,6 +293,14 @@ int tcg_agnn_backward_fused(const tcg_tiling* t, const float* z, int64_t ldz, co
  * A^T SpMM. tcg_agnn_backward_fused does the same for dS when ds_t is given.
  * (Writing the A^T copy from the kernel epilogue was measured slower than
  * this separate coalesced-read scatter.) */
+/* tcg_agnn_forward plus the next AGNN layer's dense step in the same launch:
+ * z_next = Y w_next (w_next [dim x co] row-major, 3xTF32, fp32-class), for the
+ * stacked AGNNConv layers of the paper's model. D = co = 32
+ * runs fused in the forward kernel's epilogue; other shapes run the two steps.
+ * Rows of z_next follow y (y_row0). */
+int tcg_agnn_forward_next(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim, float* p,
+                          float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
+                          const float* w_next, int64_t co, float* z_next, int64_t ldzn, void* stream);
 int tcg_agnn_forward_t(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim, float* p,
                        float* p_t, const uint32_t* inv_perm, float* y, int64_t ldy,
                        int64_t y_row0, int64_t win_begin, int64_t win_end, void* stream);

@@ -112,6 +112,8 @@ SIGNATURES = {
                                      _SZ, _P]),
     "tcg_colsum_workspace_bytes": (_SZ, [_I64, _I64]),
     "tcg_colsum": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _SZ, _P]),
+    "tcg_agnn_forward_next": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _I64, _P, _P, _I64, _I64, _I64, _I64,
+                                        _P, _I64, _P, _I64, _P]),
     "tcg_colsum_gate": (C.c_int, [_P, _I64, _P, _I64, _I64, _I64, _P, _I64, _P, _P, _SZ, _P]),
     "tcg_spmm_act": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _I64,
                                _I64, _I32, _I32, _I32, _P]),

@@ -240,6 +240,26 @@ extern "C" int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz
   return win::launch(win::MODE_AGNN_FWD, nt, q, as_stream(stream));
 }
 
+extern "C" int tcg_agnn_forward_next(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim, float* p,
+                                     float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
+                                     const float* w_next, int64_t co, float* z_next, int64_t ldzn, void* stream) {
+  TCG_REQUIRE(t != nullptr && w_next && z_next && co >= 1 && ldzn >= co, "tcg_agnn_forward_next: bad arguments");
+  static const bool no_stream = std::getenv("TCG_NO_STREAM") != nullptr;
+  if (!no_stream && dim == 32 && co == 32 && t->num_edges > 0 && win_begin < win_end && z && p &&
+      y && t->blk_h == 16 && t->blk_w == 8 && row0_ok(t, win_begin, win_end, y_row0)) {
+    const int rc = stream_agnn(t, false, (int)dim, z, ldz, z, ldz, nullptr, 0, nullptr, p, y, ldy, y_row0,
+                               win_begin, win_end, as_stream(stream), w_next, z_next, ldzn);
+    if (rc != TCG_E_UNSUPPORTED) return rc;
+  }
+  // the two-step form: the aggregation, then the dense step on its rows
+  const int rc = tcg_agnn_forward(t, z, ldz, dim, p, y, ldy, y_row0, win_begin, win_end, stream);
+  if (rc != TCG_OK || win_begin == win_end) return rc;
+  const int64_t r0 = win_begin * t->blk_h, r1 = std::min<int64_t>(win_end * (int64_t)t->blk_h, t->num_nodes);
+  if (r1 <= r0) return TCG_OK;
+  return tcg_dense(y + (r0 - y_row0) * ldy, ldy, r1 - r0, dim, w_next, co, 0, nullptr, 0, nullptr, 0,
+                   z_next + (r0 - y_row0) * ldzn, ldzn, stream);
+}
+
 extern "C" int tcg_agnn_forward_t(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim,
                                   float* p, float* p_t, const uint32_t* inv_perm, float* y,
                                   int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,

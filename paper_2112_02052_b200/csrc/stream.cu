@@ -886,6 +886,9 @@ struct AgnnArgs {
   int64_t ldy, y_row0;
   int epi;           // SDDMM-only launches: TCG_EPI_*
   int dv;            // MASK launches: valid features (a multiple of 4, < 32); the rest read as 0
+  const float* wn;   // NEXT (fwd): the next layer's W (32 x 32, row-major); zn = Y wn
+  float* zn;
+  int64_t ldzn;
 };
 
 constexpr float kTau = 8.f;  // lazy-rescale threshold of the online softmax (natural log)
@@ -924,7 +927,11 @@ __device__ __forceinline__ uint32_t agnn_off(int r, int c) {
 // MASK: D < 32 (a multiple of 4) run in the D = 32 layout with the missing
 // features zero-filled by the copies (src-size 0) and never stored: the scores,
 // softmax and products are those of the D-wide rows.
-template <int KIND, bool PAIR = false, bool MASK = false>
+// NEXT (forward, D = 32): the epilogue also computes the next layer's dense step
+// Zn = Y Wn (3xTF32 mma.sync; Y staged through the window's slot-map area, free
+// at the window end; Wn as tf32 hi / lo after the warps' areas), so Y is not
+// read back by a separate GEMM.
+template <int KIND, bool PAIR = false, bool MASK = false, bool NEXT = false>
 __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const AgnnArgs a) {
   using C = AgnnCfg<KIND>;
   constexpr bool BWD = KIND == 1;   // 0: forward, 1: backward A-side, 2: SDDMM only
@@ -953,6 +960,16 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
   const int64_t TBr = B1 - B0;
   const int lo_b = B0 + (int)(TBr * gw / a.nwarps);
   const int hi_b = B0 + (int)(TBr * (gw + 1) / a.nwarps);
+  float* wnh = reinterpret_cast<float*>(smem + C::WPC * C::WARP);  // NEXT: [2][32][32]
+  if constexpr (NEXT) {
+    for (int i = threadIdx.x; i < 1024; i += C::WPC * 32) {
+      const float v = __ldg(a.wn + i);
+      const float hi = __uint_as_float(tf32_rn(v));
+      wnh[i] = hi;
+      wnh[1024 + i] = __uint_as_float(tf32_rn(v - hi));
+    }
+    __syncthreads();
+  }
   const int ws = warp_lower_bound(a.boff, a.win_begin, a.win_end, lo_b);
   const int we = gw + 1 == a.nwarps ? a.win_end : warp_lower_bound(a.boff, ws, a.win_end, hi_b);
   if (ws >= we) return;
@@ -1280,31 +1297,87 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
         yr[1] = make_float4(acc[0][2 * h + 1] * inv[h], acc[1][2 * h + 1] * inv[h],
                             acc[2][2 * h + 1] * inv[h], acc[3][2 * h + 1] * inv[h]);
     }
+    if constexpr (NEXT) {
+      // Y tile (rows g / g + 8, features 8t .. 8t + 7 per lane) into the map area as a
+      // 16 x 32 tile, 16-B chunk c of row r at r * 128 + ((c ^ (r & 7)) << 4)
+      const uint32_t ts = smem_u32(map);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rr = g + 8 * h;
+        const float4 v0 = make_float4(acc[0][2 * h] * inv[h], acc[1][2 * h] * inv[h], acc[2][2 * h] * inv[h],
+                                      acc[3][2 * h] * inv[h]);
+        const float4 v1 = make_float4(acc[0][2 * h + 1] * inv[h], acc[1][2 * h + 1] * inv[h],
+                                      acc[2][2 * h + 1] * inv[h], acc[3][2 * h + 1] * inv[h]);
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(ts + rr * 128 + (((2 * t) ^ (rr & 7)) << 4)),
+                     "f"(v0.x), "f"(v0.y), "f"(v0.z), "f"(v0.w) : "memory");
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(ts + rr * 128 + (((2 * t + 1) ^ (rr & 7)) << 4)),
+                     "f"(v1.x), "f"(v1.y), "f"(v1.z), "f"(v1.w) : "memory");
+      }
+      __syncwarp();
+      // Zn = Y Wn, n-tile j column n <-> output 4n + j (each lane's outputs contiguous)
+      float zc[4][4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) zc[j][0] = zc[j][1] = zc[j][2] = zc[j][3] = 0.f;
+      const int mm = lane >> 3, r8 = (lane & 7) + 8 * (mm & 1);
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) {
+        uint32_t av4[4], ah[4], al[4];
+        const int c = 2 * kc + (mm >> 1);
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                     : "=r"(av4[0]), "=r"(av4[1]), "=r"(av4[2]), "=r"(av4[3])
+                     : "r"(ts + r8 * 128 + ((c ^ (r8 & 7)) << 4)));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          ah[i] = tf32_rn(__uint_as_float(av4[i]));
+          al[i] = tf32_rn(__uint_as_float(av4[i]) - __uint_as_float(ah[i]));
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k0 = 8 * kc + t, col = 4 * g + j;
+          const uint32_t bh0 = __float_as_uint(wnh[k0 * 32 + col]), bh1 = __float_as_uint(wnh[(k0 + 4) * 32 + col]);
+          const uint32_t bl0 = __float_as_uint(wnh[1024 + k0 * 32 + col]),
+                         bl1 = __float_as_uint(wnh[1024 + (k0 + 4) * 32 + col]);
+          mma_tf32(zc[j], al[0], al[1], al[2], al[3], bh0, bh1);
+          mma_tf32(zc[j], ah[0], ah[1], ah[2], ah[3], bl0, bl1);
+          mma_tf32(zc[j], ah[0], ah[1], ah[2], ah[3], bh0, bh1);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t r = (int64_t)w * 16 + g + 8 * h;
+        if (r >= a.n) continue;
+        float4* zr = reinterpret_cast<float4*>(a.zn + (r - a.y_row0) * a.ldzn + 8 * t);
+        zr[0] = make_float4(zc[0][2 * h], zc[1][2 * h], zc[2][2 * h], zc[3][2 * h]);
+        zr[1] = make_float4(zc[0][2 * h + 1], zc[1][2 * h + 1], zc[2][2 * h + 1], zc[3][2 * h + 1]);
+      }
+      __syncwarp();  // the map area is cleared by the next window's InitSparse
+    }
     cb0 = cb1, cb1 = nb2, nb2 = nb3, nb3 = blk_of(w + 4);
     e0 = e1, e1 = e2, e2 = e3, e3 = ptr_of(w + 4);
   }
   cp_wait<0>();
 }
 
-template <int KIND, bool PAIR = false, bool MASK = false>
+template <int KIND, bool PAIR = false, bool MASK = false, bool NEXT = false>
 int launch_agnn(AgnnArgs& a, cudaStream_t s) {
   using C = AgnnCfg<KIND>;
-  auto kern = agnn_stream<KIND, PAIR, MASK>;
+  auto kern = agnn_stream<KIND, PAIR, MASK, NEXT>;
+  constexpr int SMEM = C::SMEM + (NEXT ? 2 * 1024 * 4 : 0);
   static int configured = -1;
   int dev = 0;
   TCG_CUDA(cudaGetDevice(&dev), "agnn_stream device");
   if (configured != dev) {
-    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
+    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM),
              "agnn_stream attr");
     configured = dev;
   }
   int per_sm = 1;
-  TCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPC * 32, C::SMEM),
+  TCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPC * 32, SMEM),
            "agnn_stream occupancy");
   if (per_sm < 1) per_sm = 1;
   const int64_t ctas = (int64_t)num_sms() * per_sm;
   a.nwarps = (int)(ctas * C::WPC);
-  kern<<<(unsigned)ctas, C::WPC * 32, C::SMEM, s>>>(a);
+  kern<<<(unsigned)ctas, C::WPC * 32, SMEM, s>>>(a);
   TCG_LAUNCHED(KIND == 1 ? "agnn_stream_bwd" : KIND == 0 ? "agnn_stream_fwd" : "sddmm_stream");
   return TCG_OK;
 }
@@ -1498,7 +1571,7 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
 int stream_agnn(const tcg_tiling* t, bool bwd, int dim, const float* z, int64_t ldz, const float* za,
                 int64_t lda, const float* yf, int64_t ldyf, const float* pin, float* eout,
                 float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
-                cudaStream_t s) {
+                cudaStream_t s, const float* wn, float* zn, int64_t ldzn) {
   if (dim < 4 || dim > 32 || dim % 4) return TCG_E_UNSUPPORTED;
   if (!t->block_offsets || !t->col_stream || !t->edge_frag) return TCG_E_UNSUPPORTED;
   if (t->max_window_edges <= 0 || t->max_window_edges > stream::kMaxE ||
@@ -1516,6 +1589,13 @@ int stream_agnn(const tcg_tiling* t, bool bwd, int dim, const float* z, int64_t 
   a.dv = dim;
   const bool mk = dim < 32;
   static const bool pair_off = std::getenv("TCG_NO_PAIRS") != nullptr;
+  if (wn) {  // forward with the next layer's dense step in the epilogue (D = 32)
+    if (bwd || mk || !zn || !al(zn) || ldzn % 4 || !t->pair_offsets || !t->pair_stream || pair_off)
+      return TCG_E_UNSUPPORTED;
+    a.wn = wn, a.zn = zn, a.ldzn = ldzn;
+    a.boff = t->pair_offsets, a.cs = t->pair_stream;
+    return stream::launch_agnn<0, true, false, true>(a, s);
+  }
   // forward: two blocks per step (arxiv 59.4 -> 55.3 us cold); the backward
   // measured slower that way (55.3 -> 57.3 us with the coalesced dS writes,
   // 59.5 -> 63.5 us before) and keeps one block per step

@@ -87,6 +87,6 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s);
 int stream_agnn(const tcg_tiling* t, bool bwd, int dim, const float* z, int64_t ldz, const float* za,
                 int64_t lda, const float* yf, int64_t ldyf, const float* pin, float* eout,
                 float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
-                cudaStream_t s);
+                cudaStream_t s, const float* wn = nullptr, float* zn = nullptr, int64_t ldzn = 0);
 
 }  // namespace tcg

@@ -342,6 +342,30 @@ def agnn_forward_device(t: TiledGraph, z, *, p=None, out=None, win_range=None, y
     return out, p
 
 
+def agnn_forward_next_device(t: TiledGraph, z, w_next, *, p=None, out=None, z_next=None):
+    """tcg_agnn_forward_next: (Y, P, Y @ w_next), the next layer's dense step in
+    the forward kernel's epilogue at D = 32 (3xTF32)."""
+    import torch
+
+    from .dense import rows_empty
+
+    lib = _lib.load()
+    n = t.num_nodes
+    co = w_next.shape[1]
+    if p is None:
+        p = torch.empty(max(t.num_edges, 1), dtype=torch.float32, device=z.device)
+    if out is None:
+        out = torch.empty((n, z.shape[1]), dtype=torch.float32, device=z.device)
+    if z_next is None:
+        z_next = rows_empty(n, co, z.device)
+    w_next = w_next.contiguous()
+    _lib.check(lib.tcg_agnn_forward_next(C.byref(t.abi()), z.data_ptr(), z.stride(0), z.shape[1],
+                                         p.data_ptr(), out.data_ptr(), out.stride(0), 0, 0,
+                                         t.num_row_windows, w_next.data_ptr(), co, z_next.data_ptr(),
+                                         z_next.stride(0), _stream()), "tcg_agnn_forward_next")
+    return out, p, z_next
+
+
 def agnn_backward_device(t: TiledGraph, z, gy, p, *, ds=None, out=None, win_range=None,
                          y_row0=0, y_fwd=None, ds_t=None, inv_perm=None):
     """A-side half of the AGNN backward (tcg_agnn_backward): returns (dZ_A, dS)

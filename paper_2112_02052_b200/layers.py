@@ -35,6 +35,7 @@ from . import _lib
 from .dist import Shard, allgather_edges, allgather_rows
 from .dense import (  # noqa: F401  (re-exported)
     DenseFn,
+    dense_backward,
     Linear,
     SoftmaxXentFn,
     colsum,
@@ -46,6 +47,7 @@ from .dense import (  # noqa: F401  (re-exported)
     rows_ok,
 )
 from .kernels import (
+    agnn_forward_next_device,
     agnn_backward_device,
     agnn_forward_device,
     invert_perm_device,
@@ -170,6 +172,9 @@ _PERMUTE_WEIGHTS = os.environ.get("TCG_GATHER_WEIGHTS") is None
 # was measured slower (1.22 vs 1.15 ms / epoch) and is not offered.
 _FUSED_PT = os.environ.get("TCG_FUSED_PT") is not None
 
+# AGNN model: the next layer's dense step in the AGNN forward epilogue (opt-in, see AGNN._trunk)
+_AGNN_NEXT = os.environ.get("TCG_AGNN_NEXT") == "1"
+
 
 def _inv_perm(t: TiledGraph):
     """A^T position of every A edge (cached per tiling)."""
@@ -207,33 +212,59 @@ class AgnnAggregate(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g):
         z, p, y_fwd, p_t = ctx.saved_tensors
-        t, mode = ctx.t, ctx.mode
-        g = g.contiguous()
-        m = t.num_edges
-        out = _rows_out(t, z.shape[1], z)
-        if m == 0:
-            out.zero_()
-            return out, None, None
-        ds = torch.empty(m, dtype=torch.float32, device=z.device)
-        ds_t = torch.empty(m, dtype=torch.float32, device=z.device) if p_t is not None else None
-        if mode == "tf32":
-            # dS and A_dS Z from one gather of Z's neighbour rows (dS also in A^T order)
-            agnn_backward_device(t, z, g, p, ds=ds, out=out, y_fwd=y_fwd, ds_t=ds_t,
-                                 inv_perm=_inv_perm(t) if ds_t is not None else None)
-        else:
-            sddmm_device(t, g, z, mode=mode, epilogue=_lib.EPI_SOFTMAX_BWD, aux=p, out=ds)
-            spmm_device(t, z, ds, mode=mode, out=out)
-        tt = t.transpose()
-        # one dual SpMM on A^T: A^T_P G + A^T_dS Z
-        if p_t is not None:
-            spmm_device(tt.tiled, g, p_t, x2=z, weights2=ds_t, mode=mode, out=out, accumulate=True)
-        elif mode == "tf32" and not _PERMUTE_WEIGHTS:
-            spmm_device(tt.tiled, g, p, weight_idx=tt.perm, x2=z, weights2=ds, weight_idx2=tt.perm,
-                        mode=mode, out=out, accumulate=True)
-        else:
-            pt, dst = permute2_device(p, ds, tt.perm)
-            spmm_device(tt.tiled, g, pt, x2=z, weights2=dst, mode=mode, out=out, accumulate=True)
-        return out, None, None
+        return _agnn_backward(ctx.t, ctx.mode, z, p, y_fwd, p_t, g), None, None
+
+
+def _agnn_backward(t: TiledGraph, mode: str, z, p, y_fwd, p_t, g):
+    """dZ of Y = spmm(A, P; Z) for the incoming gradient g: the A-side
+    (dS = P (dP - rowsum), A_dS Z) and one dual SpMM on A^T (A^T_P G + A^T_dS Z)."""
+    g = g.contiguous()
+    m = t.num_edges
+    out = _rows_out(t, z.shape[1], z)
+    if m == 0:
+        out.zero_()
+        return out
+    ds = torch.empty(m, dtype=torch.float32, device=z.device)
+    ds_t = torch.empty(m, dtype=torch.float32, device=z.device) if p_t is not None else None
+    if mode == "tf32":
+        # dS and A_dS Z from one gather of Z's neighbour rows (dS also in A^T order)
+        agnn_backward_device(t, z, g, p, ds=ds, out=out, y_fwd=y_fwd, ds_t=ds_t,
+                             inv_perm=_inv_perm(t) if ds_t is not None else None)
+    else:
+        sddmm_device(t, g, z, mode=mode, epilogue=_lib.EPI_SOFTMAX_BWD, aux=p, out=ds)
+        spmm_device(t, z, ds, mode=mode, out=out)
+    tt = t.transpose()
+    # one dual SpMM on A^T: A^T_P G + A^T_dS Z
+    if p_t is not None:
+        spmm_device(tt.tiled, g, p_t, x2=z, weights2=ds_t, mode=mode, out=out, accumulate=True)
+    elif mode == "tf32" and not _PERMUTE_WEIGHTS:
+        spmm_device(tt.tiled, g, p, weight_idx=tt.perm, x2=z, weights2=ds, weight_idx2=tt.perm,
+                    mode=mode, out=out, accumulate=True)
+    else:
+        pt, dst = permute2_device(p, ds, tt.perm)
+        spmm_device(tt.tiled, g, pt, x2=z, weights2=dst, mode=mode, out=out, accumulate=True)
+    return out
+
+
+class AgnnAggregateNext(torch.autograd.Function):
+    """Z_next = AGNN(Z) W_next: an AGNN aggregation and the next layer's dense
+    step in one launch (tcg_agnn_forward_next; D = 32 on the tensor cores). The
+    backward is the dense backward (dY = dZ_next W_nextᵀ, dW_next = Yᵀ dZ_next,
+    one pass) followed by the AGNN backward."""
+
+    @staticmethod
+    def forward(ctx, z, w_next, t: TiledGraph, mode: str):
+        z = z.contiguous()
+        y, p, zn = agnn_forward_next_device(t, z, w_next, out=_rows_out(t, z.shape[1], z))
+        ctx.save_for_backward(z, p, y, w_next)
+        ctx.t, ctx.mode = t, mode
+        return zn
+
+    @staticmethod
+    def backward(ctx, gzn):
+        z, p, y, w = ctx.saved_tensors
+        gy, dw = dense_backward(y, rows_ok(gzn), w.contiguous())
+        return _agnn_backward(ctx.t, ctx.mode, z, p, y, None, gy), dw, None, None
 
 
 class AgnnAggShard(torch.autograd.Function):
@@ -425,15 +456,30 @@ class AGNN(nn.Module):
         self.convs = nn.ModuleList([AGNNConv(hidden, hidden, mode, gen) for _ in range(layers)])
         self.lin_out = Linear(hidden, classes, bias=True, gen=gen)
 
+    def _trunk(self, x, t, shard=None):
+        """The last AGNN layer's output. With TCG_AGNN_NEXT=1 (unsharded, TF32)
+        each aggregation also computes the next layer's Z = Y W in its epilogue
+        (AgnnAggregateNext); measured even with the separate GEMM at arxiv
+        (0.900-0.915 vs 0.910 ms / epoch: the epilogue adds 11.4 us to each
+        forward launch, the GEMM it replaces took 11), so it is opt-in."""
+        h = self.lin_in(x)
+        convs = list(self.convs)
+        if (not _AGNN_NEXT or shard is not None or not convs
+                or any(c.mode != "tf32" for c in convs)):
+            for i, c in enumerate(convs):
+                h = c(h, t, shard, i)
+            return h
+        z = DenseFn.apply(h, convs[0].weight, None, False)
+        for c in convs[1:]:
+            z = AgnnAggregateNext.apply(z, c.weight, t, c.mode)
+        return AgnnAggregate.apply(z, t, convs[-1].mode)
+
     def forward(self, x, t, shard=None):
         """Logits of all rows, or with a Shard of this rank's rows (x: all rows)."""
         if shard is not None:
             r0, r1 = shard.plan.my_rows
             x = x[r0:r1]
-        h = self.lin_in(x)
-        for i, c in enumerate(self.convs):
-            h = c(h, t, shard, i)
-        return self.lin_out(h)
+        return self.lin_out(self._trunk(x, t, shard))
 
     def loss(self, x, t, labels, shard=None):
         """Mean cross-entropy of the logits against labels with lin_out fused
@@ -443,9 +489,7 @@ class AGNN(nn.Module):
             r0, r1 = shard.plan.my_rows
             x, labels = x[r0:r1], labels[r0:r1]
             div = shard.plan.num_nodes
-        h = self.lin_in(x)
-        for i, c in enumerate(self.convs):
-            h = c(h, t, shard, i)
+        h = self._trunk(x, t, shard)
         lo = self.lin_out
         if lo.relu:
             return cross_entropy(lo(h), labels) if div is None else \

@@ -105,6 +105,68 @@ def test_gcn_aggregate_fused_relu(env, mode, d):
     assert (outs[0][0] == 0).any() and (outs[0][0] > 0).any()
 
 
+@pytest.mark.parametrize("kind", ["uniform", "hub"])
+def test_agnn_aggregate_next(env, kind):
+    """AgnnAggregateNext (the next layer's Z = Y W in the AGNN forward kernel's
+    epilogue) against AgnnAggregate followed by DenseFn: forward and gradients
+    within fp32-class tolerance (both 3xTF32), and the fused kernel is what runs
+    (on the hub graph the > 255-edge windows take the two-step form)."""
+    tcg, layers, torch = env
+    from torch.profiler import ProfilerActivity, profile
+
+    if kind == "uniform":
+        g = tcg.synth.gen_uniform(4000, 7, 11)
+    else:
+        rng = np.random.default_rng(3)
+        n = 3000
+        src = np.concatenate([rng.integers(0, n, n * 5), np.repeat(np.arange(3), 400)])
+        dst = np.concatenate([rng.integers(0, n, n * 5), rng.integers(0, n, 1200)])
+        g = tcg.CsrGraph.from_edges(src, dst, n)
+    t = tcg.translate(g, tcg.BlockConfig())
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    z = torch.randn(g.num_nodes, 32, device="cuda", generator=gen)
+    w = torch.randn(32, 32, device="cuda", generator=gen) / 32 ** 0.5
+    gz = torch.randn(g.num_nodes, 32, device="cuda", generator=gen)
+    res = []
+    for fused in (True, False):
+        zt, wt = z.clone().requires_grad_(True), w.clone().requires_grad_(True)
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            if fused:
+                zn = layers.AgnnAggregateNext.apply(zt, wt, t, "tf32")
+            else:
+                zn = layers.DenseFn.apply(layers.AgnnAggregate.apply(zt, t, "tf32"), wt, None, False)
+            torch.cuda.synchronize()
+        if fused and kind == "uniform":
+            names = [e.name for e in prof.events()]
+            assert any("agnn_stream<0, true, false, true>" in nm or "agnn_stream<0, 1, 0, 1>" in nm
+                       for nm in names), names
+        zn.backward(gz)
+        res.append((zn.detach(), zt.grad, wt.grad))
+    for a, b in zip(*res):
+        assert rel_l2(a.cpu().numpy(), b.cpu().numpy()) < 2e-6
+
+
+def test_agnn_model_next_layer_fusion(env, monkeypatch):
+    """The AGNN model with the next layer's dense step fused into each AGNN
+    forward (TCG_AGNN_NEXT=1) against the default: same loss and gradients
+    within fp32-class tolerance."""
+    tcg, layers, torch = env
+    g = tcg.synth.gen_uniform(5000, 7, 13)
+    t = tcg.translate(g, tcg.BlockConfig())
+    x = torch.randn(5000, 64, device="cuda")
+    lab = torch.randint(0, 7, (5000,), device="cuda")
+    out = []
+    for fused in (False, True):
+        monkeypatch.setattr(layers, "_AGNN_NEXT", fused)
+        torch.manual_seed(0)
+        net = layers.AGNN(64, 32, 7, layers=3).cuda()
+        loss = net.loss(x, t, lab)
+        loss.backward()
+        out.append([loss.detach()] + [p.grad.detach().clone() for p in net.parameters()])
+    for a, b in zip(*out):
+        assert rel_l2(a.reshape(-1).cpu().numpy(), b.reshape(-1).cpu().numpy()) < 1e-5
+
+
 def test_models_train_and_graph_capture(env):
     tcg, layers, torch = env
     g = tcg.synth.gen_uniform(5000, 7, 2)
