@@ -828,6 +828,284 @@ int launch_tma(Args& a, const CUtensorMap& tm, int nchunks, cudaStream_t s) {
   return TCG_OK;
 }
 
+// ---- warp-specialised TMA gather (round 2) --------------------------------------
+//
+// spmm_tma above makes every consumer warp issue its own gathers, so the TMA issue
+// (a waterfall over the lanes holding row ids) and the id copies sit on the same
+// serial chain as the mma. Here one producer warp per CTA issues the gathers of
+// all NCW consumer warps: producer lane c walks consumer c's contiguous slice of
+// the block stream, polls the slot's `empty` barrier (non-blocking), and issues
+// the block's two tile::gather4 (8 rows, 1 KB) with complete_tx on `full`. The
+// consumers only wait, read two LDS.128 + one fragment LDS.128 and run the 4 mma.
+// Row layout in a slot and the 128-B swizzle are those of spmm_tma.
+template <int NCW_, int NS_, int MB_>
+struct WsCfg {
+  static constexpr int NCW = NCW_, NS = NS_, MB = MB_;
+  static constexpr int RING = NS * 1024;
+  static constexpr int AFR = MB * 512;
+  static constexpr int WARP = (RING + AFR + 1023) & ~1023;
+  static constexpr int BARS = 2 * NCW * NS * 8;
+  static constexpr int THREADS = (NCW + 1) * 32;
+  static constexpr int SMEM = NCW * WARP + BARS + 1024;
+};
+
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+template <int NCW_, int NS_, int MB_, int MINB>
+__global__ void __launch_bounds__(WsCfg<NCW_, NS_, MB_>::THREADS, MINB)
+    spmm_ws(const Args a, const __grid_constant__ CUtensorMap tmx) {
+  using C = WsCfg<NCW_, NS_, MB_>;
+  constexpr int NCW = C::NCW, NS = C::NS, MB = C::MB;
+  constexpr uint32_t RS = MB * 128;
+  extern __shared__ unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bars = base + NCW * C::WARP;  // full[c][s], then empty[c][s]
+  auto full_bar = [&](int c, int s) { return bars + 8u * (uint32_t)(c * NS + s); };
+  auto empty_bar = [&](int c, int s) { return bars + 8u * (uint32_t)(NCW * NS + c * NS + s); };
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 2 * NCW * NS; ++q) mbar_init(bars + 8 * q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int B0 = __ldg(a.boff + a.win_begin), B1 = __ldg(a.boff + a.win_end);
+  const int64_t TBr = B1 - B0;
+  // window range of consumer gw (whole warp)
+  auto range_of = [&](int gw, int& ws, int& we) {
+    const int lo_b = B0 + (int)(TBr * gw / a.nwarps);
+    const int hi_b = B0 + (int)(TBr * (gw + 1) / a.nwarps);
+    ws = warp_lower_bound(a.boff, a.win_begin, a.win_end, lo_b);
+    we = gw + 1 == a.nwarps ? a.win_end : warp_lower_bound(a.boff, ws, a.win_end, hi_b);
+    if (we < ws) we = ws;
+  };
+  const int xcol = a.d0 + blockIdx.y * 32;
+
+  if (wid == NCW) {
+    // ---- producer: lane c serves consumer c ----
+    int my_gb0 = 0, my_nb = 0;
+    for (int c = 0; c < NCW; ++c) {
+      int ws, we;
+      range_of(blockIdx.x * NCW + c, ws, we);
+      if (lane == c && ws < we) {
+        my_gb0 = __ldg(a.boff + ws);
+        my_nb = __ldg(a.boff + we) - my_gb0;
+      }
+    }
+    const int c = lane < NCW ? lane : 0;
+    const uint4* ids = reinterpret_cast<const uint4*>(a.cs + 8 * (int64_t)my_gb0);
+    const uint32_t ring = base + c * C::WARP;
+    int b = 0;
+    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0;
+    if (my_nb > 0) r0 = __ldg(ids), r1 = __ldg(ids + 1);
+    while (__any_sync(0xffffffffu, b < my_nb)) {
+      if (b < my_nb) {
+        const int s = b % NS;
+        const bool ready = b < NS || mbar_test(empty_bar(c, s), (uint32_t)((b / NS) - 1) & 1u);
+        if (ready) {
+          const uint32_t fb = full_bar(c, s);
+          mbar_expect_tx(fb, 1024);
+          tma_gather4(ring + s * 1024, &tmx, xcol, r0, fb);
+          tma_gather4(ring + s * 1024 + 512, &tmx, xcol, r1, fb);
+          ++b;
+          if (b < my_nb) r0 = __ldg(ids + 2 * b), r1 = __ldg(ids + 2 * b + 1);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warp `wid` ----
+  int ws, we;
+  range_of(blockIdx.x * NCW + wid, ws, we);
+  if (ws >= we) return;
+  const int g = lane >> 2, t = lane & 3;
+  const uint32_t ring = base + wid * C::WARP;
+  const uint32_t afr_s = ring + C::RING;
+  uint32_t* afr = reinterpret_cast<uint32_t*>(smem_raw + (afr_s - smem_u32(smem_raw)));
+  const int gb0 = __ldg(a.boff + ws);
+  const int nb = __ldg(a.boff + we) - gb0;
+
+  auto ptr_of = [&](int w) { return (int64_t)__ldg(a.ptr + min((int64_t)w * 16, a.n)); };
+  auto blk_of = [&](int w) { return __ldg(a.boff + min(w, a.win_end)) - gb0; };
+  int w = ws;
+  int cb0 = 0, cb1 = blk_of(ws + 1), nb2 = blk_of(ws + 2), nb3 = blk_of(ws + 3);
+  int64_t e0 = ptr_of(ws), e1 = ptr_of(ws + 1), e2 = ptr_of(ws + 2), e3 = ptr_of(ws + 3);
+  uint32_t pf[kEPL], of[kEPL];
+  float pw[kEPL], ow[kEPL];
+  auto weight = [&](int64_t e) {
+    return a.w ? (a.widx ? __ldg(a.w + __ldg(a.widx + e)) : __ldg(a.w + e)) : 1.f;
+  };
+  auto prefetch = [&](int64_t lo, int64_t hi) {
+#pragma unroll
+    for (int k = 0; k < kEPL; ++k) {
+      const int64_t e = lo + lane + 32 * k;
+      const bool ok = e < hi;
+      pf[k] = ok ? __ldg(a.efrag + e) : 0xffffffffu;
+      pw[k] = ok ? weight(e) : 0.f;
+    }
+  };
+  auto clear_frags = [&]() {
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < MB; ++q) reinterpret_cast<uint4*>(afr)[q * 32 + lane] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+  };
+  auto put_round = [&](uint32_t lo, bool zero) {
+#pragma unroll
+    for (int k = 0; k < kEPL; ++k) {
+      const uint32_t f = of[k] - lo;
+      if (f < RS) afr[f] = zero ? 0u : tf32_rn(ow[k]);
+    }
+  };
+  auto hub_load = [&](int r0) {
+    clear_frags();
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const uint32_t f = __ldg(a.efrag + e) - (uint32_t)(r0 * 128);
+      if (f < RS) afr[f] = tf32_rn(weight(e));
+    }
+    __syncwarp();
+  };
+  float acc[4][4];
+  auto store = [&]() {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t r = (int64_t)w * 16 + g + 8 * h;
+      if (r >= a.n) continue;
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] = acc[j][2 * h] + 0.f, o[4 + j] = acc[j][2 * h + 1] + 0.f;
+      const int fo = xcol + 8 * t;
+      float* yr = a.y + (r - a.y_row0) * a.ldy + fo;
+      if (a.bias) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] += __ldg(a.bias + fo + q);
+      }
+      if (a.accumulate) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] += yr[q];
+      }
+      if (a.relu) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] = fmaxf(o[q], 0.f);
+      }
+      if (!a.vec_out) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) yr[q] = o[q];
+      } else {
+        reinterpret_cast<float4*>(yr)[0] = make_float4(o[0], o[1], o[2], o[3]);
+        reinterpret_cast<float4*>(yr)[1] = make_float4(o[4], o[5], o[6], o[7]);
+      }
+    }
+  };
+  bool hub = false;
+  auto begin_window = [&]() {
+#pragma unroll
+    for (int k = 0; k < kEPL; ++k) of[k] = pf[k], ow[k] = pw[k];
+    hub = e1 - e0 > 32 * kEPL;
+    __syncwarp();
+    if (!hub) {
+      put_round(0, false);
+      __syncwarp();
+    } else {
+      hub_load(0);
+    }
+    prefetch(e1, e2);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  };
+  auto end_window = [&]() {
+    store();
+    const int nbw = cb1 - cb0;
+    __syncwarp();
+    if (!hub) {
+      put_round((uint32_t)(nbw > 0 ? ((nbw - 1) & ~(MB - 1)) : 0) * 128, true);
+    } else {
+      clear_frags();
+    }
+    ++w;
+    cb0 = cb1, cb1 = nb2, nb2 = nb3, nb3 = blk_of(w + 3);
+    e0 = e1, e1 = e2, e2 = e3, e3 = ptr_of(w + 3);
+  };
+
+  const uint32_t b0o = (2 * t) * 128 + ((g ^ (2 * t)) & 7) * 16;
+  const uint32_t b1o = (2 * t + 1) * 128 + ((g ^ (2 * t + 1)) & 7) * 16;
+  const uint32_t as = afr_s + lane * 16;
+  clear_frags();
+  prefetch(e0, e1);
+  begin_window();
+  for (int s = 0; s < nb; ++s) {
+    while (s == cb1) {
+      end_window();
+      begin_window();
+    }
+    const int lb = s - cb0;
+    if (lb > 0 && (lb & (MB - 1)) == 0) {
+      if (!hub) {
+        __syncwarp();
+        put_round((uint32_t)(lb - MB) * 128, true);
+        __syncwarp();
+        put_round((uint32_t)lb * 128, false);
+        __syncwarp();
+      } else {
+        hub_load(lb);
+      }
+    }
+    const int sl = s % NS;
+    const uint32_t slot = ring + sl * 1024;
+    mbar_wait(full_bar(wid, sl), (uint32_t)(s / NS) & 1u);
+    {
+      float x0[4], x1[4];
+      lds_slice<4>(x0, slot + b0o);
+      lds_slice<4>(x1, slot + b1o);
+      const uint4 af = lds_frag(as + (uint32_t)(lb & (MB - 1)) * 512);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_bar(wid, sl));
+  }
+  for (;;) {
+    end_window();
+    if (w >= we) break;
+    begin_window();
+  }
+}
+
+template <int NCW, int NS, int MB, int MINB>
+int launch_ws(Args& a, const CUtensorMap& tm, int nchunks, cudaStream_t s) {
+  using C = WsCfg<NCW, NS, MB>;
+  auto kern = spmm_ws<NCW, NS, MB, MINB>;
+  static int configured = -1;
+  int dev = 0;
+  TCG_CUDA(cudaGetDevice(&dev), "spmm_ws device");
+  if (configured != dev) {
+    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM),
+             "spmm_ws attr");
+    configured = dev;
+  }
+  int per_sm = 1;
+  TCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM),
+           "spmm_ws occupancy");
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ctas = (int64_t)num_sms() * per_sm;
+  a.nwarps = (int)(ctas * NCW);
+  dim3 grid((unsigned)ctas, (unsigned)nchunks);
+  kern<<<grid, C::THREADS, C::SMEM, s>>>(a, tm);
+  TCG_LAUNCHED("spmm_ws");
+  return TCG_OK;
+}
+
 // 2-D tensor map over X (rows = nodes, inner = features), 32-feature boxes of one
 // row, 128-B swizzle: the operand of tile::gather4. false when it cannot be made.
 bool make_row_map(CUtensorMap* tm, const float* x, int64_t rows, int64_t dim, int64_t ld) {
@@ -1499,6 +1777,23 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
     static const char* eng = std::getenv("TCG_SPMM_ENGINE");
     static const bool pair_off = std::getenv("TCG_NO_PAIRS") != nullptr;  // A/B: one block per step
     const bool use_tma = eng && std::strcmp(eng, "tma") == 0;
+    const bool use_ws = eng && std::strcmp(eng, "ws") == 0;
+    if (use_ws && !dual && !mk && nt == 4) {
+      CUtensorMap tm;
+      if (stream::make_row_map(&tm, q.x, q.n, q.dim, q.ldx)) {
+        static const char* wc = std::getenv("TCG_WS_CFG");
+        const int cfg = wc ? std::atoi(wc) : 0;
+        switch (cfg) {
+          case 1: return stream::launch_ws<8, 6, 8, 2>(a, tm, nchunks, s);
+          case 2: return stream::launch_ws<4, 4, 8, 4>(a, tm, nchunks, s);
+          case 3: return stream::launch_ws<8, 4, 8, 3>(a, tm, nchunks, s);
+          case 4: return stream::launch_ws<12, 4, 8, 2>(a, tm, nchunks, s);
+          case 5: return stream::launch_ws<8, 8, 8, 2>(a, tm, nchunks, s);
+          case 6: return stream::launch_ws<6, 4, 8, 3>(a, tm, nchunks, s);
+          default: return stream::launch_ws<8, 4, 8, 2>(a, tm, nchunks, s);
+        }
+      }
+    }
     if (use_tma && !dual && !big && !mk && nt == 4 && !q.relu) {
       CUtensorMap tm;
       if (stream::make_row_map(&tm, q.x, q.n, q.dim, q.ldx)) {

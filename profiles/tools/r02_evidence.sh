@@ -3,7 +3,7 @@
 # every workload, the reference arm, ncu launch lists of the bench command and of
 # one AGNN / GCN epoch, and ncu --set full of the dense tensor-core kernels.
 set -u
-O=gpurun_out/r02e
+O=${OUT:-gpurun_out/r02e}
 mkdir -p $O
 python bench.py > $O/bench_line.json 2> $O/bench_line.err
 python bench.py --impl reference > $O/bench_reference_line.json 2> $O/bench_reference_line.err
@@ -18,4 +18,7 @@ for k in agnn gcn; do
 done
 ncu --set full --import-source on --clock-control none -k regex:"dense_in_mma|gemm_tn_mma|linear_xent|mma32" \
   -c 8 -o $O/dense_mma_full python profiles/tools/epoch_prof.py agnn > /dev/null 2>&1
+ls -la $O
+ncu --set full --import-source on --clock-control none -k regex:"spmm_stream" -s 5 -c 1 \
+  -o $O/roofline_spmm_full python profiles/tools/ws_ab.py arxiv 32 > /dev/null 2>&1
 ls -la $O
