@@ -54,6 +54,8 @@ for _ in range(5):
     run()
 torch.cuda.synchronize()
 eng = os.environ.get("TCG_SPMM_ENGINE", "default") + os.environ.get("TCG_WS_CFG", "")
+if os.environ.get("TCG_SPMM_PF"):
+    eng += "+pf" + os.environ["TCG_SPMM_PF"] + "/" + os.environ.get("TCG_SPMM_PFD", "16")
 refp = f"gpurun_out/ws_ref_{name}_{D}.pt"
 if eng == "default":
     torch.save(out.cpu(), refp)
