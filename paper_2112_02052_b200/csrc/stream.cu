@@ -1660,6 +1660,217 @@ int launch_agnn(AgnnArgs& a, cudaStream_t s) {
   return TCG_OK;
 }
 
+// ---- SDDMM for wide windows (round 2) ------------------------------------------
+//
+// agnn_stream<2> keeps a u8 slot map of the window's first 24 blocks and its
+// scores in a 256-entry buffer, so products-like windows (~400 edges, ~50
+// blocks) fell back to the window engine (7.1 ms at products D = 16). This
+// variant takes windows of up to kWideE edges: the slot map is u16 and covers a
+// round of kWideRB blocks, rebuilt per round by two lanes per row walking their
+// row's edges (within a row the edges are sorted by column, hence by block, so
+// each edge's fragment slot is read once per window); scores, the per-edge row
+// and the row epilogue (raw / softmax / softmax backward) are those of
+// agnn_stream<2> with kWideE-entry buffers. One block per step.
+constexpr int kWideE = 1024;
+constexpr int kWideRB = 16;
+struct WideCfg {
+  static constexpr int NB = 4, NI = 8;
+  static constexpr int RING = NB * 1024;
+  static constexpr int IDX = NI * 32;
+  static constexpr int MAP = kWideRB * 128 * 2;  // u16 per fragment slot: local edge + 1
+  static constexpr int ESC = kWideE * 4;
+  static constexpr int ROW = 64 * 4;
+  static constexpr int EROW = kWideE;
+  static constexpr int WARP = RING + IDX + MAP + ESC + ROW + EROW;
+  static constexpr int WPC = 8;
+  static constexpr int SMEM = WPC * WARP;
+};
+
+template <bool MASK>
+__global__ void __launch_bounds__(WideCfg::WPC * 32, 2) sddmm_wide(const AgnnArgs a) {
+  using C = WideCfg;
+  constexpr int NB = C::NB, NI = C::NI;
+  constexpr uint32_t RS = kWideRB * 128;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gw = blockIdx.x * C::WPC + wid;
+  const int g = lane >> 2, t = lane & 3;
+  unsigned char* wsm = smem + wid * C::WARP;
+  const uint32_t ring = smem_u32(wsm);
+  const uint32_t iring = ring + C::RING;
+  const unsigned char* iring_p = wsm + C::RING;
+  uint16_t* map = reinterpret_cast<uint16_t*>(wsm + C::RING + C::IDX);
+  float* esc = reinterpret_cast<float*>(wsm + C::RING + C::IDX + C::MAP);
+  float* rowm = esc + kWideE;
+  float* rowl = rowm + 16;
+  float* rowrs = rowl + 16;
+  unsigned char* erow = reinterpret_cast<unsigned char*>(esc + kWideE + 64);
+
+  const int B0 = __ldg(a.boff + a.win_begin), B1 = __ldg(a.boff + a.win_end);
+  const int64_t TBr = B1 - B0;
+  const int lo_b = B0 + (int)(TBr * gw / a.nwarps);
+  const int hi_b = B0 + (int)(TBr * (gw + 1) / a.nwarps);
+  const int ws = warp_lower_bound(a.boff, a.win_begin, a.win_end, lo_b);
+  const int we = gw + 1 == a.nwarps ? a.win_end : warp_lower_bound(a.boff, ws, a.win_end, hi_b);
+  if (ws >= we) return;
+  const int gb0 = __ldg(a.boff + ws);
+
+  const char* xb = reinterpret_cast<const char*>(a.z + g * 4);
+  const uint32_t xrow = (uint32_t)a.ldz * 4u;
+  const uint32_t so0 = agnn_off(t, g), so1 = agnn_off(t + 4, g);
+  const int pr = (g >> 1) + 4 * (g & 1);
+  const uint32_t sd0 = agnn_off(pr, t), sd1 = agnn_off(pr, t + 4);
+  const uint32_t* csw = a.cs + 8 * (int64_t)gb0;
+  auto issue_idx = [&](int s) {
+    if (lane < 2) cp_async<16>(iring + (s & (NI - 1)) * 32 + lane * 16, csw + 8 * (int64_t)s + 4 * lane);
+  };
+  const int xvb = MASK ? (4 * g < a.dv ? 16 : 0) : 16;
+  auto issue_x = [&](int s) {
+    const uint2 id = *reinterpret_cast<const uint2*>(iring_p + (s & (NI - 1)) * 32 + 8 * t);
+    const uint32_t sb = ring + (s & (NB - 1)) * 1024;
+    if constexpr (MASK) {
+      const void* z0 = a.z;
+      cp_async_n<16>(sb + so0, xvb ? (const void*)(xb + (uint64_t)id.x * xrow) : z0, xvb);
+      cp_async_n<16>(sb + so1, xvb ? (const void*)(xb + (uint64_t)id.y * xrow) : z0, xvb);
+    } else {
+      cp_async<16>(sb + so0, xb + (uint64_t)id.x * xrow);
+      cp_async<16>(sb + so1, xb + (uint64_t)id.y * xrow);
+    }
+  };
+  for (int s = 0; s < NB; ++s) issue_idx(s);
+  cp_commit();
+  cp_wait<0>();
+  __syncwarp();
+  for (int s = 0; s < NB; ++s) {
+    issue_x(s);
+    issue_idx(s + NB);
+    cp_commit();
+  }
+
+  auto ptr_of = [&](int w) { return (int64_t)__ldg(a.ptr + min((int64_t)w * 16, a.n)); };
+  auto blk_of = [&](int w) { return __ldg(a.boff + min(w, a.win_end)) - gb0; };
+  int cb0 = 0, cb1 = blk_of(ws + 1);
+  int64_t e0 = ptr_of(ws), e1 = ptr_of(ws + 1);
+  float4 own[4];
+  const uint32_t* map32 = reinterpret_cast<const uint32_t*>(map);
+  int s = 0;
+  for (int w = ws; w < we; ++w) {
+    const int nbw = cb1 - cb0;
+    const int ne = (int)(e1 - e0);
+    // own rows (SDDMM A operand): rows g, g+8; features 4t.. and 4(t+4)..
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int64_t r = (int64_t)w * 16 + g + 8 * (h & 1);
+      const int f = 4 * (t + 4 * (h >> 1));
+      const bool ok = r < a.n && (!MASK || f < a.dv);
+      own[h] = ok ? __ldg(reinterpret_cast<const float4*>(a.za + r * a.lda + f)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    // two lanes per row: the row's edges [rb, re) (window-local)
+    const int r = lane >> 1, sub = lane & 1;
+    const int64_t rg = (int64_t)w * 16 + r;
+    const bool live = rg < a.n;
+    const int rb = live ? (int)(__ldg(a.ptr + rg) - e0) : 0;
+    const int re = live ? (int)(__ldg(a.ptr + rg + 1) - e0) : 0;
+    __syncwarp();
+    for (int j = rb + sub; j < re; j += 2) erow[j] = (unsigned char)r;
+    int rc = rb + sub;  // this lane's cursor into its row's edges
+    uint32_t ao[4][4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      ao[h][0] = tf32_rn(own[h].x), ao[h][1] = tf32_rn(own[h].y);
+      ao[h][2] = tf32_rn(own[h].z), ao[h][3] = tf32_rn(own[h].w);
+    }
+    for (int lb = 0; lb < nbw; ++lb, ++s) {
+      if (lb % kWideRB == 0) {  // slot map of blocks [lb, lb + kWideRB)
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < (int)(RS * 2 / 16 / 32); ++q)
+          reinterpret_cast<uint4*>(map)[q * 32 + lane] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        const uint32_t lo = (uint32_t)lb * 128;
+        while (rc < re) {
+          const uint32_t f = __ldg(a.efrag + e0 + rc) - lo;
+          if (f >= RS) break;  // this row's next edges belong to a later round
+          map[f] = (uint16_t)(rc + 1);
+          rc += 2;
+        }
+        __syncwarp();
+      }
+      cp_wait<NB - 1>();
+      __syncwarp();
+      const uint32_t sb = ring + (s & (NB - 1)) * 1024;
+      float sc[4] = {0.f, 0.f, 0.f, 0.f};
+      float b0[4], b1[4];
+      lds_slice<4>(b0, sb + sd0);
+      lds_slice<4>(b1, sb + sd1);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) mma_tf32_rb(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], b0[j], b1[j]);
+      const float v[4] = {sc[0], sc[2], sc[1], sc[3]};
+      const uint2 mw = reinterpret_cast<const uint2*>(map32)[(lb % kWideRB) * 32 + lane];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t ej = ((q < 2 ? mw.x : mw.y) >> (16 * (q & 1))) & 0xffffu;
+        if (ej) esc[ej - 1] = v[q];
+      }
+      __syncwarp();
+      issue_x(s + NB);
+      issue_idx(s + 2 * NB);
+      cp_commit();
+    }
+    // StoreSparse + the row epilogue (as agnn_stream<2>)
+    __syncwarp();
+    if (a.epi == TCG_EPI_NONE) {
+      for (int j = lane; j < ne; j += 32) a.eout[e0 + j] = esc[j];
+    } else if (a.epi == TCG_EPI_SOFTMAX) {
+      float mx = -INFINITY;
+      for (int j = rb + sub; j < re; j += 2) mx = fmaxf(mx, esc[j]);
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      float sm = 0.f;
+      for (int j = rb + sub; j < re; j += 2) sm += expf(esc[j] - mx);
+      sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+      if (sub == 0) rowm[r] = mx, rowl[r] = sm;
+      __syncwarp();
+      for (int j = lane; j < ne; j += 32) {
+        const int q = erow[j];
+        a.eout[e0 + j] = expf(esc[j] - rowm[q]) / rowl[q];
+      }
+    } else {
+      float rsum = 0.f;
+      for (int j = rb + sub; j < re; j += 2) rsum += __ldg(a.pin + e0 + j) * esc[j];
+      rsum += __shfl_xor_sync(0xffffffffu, rsum, 1);
+      if (sub == 0) rowrs[r] = rsum;
+      __syncwarp();
+      for (int j = lane; j < ne; j += 32) a.eout[e0 + j] = __ldg(a.pin + e0 + j) * (esc[j] - rowrs[erow[j]]);
+    }
+    __syncwarp();
+    cb0 = cb1, cb1 = blk_of(w + 2);
+    e0 = e1, e1 = ptr_of(w + 2);
+  }
+  cp_wait<0>();
+}
+
+template <bool MASK>
+int launch_wide(AgnnArgs& a, cudaStream_t s) {
+  using C = WideCfg;
+  auto kern = sddmm_wide<MASK>;
+  static int configured = -1;
+  int dev = 0;
+  TCG_CUDA(cudaGetDevice(&dev), "sddmm_wide device");
+  if (configured != dev) {
+    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM), "sddmm_wide attr");
+    configured = dev;
+  }
+  int per_sm = 1;
+  TCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WPC * 32, C::SMEM),
+           "sddmm_wide occupancy");
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ctas = (int64_t)num_sms() * per_sm;
+  a.nwarps = (int)(ctas * C::WPC);
+  kern<<<(unsigned)ctas, C::WPC * 32, C::SMEM, s>>>(a);
+  TCG_LAUNCHED("sddmm_wide");
+  return TCG_OK;
+}
+
 // ---- tiling preprocessing ---------------------------------------------------
 
 // block_offsets[w] = sum of win_partition[0..w) (single CTA; once per tiling)
@@ -1909,8 +2120,9 @@ int stream_sddmm(const tcg_tiling* t, int dim, const float* xa, int64_t lda, con
                  cudaStream_t s) {
   if (dim < 4 || dim > 32 || dim % 4) return TCG_E_UNSUPPORTED;
   if (!t->block_offsets || !t->col_stream || !t->edge_frag) return TCG_E_UNSUPPORTED;
-  if (t->max_window_edges <= 0 || t->max_window_edges > stream::kMaxE ||
-      t->max_window_unique > 8 * stream::kMapB)
+  // windows past the u8 slot map (products-like degree) take the wide variant
+  const bool wide = t->max_window_edges > stream::kMaxE || t->max_window_unique > 8 * stream::kMapB;
+  if (t->max_window_edges <= 0 || t->max_window_edges > (wide ? stream::kWideE : stream::kMaxE))
     return TCG_E_UNSUPPORTED;
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (!al(xa) || !al(xb) || lda % 4 || ldb % 4) return TCG_E_UNSUPPORTED;
@@ -1923,6 +2135,8 @@ int stream_sddmm(const tcg_tiling* t, int dim, const float* xa, int64_t lda, con
   a.dv = dim;
   const bool mk = dim < 32;
   static const bool pair_off = std::getenv("TCG_NO_PAIRS") != nullptr;
+  static const bool wide_all = std::getenv("TCG_SDDMM_WIDE") != nullptr;  // test hook: every window
+  if (wide || wide_all) return mk ? stream::launch_wide<true>(a, s) : stream::launch_wide<false>(a, s);
   if (t->pair_offsets && t->pair_stream && !pair_off) {
     a.boff = t->pair_offsets, a.cs = t->pair_stream;
     return mk ? stream::launch_agnn<2, true, true>(a, s) : stream::launch_agnn<2, true>(a, s);

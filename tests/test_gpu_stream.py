@@ -393,3 +393,54 @@ def test_tma_gather_engine_opt_in(tmp_path):
                        text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) <= TF32_REL_L2
+
+
+def test_ws_gather_engine_opt_in(tmp_path):
+    """The opt-in warp-specialised TMA gather4 SpMM (TCG_SPMM_ENGINE=ws: one
+    producer warp per CTA; measured slower, profiles/r02/spmm_engines_ab.txt)
+    matches the oracle (32- and 64-wide operands; the masked 40-wide tail takes
+    the ring)."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    env = dict(os.environ, TCG_SPMM_ENGINE="ws")
+    r = subprocess.run([sys.executable, "-c", _TMA_SCRIPT, str(ROOT)], env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= TF32_REL_L2
+
+
+@pytest.mark.parametrize("dim", [8, 16, 32])
+def test_stream_sddmm_wide_windows(env, oracle, dim):
+    """Products-like windows (~480 edges, up to ~900 with the hub rows): the
+    wide SDDMM (u16 slot map rebuilt per 16-block round) with each epilogue,
+    against the oracle; the launch is sddmm_wide, not the window engine."""
+    tcg, kernels, _, torch = env
+    from paper_2112_02052_b200 import _lib
+
+    rng = np.random.default_rng(100 + dim)
+    n = 2000
+    src = np.concatenate([rng.integers(0, n, n * 30), np.repeat(np.arange(16), 25)])
+    dst = np.concatenate([rng.integers(0, n, n * 30), rng.integers(0, n, 16 * 25)])
+    g = tcg.CsrGraph.from_edges(src, dst, n)
+    t = tcg.translate(g, tcg.BlockConfig())
+    ptr, cols = g.node_pointer, g.edge_list
+    wmax = int(np.diff(ptr[::16]).max())
+    assert 255 < wmax <= 1024, wmax
+    xa = rng.standard_normal((n, dim)).astype(np.float32)
+    xb = rng.standard_normal((n, dim)).astype(np.float32)
+    xat, xbt = torch.from_numpy(xa).cuda(), torch.from_numpy(xb).cuda()
+    res = {}
+    names = _kernel_names(torch, lambda: res.update(s=kernels.sddmm_device(t, xat, xbt)))
+    assert any("sddmm_wide" in k for k in names), names
+    s_ref = oracle.sddmm(ptr, cols, xa, xb)
+    assert rel_l2(res["s"].cpu().numpy(), s_ref) <= TF32_REL_L2
+    p = kernels.sddmm_device(t, xat, epilogue=_lib.EPI_SOFTMAX)
+    p_ref = oracle.segment_softmax(oracle.sddmm(ptr, cols, xa), ptr)
+    assert rel_l2(p.cpu().numpy(), p_ref) <= TF32_REL_L2
+    ds = kernels.sddmm_device(t, xat, xbt, epilogue=_lib.EPI_SOFTMAX_BWD, aux=torch.from_numpy(p_ref).cuda())
+    ds_ref = oracle.softmax_backward(p_ref, s_ref, ptr)
+    assert rel_l2(ds.cpu().numpy(), ds_ref) <= TF32_REL_L2
