@@ -119,6 +119,14 @@ bool fits_fused(const tcg_tiling* t, int nt) {
          t->max_window_unique <= win::cols_per_round(nt, win::MODE_AGNN_FWD);
 }
 
+// windows too wide for the fused stream kernels: the two-step form on the block
+// stream (sddmm_wide + row epilogue, then the stream SpMM) beats the window
+// engine's fused kernels there (products D=16: the SDDMM alone 7.1 -> 1.7 ms)
+bool wide_two_step(const tcg_tiling* t, int64_t dim) {
+  static const bool off = std::getenv("TCG_NO_STREAM") != nullptr || std::getenv("TCG_AGNN_WIN_FUSED") != nullptr;
+  return !off && dim <= 32 && dim % 4 == 0 && stream_sddmm_wide(t);
+}
+
 }  // namespace
 }  // namespace tcg
 
@@ -220,7 +228,7 @@ extern "C" int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz
                                win_begin, win_end, as_stream(stream));
     if (rc != TCG_E_UNSUPPORTED) return rc;
   }
-  if (t->num_edges == 0 || dim > 64 || !fits_fused(t, nt)) {
+  if (t->num_edges == 0 || dim > 64 || !fits_fused(t, nt) || wide_two_step(t, dim)) {
     if (t->num_edges) {
       int rc = tcg_sddmm(t, z, ldz, z, ldz, dim, nullptr, p, win_begin, win_end, TCG_PREC_TF32,
                          TCG_EPI_SOFTMAX, stream);
@@ -315,7 +323,7 @@ extern "C" int tcg_agnn_backward(const tcg_tiling* t, const float* z, int64_t ld
   TCG_REQUIRE(row0_ok(t, win_begin, win_end, dz_row0),
               "tcg_agnn_backward: dz_row0 %lld beyond first output row", (long long)dz_row0);
   const int nt = win::nt_for(dim);
-  if (t->num_edges == 0 || dim > 64 || !fits_fused(t, nt)) {
+  if (t->num_edges == 0 || dim > 64 || !fits_fused(t, nt) || wide_two_step(t, dim)) {
     if (t->num_edges) {
       int rc = tcg_sddmm(t, gy, ldg, z, ldz, dim, p, ds, win_begin, win_end, TCG_PREC_TF32,
                          TCG_EPI_SOFTMAX_BWD, stream);

@@ -2113,6 +2113,14 @@ int stream_agnn(const tcg_tiling* t, bool bwd, int dim, const float* z, int64_t 
   return mk ? stream::launch_agnn<0, false, true>(a, s) : stream::launch_agnn<0>(a, s);
 }
 
+// true when the tiling's windows are past the fused stream kernels' slot map but
+// within sddmm_wide's
+bool stream_sddmm_wide(const tcg_tiling* t) {
+  return t->block_offsets && t->col_stream && t->edge_frag && t->max_window_edges > 0 &&
+         (t->max_window_edges > stream::kMaxE || t->max_window_unique > 8 * stream::kMapB) &&
+         t->max_window_edges <= stream::kWideE;
+}
+
 // SDDMM (+ softmax / softmax-backward row epilogue) on the block stream, D <= 32
 // (a multiple of 4; D < 32 runs masked)
 int stream_sddmm(const tcg_tiling* t, int dim, const float* xa, int64_t lda, const float* xb, int64_t ldb,

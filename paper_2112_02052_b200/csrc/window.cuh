@@ -84,6 +84,7 @@ int stream_sddmm(const tcg_tiling* t, int dim, const float* xa, int64_t lda, con
                  const float* aux, float* out, int epi, int64_t win_begin, int64_t win_end,
                  cudaStream_t s);
 int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s);
+bool stream_sddmm_wide(const tcg_tiling* t);
 int stream_agnn(const tcg_tiling* t, bool bwd, int dim, const float* z, int64_t ldz, const float* za,
                 int64_t lda, const float* yf, int64_t ldyf, const float* pin, float* eout,
                 float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
