@@ -48,6 +48,44 @@ std::atomic<int64_t>& launch_counter();
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// The epoch's kernels are launched with programmatic stream serialisation: a
+// kernel's CTAs may be scheduled while its predecessor drains, and block in
+// griddepcontrol.wait (TCG_PDL_ENTRY, the first statement of every such kernel)
+// until the predecessor has completed and its writes are visible. Nothing is
+// read or written before the wait, so the semantics are those of plain stream
+// order; what overlaps is the launch and CTA rasterisation with the
+// predecessor's tail. TCG_PDL=0 turns it off (A/B).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#ifndef TCG_PDL_TRIGGER
+#define TCG_PDL_TRIGGER 0
+#endif
+#define TCG_PDL_ENTRY()                   \
+  do {                                    \
+    ::tcg::pdl_wait();                    \
+    if (TCG_PDL_TRIGGER) ::tcg::pdl_trigger(); \
+  } while (0)
+bool pdl_enabled();
+template <typename... P, typename... A>
+inline void launch_pdl(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+  if (!pdl_enabled()) {
+    k<<<grid, block, smem, s>>>(static_cast<P>(args)...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, static_cast<P>(args)...);
+}
+
 int num_sms();
 
 // ---- numerics ---------------------------------------------------------------

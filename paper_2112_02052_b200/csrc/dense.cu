@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(1024) sum_slabs(const float* __restrict__ part, int slabs,
                                                   int64_t len, float* __restrict__ out,
                                                   int64_t split = INT64_MAX, float* __restrict__ out2 = nullptr) {
+  TCG_PDL_ENTRY();
   // 32 outputs x 32 slab groups per CTA (the partial count is ~300-600, so
   // every thread keeps ~10-20 independent loads in flight); the groups are
   // combined in a fixed order (deterministic)
@@ -188,6 +189,7 @@ __global__ void __launch_bounds__(256)
     softmax_xent(const float* __restrict__ logits, int64_t ld, const int64_t* __restrict__ labels,
                  int64_t n, int c, float* __restrict__ dlogits, int64_t ldd,
                  const float* __restrict__ gscale, float* __restrict__ lpart, int64_t parts) {
+  TCG_PDL_ENTRY();
   __shared__ float rowc[32];
   const int sub = threadIdx.x & 7, lr_ = threadIdx.x >> 3;
   const int64_t row = (int64_t)blockIdx.x * 32 + lr_;
@@ -233,6 +235,7 @@ __global__ void __launch_bounds__(256)
 
 __global__ void final_loss(const float* __restrict__ lpart, int64_t parts, int64_t n,
                            float* __restrict__ loss) {
+  TCG_PDL_ENTRY();
   __shared__ float sh[256];
   float s = 0.f;
   for (int64_t i = threadIdx.x; i < parts; i += 256) s += lpart[i];
@@ -421,6 +424,7 @@ __global__ void __launch_bounds__(256)
     colsum_part(const float* __restrict__ x, int64_t ld, int64_t n, int c, int64_t rows,
                 float* __restrict__ part, const float* __restrict__ gate = nullptr, int64_t ldg = 0,
                 float* __restrict__ gout = nullptr, int64_t ldo = 0) {
+  TCG_PDL_ENTRY();
   using VT = typename std::conditional<V == 4, float4, float>::type;
   __shared__ VT sh[256];
   const int units = c / V;
@@ -602,10 +606,10 @@ extern "C" int tcg_gemm_tn(const float* a, int64_t lda, const float* b, int64_t 
       rc = fast_gemm_tn(a, lda, b, ldb, mask, ldm, n, (int)k, (int)c, part, colsum ? colpart : nullptr,
                         slabs, &used, s);
     if (rc == TCG_OK) {
-      sum_slabs<<<(unsigned)((k * c + 31) / 32), 1024, 0, s>>>(part, (int)used, k * c, out);
+      ::tcg::launch_pdl(sum_slabs, (unsigned)((k * c + 31) / 32), 1024, 0, s, part, (int)used, k * c, out, (int64_t)INT64_MAX, (float*)nullptr);
       TCG_LAUNCHED("sum_slabs");
       if (colsum) {
-        sum_slabs<<<(unsigned)((c + 31) / 32), 1024, 0, s>>>(colpart, (int)used, c, colsum);
+        ::tcg::launch_pdl(sum_slabs, (unsigned)((c + 31) / 32), 1024, 0, s, colpart, (int)used, c, colsum, (int64_t)INT64_MAX, (float*)nullptr);
         TCG_LAUNCHED("sum_slabs");
       }
       return TCG_OK;
@@ -616,10 +620,10 @@ extern "C" int tcg_gemm_tn(const float* a, int64_t lda, const float* b, int64_t 
   gemm_tn_partial<<<grid, 256, 0, s>>>(a, lda, b, ldb, mask, ldm, n, (int)k, (int)c, rows, part,
                                        colsum ? colpart : nullptr);
   TCG_LAUNCHED("gemm_tn_partial");
-  sum_slabs<<<(unsigned)((k * c + 31) / 32), 1024, 0, s>>>(part, (int)slabs, k * c, out);
+  ::tcg::launch_pdl(sum_slabs, (unsigned)((k * c + 31) / 32), 1024, 0, s, part, (int)slabs, k * c, out, (int64_t)INT64_MAX, (float*)nullptr);
   TCG_LAUNCHED("sum_slabs");
   if (colsum) {
-    sum_slabs<<<(unsigned)((c + 31) / 32), 1024, 0, s>>>(colpart, (int)slabs, c, colsum);
+    ::tcg::launch_pdl(sum_slabs, (unsigned)((c + 31) / 32), 1024, 0, s, colpart, (int)slabs, c, colsum, (int64_t)INT64_MAX, (float*)nullptr);
     TCG_LAUNCHED("sum_slabs");
   }
   return TCG_OK;
@@ -641,13 +645,13 @@ extern "C" int tcg_softmax_xent(const float* logits, int64_t ld, const int64_t* 
   float* lpart = static_cast<float*>(workspace);
   const unsigned grid = (unsigned)((n + 31) / 32);
   if (dlogits)
-    softmax_xent<true, true><<<grid, 256, 0, s>>>(logits, ld, labels, n, (int)c, dlogits, c,
+    ::tcg::launch_pdl(softmax_xent<true, true>, grid, 256, 0, s, logits, ld, labels, n, (int)c, dlogits, c,
                                                   nullptr, lpart, parts);
   else
-    softmax_xent<true, false><<<grid, 256, 0, s>>>(logits, ld, labels, n, (int)c, nullptr, 0,
+    ::tcg::launch_pdl(softmax_xent<true, false>, grid, 256, 0, s, logits, ld, labels, n, (int)c, nullptr, 0,
                                                    nullptr, lpart, parts);
   TCG_LAUNCHED("softmax_xent");
-  final_loss<<<1, 256, 0, s>>>(lpart, parts, n, loss);
+  ::tcg::launch_pdl(final_loss, 1, 256, 0, s, lpart, parts, n, loss);
   TCG_LAUNCHED("final_loss");
   return TCG_OK;
 }
@@ -657,7 +661,7 @@ extern "C" int tcg_softmax_xent_backward(const float* logits, int64_t ld, const 
                                          float* dlogits, int64_t ldd, void* stream) {
   TCG_REQUIRE(n >= 1 && c >= 1 && ld >= c && ldd >= c, "tcg_softmax_xent_backward: bad shape");
   TCG_REQUIRE(logits && labels && dlogits, "tcg_softmax_xent_backward: null pointer");
-  softmax_xent<false, true><<<(unsigned)((n + 31) / 32), 256, 0, as_stream(stream)>>>(
+  ::tcg::launch_pdl(softmax_xent<false, true>, (unsigned)((n + 31) / 32), 256, 0, as_stream(stream), 
       logits, ld, labels, n, (int)c, dlogits, ldd, grad_scale, nullptr, 0);
   TCG_LAUNCHED("softmax_xent_backward");
   return TCG_OK;
@@ -685,7 +689,7 @@ extern "C" int tcg_linear_xent(const float* x, int64_t ldx, int64_t n, int64_t k
     set_error("tcg_linear_xent: shape not covered (needs kin a multiple of 4 <= 32, c <= 48, 16-B rows)");
     return TCG_E_UNSUPPORTED;
   }
-  final_loss<<<1, 256, 0, s>>>(lpart, parts, div, loss);
+  ::tcg::launch_pdl(final_loss, 1, 256, 0, s, lpart, parts, div, loss);
   TCG_LAUNCHED("final_loss");
   return TCG_OK;
 }
@@ -714,7 +718,7 @@ extern "C" int tcg_linear_xent_backward(const float* x, int64_t ldx, int64_t n, 
     return TCG_E_UNSUPPORTED;
   }
   const int64_t len = kin * c + c;
-  sum_slabs<<<(unsigned)((len + 31) / 32), 1024, 0, s>>>(part, (int)slabs, len, dw, kin * c, db);
+  ::tcg::launch_pdl(sum_slabs, (unsigned)((len + 31) / 32), 1024, 0, s, part, (int)slabs, len, dw, kin * c, db);
   TCG_LAUNCHED("sum_slabs");
   return TCG_OK;
 }
@@ -742,20 +746,20 @@ extern "C" int tcg_colsum(const float* x, int64_t ld, int64_t n, int64_t c, floa
   const int64_t c4 = (c + 3) / 4 * 4;
   const bool v4 = ld % 4 == 0 && c4 <= ld && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   if (v4) {
-    colsum_part<4><<<(unsigned)slabs, 256, 0, s>>>(x, ld, n, (int)c4, rows, part);
+    ::tcg::launch_pdl(colsum_part<4>, (unsigned)slabs, 256, 0, s, x, ld, n, (int)c4, rows, part, (const float*)nullptr, (int64_t)0, (float*)nullptr, (int64_t)0);
     TCG_LAUNCHED("colsum_part");
     if (c4 == c) {
-      sum_slabs<<<(unsigned)((c + 31) / 32), 1024, 0, s>>>(part, (int)slabs, c, out);
+      ::tcg::launch_pdl(sum_slabs, (unsigned)((c + 31) / 32), 1024, 0, s, part, (int)slabs, c, out, (int64_t)INT64_MAX, (float*)nullptr);
     } else {
       float* tmp = part + slabs * c4;
-      sum_slabs<<<(unsigned)((c4 + 31) / 32), 1024, 0, s>>>(part, (int)slabs, c4, tmp);
+      ::tcg::launch_pdl(sum_slabs, (unsigned)((c4 + 31) / 32), 1024, 0, s, part, (int)slabs, c4, tmp, (int64_t)INT64_MAX, (float*)nullptr);
       TCG_CUDA(cudaMemcpyAsync(out, tmp, sizeof(float) * c, cudaMemcpyDeviceToDevice, s),
                "tcg_colsum copy");
     }
   } else {
-    colsum_part<1><<<(unsigned)slabs, 256, 0, s>>>(x, ld, n, (int)c, rows, part);
+    ::tcg::launch_pdl(colsum_part<1>, (unsigned)slabs, 256, 0, s, x, ld, n, (int)c, rows, part, (const float*)nullptr, (int64_t)0, (float*)nullptr, (int64_t)0);
     TCG_LAUNCHED("colsum_part");
-    sum_slabs<<<(unsigned)((c + 31) / 32), 1024, 0, s>>>(part, (int)slabs, c, out);
+    ::tcg::launch_pdl(sum_slabs, (unsigned)((c + 31) / 32), 1024, 0, s, part, (int)slabs, c, out, (int64_t)INT64_MAX, (float*)nullptr);
   }
   TCG_LAUNCHED("sum_slabs");
   return TCG_OK;
@@ -778,11 +782,11 @@ extern "C" int tcg_colsum_gate(const float* x, int64_t ld, const float* gate, in
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool v4 = c % 4 == 0 && ld % 4 == 0 && ldg % 4 == 0 && ldo % 4 == 0 && al(x) && al(gate) && al(gout);
   if (v4)
-    colsum_part<4, true><<<(unsigned)slabs, 256, 0, s>>>(x, ld, n, (int)c, rows, part, gate, ldg, gout, ldo);
+    ::tcg::launch_pdl(colsum_part<4, true>, (unsigned)slabs, 256, 0, s, x, ld, n, (int)c, rows, part, gate, ldg, gout, ldo);
   else
-    colsum_part<1, true><<<(unsigned)slabs, 256, 0, s>>>(x, ld, n, (int)c, rows, part, gate, ldg, gout, ldo);
+    ::tcg::launch_pdl(colsum_part<1, true>, (unsigned)slabs, 256, 0, s, x, ld, n, (int)c, rows, part, gate, ldg, gout, ldo);
   TCG_LAUNCHED("colsum_gate");
-  sum_slabs<<<(unsigned)((c + 31) / 32), 1024, 0, s>>>(part, (int)slabs, c, out);
+  ::tcg::launch_pdl(sum_slabs, (unsigned)((c + 31) / 32), 1024, 0, s, part, (int)slabs, c, out, (int64_t)INT64_MAX, (float*)nullptr);
   TCG_LAUNCHED("sum_slabs");
   return TCG_OK;
 }
@@ -821,7 +825,7 @@ extern "C" int tcg_dense_backward(const float* x, int64_t ldx, const float* g, i
     float* part = static_cast<float*>(workspace);
     const int rc = dense_mma32_bwd(x, ldx, g, ldg, n, w, dx, lddx, part, &slabs, s);
     if (rc == TCG_OK) {
-      sum_slabs<<<(unsigned)((ci * co + 31) / 32), 1024, 0, s>>>(part, (int)slabs, ci * co, dw);
+      ::tcg::launch_pdl(sum_slabs, (unsigned)((ci * co + 31) / 32), 1024, 0, s, part, (int)slabs, ci * co, dw, (int64_t)INT64_MAX, (float*)nullptr);
       TCG_LAUNCHED("sum_slabs");
       return TCG_OK;
     }
@@ -843,7 +847,7 @@ extern "C" int tcg_dense_backward(const float* x, int64_t ldx, const float* g, i
   dr::dense_bwd_tile<32, 32><<<(unsigned)blocks, Cfg::NT, Cfg::SMEM, s>>>(x, ldx, g, ldg, n, w,
                                                                           dx, lddx, part);
   TCG_LAUNCHED("dense_bwd_tile");
-  sum_slabs<<<(unsigned)((ci * co + 31) / 32), 1024, 0, s>>>(part, (int)blocks, ci * co, dw);
+  ::tcg::launch_pdl(sum_slabs, (unsigned)((ci * co + 31) / 32), 1024, 0, s, part, (int)blocks, ci * co, dw, (int64_t)INT64_MAX, (float*)nullptr);
   TCG_LAUNCHED("sum_slabs");
   return TCG_OK;
 }

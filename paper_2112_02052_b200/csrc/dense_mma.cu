@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(WPC * 32) mma32_fwd(const float* __restrict__ 
                                                        const float* __restrict__ w, int trans,
                                                        const float* __restrict__ bias, int relu,
                                                        float* __restrict__ y, int64_t ldy) {
+  TCG_PDL_ENTRY();
   constexpr int RD = 4;  // tiles in flight per warp
   __shared__ __align__(128) unsigned char sm[WPC][RD][2048];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -188,6 +189,7 @@ __global__ void __launch_bounds__(WPC * 32) mma32_bwd(const float* __restrict__ 
                                                        const float* __restrict__ g, int64_t ldg, int64_t n,
                                                        const float* __restrict__ w, float* __restrict__ dx,
                                                        int64_t lddx, float* __restrict__ part) {
+  TCG_PDL_ENTRY();
   constexpr int RD = 2;  // tiles in flight per warp
   __shared__ __align__(128) unsigned char sm[WPC][RD][2][2048];  // [warp][buffer][x | g]
   float (*red)[32][33] = reinterpret_cast<float (*)[32][33]>(&sm[0][0][0][0]);  // reused at the end
@@ -303,7 +305,7 @@ int dense_mma32(const float* x, int64_t ldx, int64_t n, int ci, const float* w, 
   int64_t blocks = (tiles + dm::WPC - 1) / dm::WPC;
   const int64_t cap = (int64_t)num_sms() * per_sm;
   if (blocks > cap) blocks = cap;
-  dm::mma32_fwd<<<(unsigned)blocks, dm::WPC * 32, 0, s>>>(x, ldx, n, w, trans ? 1 : 0, bias, relu, y, ldy);
+  ::tcg::launch_pdl(dm::mma32_fwd, (unsigned)blocks, dm::WPC * 32, 0, s, x, ldx, n, w, trans ? 1 : 0, bias, relu, y, ldy);
   TCG_LAUNCHED("mma32_fwd");
   return TCG_OK;
 }
@@ -329,7 +331,7 @@ int dense_mma32_bwd(const float* x, int64_t ldx, const float* g, int64_t ldg, in
   int64_t blocks = (tiles + dm::WPC - 1) / dm::WPC;
   const int64_t cap = dense_mma32_bwd_slabs();
   if (blocks > cap) blocks = cap;
-  dm::mma32_bwd<<<(unsigned)blocks, dm::WPC * 32, 0, s>>>(x, ldx, g, ldg, n, w, dx, lddx, part);
+  ::tcg::launch_pdl(dm::mma32_bwd, (unsigned)blocks, dm::WPC * 32, 0, s, x, ldx, g, ldg, n, w, dx, lddx, part);
   TCG_LAUNCHED("mma32_bwd");
   *slabs = blocks;
   return TCG_OK;
@@ -473,6 +475,7 @@ __global__ void __launch_bounds__(WPC * 32, 4) linear_xent(const float* __restri
                                                          const int64_t* __restrict__ labels, float inv_div,
                                                          float* __restrict__ dl, int64_t ldd,
                                                          float* __restrict__ lpart) {
+  TCG_PDL_ENTRY();
   constexpr int RD = 3;
   __shared__ __align__(128) unsigned char sm[WPC][RD][2048];
   __shared__ LxW<NTL, KT> ws;
@@ -571,6 +574,7 @@ __global__ void __launch_bounds__(WPC * 32, 3) linear_xent_bwd(
     const float* __restrict__ x, int64_t ldx, int64_t n, int kin, const float* __restrict__ w, int c,
     const float* __restrict__ bias, const int64_t* __restrict__ labels, const float* __restrict__ gscale,
     float inv_div, float* __restrict__ dx, int64_t lddx, float* __restrict__ part) {
+  TCG_PDL_ENTRY();
   constexpr int RD = 2, WP = lx_pitch(NTL), MT = KT / 2, PW = KT * 8 * NTL * 8 + NTL * 8;
   constexpr int RING = WPC * RD * 2048, DSM = WPC * 16 * WP * 4, RED = WPC * PW * 4;
   constexpr int UNI = (RING + DSM) > RED ? (RING + DSM) : RED;
@@ -761,6 +765,7 @@ __global__ void __launch_bounds__(256, 2) gemm_tn_mma(const float* __restrict__ 
                                                        const float* __restrict__ mk, int64_t ldm, int64_t n,
                                                        int k, float* __restrict__ part,
                                                        float* __restrict__ colpart) {
+  TCG_PDL_ENTRY();
   using namespace gt;
   using Sm = Smem<CO>;
   constexpr int BP = Sm::BP, NJ = CO / 8;
@@ -891,6 +896,7 @@ template <int CO>
 __global__ void __launch_bounds__(128, 2) dense_in_mma(const float* __restrict__ x, int64_t ldx, int64_t n, int ci,
                                                         const float* __restrict__ w, const float* __restrict__ bias,
                                                         int relu, float* __restrict__ y, int64_t ldy) {
+  TCG_PDL_ENTRY();
   using namespace di;
   using Sm = Smem<CO>;
   constexpr int WP = Sm::WP, NJ = CO / 8, NT = 128;
@@ -1004,6 +1010,7 @@ __global__ void __launch_bounds__(128, 2) dense_wide_mma(const float* __restrict
                                                           int ci, const float* __restrict__ w,
                                                           const float* __restrict__ bias, int relu,
                                                           float* __restrict__ y, int64_t ldy) {
+  TCG_PDL_ENTRY();
   using namespace dw;
   using Sm = Smem<CO>;
   constexpr int WP = Sm::WP, NJ = CO / 8, NT = 128;
@@ -1152,7 +1159,7 @@ int linear_xent_bwd(const float* x, int64_t ldx, int64_t n, int kin, const float
   {                                                                                                      \
     static const int64_t wave = lx_wave(dm::linear_xent_bwd<NV, KV>);                                    \
     blocks = std::min(blocks, wave);                                                                     \
-    dm::linear_xent_bwd<NV, KV><<<(unsigned)blocks, dm::WPC * 32, 0, s>>>(x, ldx, n, kin, w, c, bias,    \
+    ::tcg::launch_pdl(dm::linear_xent_bwd<NV, KV>, (unsigned)blocks, dm::WPC * 32, 0, s, x, ldx, n, kin, w, c, bias,    \
                                                                          labels, gscale, inv_div, dx,   \
                                                                          lddx, part);                    \
   }
@@ -1175,7 +1182,7 @@ int linear_xent(const float* x, int64_t ldx, int64_t n, int kin, const float* w,
   {                                                                                                      \
     static const int64_t wave = lx_wave(dm::linear_xent<NV, KV>);                                        \
     blocks = std::min(blocks, wave);                                                                     \
-    dm::linear_xent<NV, KV><<<(unsigned)blocks, dm::WPC * 32, 0, s>>>(x, ldx, n, kin, w, c, bias, labels, \
+    ::tcg::launch_pdl(dm::linear_xent<NV, KV>, (unsigned)blocks, dm::WPC * 32, 0, s, x, ldx, n, kin, w, c, bias, labels, \
                                                                      inv_div, dl, ldd, lpart);          \
   }
   TCG_LX_DISPATCH(TCG_LXF)
@@ -1212,7 +1219,7 @@ int gemm_tn_mma(const float* a, int64_t lda, const float* b, int64_t ldb, const 
       if (per_sm < 1) per_sm = 1;                                                                      \
     }                                                                                                  \
     const int64_t grid = std::min<int64_t>(std::min<int64_t>((int64_t)num_sms() * per_sm, chunks), cap_slabs); \
-    kern<<<dim3((unsigned)grid, panels), 256, smem, s>>>(a, lda, b, ldb, mask, ldm, n, k, part, colpart); \
+    ::tcg::launch_pdl(kern, dim3((unsigned)grid, panels), 256, smem, s, a, lda, b, ldb, mask, ldm, n, k, part, colpart); \
     *used = grid;                                                                                      \
   }
   if (c == 16) TCG_GTM(16) else TCG_GTM(32)
@@ -1245,7 +1252,7 @@ int dense_in_mma(const float* x, int64_t ldx, int64_t n, int ci, const float* w,
       if (per_sm < 1) per_sm = 1;                                                                       \
     }                                                                                                   \
     const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm, chunks);                        \
-    kern<<<(unsigned)grid, 128, smem, s>>>(x, ldx, n, ci, w, bias, relu, y, ldy);                       \
+    ::tcg::launch_pdl(kern, (unsigned)grid, 128, smem, s, x, ldx, n, ci, w, bias, relu, y, ldy);         \
   }
   if (co == 16) TCG_DIM(16) else TCG_DIM(32)
 #undef TCG_DIM
@@ -1277,7 +1284,7 @@ int dense_wide_mma(const float* x, int64_t ldx, int64_t n, int ci, const float* 
       if (per_sm < 1) per_sm = 1;                                                                       \
     }                                                                                                   \
     const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm, chunks);                        \
-    kern<<<(unsigned)grid, 128, smem, s>>>(x, ldx, n, ci, w, bias, relu, y, ldy);                       \
+    ::tcg::launch_pdl(kern, (unsigned)grid, 128, smem, s, x, ldx, n, ci, w, bias, relu, y, ldy);         \
   }
   if (co == 16) TCG_DWM(16) else TCG_DWM(32)
 #undef TCG_DWM

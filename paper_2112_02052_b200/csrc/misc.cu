@@ -4,6 +4,7 @@
 //    kernels.py:541-556) and its backward (no reference counterpart);
 //  * TF32 operand rounding (reference tiles.quantize_tf32, tiles.py:67-82);
 //  * CSR transpose with the edge permutation (backward support);
+#include <cstdlib>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -138,6 +139,16 @@ extern "C" const char* tcg_version(void) { return "tcg_b200 0.1.0 (sm_100a)"; }
 
 extern "C" int64_t tcg_launch_count(void) { return launch_counter().load(); }
 
+namespace tcg {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TCG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+}  // namespace tcg
+
 extern "C" int tcg_device_info(int64_t* num_sms_out, int64_t* l2_bytes) {
   int dev = 0, sms = 0, l2 = 0;
   TCG_CUDA(cudaGetDevice(&dev), "tcg_device_info");
@@ -188,6 +199,7 @@ namespace tcg {
 namespace {
 __global__ void permute_f32(const float* __restrict__ src, const uint32_t* __restrict__ idx,
                             float* __restrict__ dst, int64_t n) {
+  TCG_PDL_ENTRY();
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x)
     dst[k] = __ldg(src + __ldg(idx + k));
@@ -199,6 +211,7 @@ __global__ void permute_f32(const float* __restrict__ src, const uint32_t* __res
 __global__ void permute2_f32(const float* __restrict__ a, const float* __restrict__ b,
                              const uint32_t* __restrict__ idx, float* __restrict__ da,
                              float* __restrict__ db, int64_t n) {
+  TCG_PDL_ENTRY();
   const bool vec = ((reinterpret_cast<uintptr_t>(idx) | reinterpret_cast<uintptr_t>(da) |
                      reinterpret_cast<uintptr_t>(db)) & 15) == 0;
   const int64_t n4 = vec ? n / 4 : 0;
@@ -250,7 +263,7 @@ extern "C" int tcg_permute2_f32(const float* src_a, const float* src_b, const ui
   TCG_REQUIRE(src_a && src_b && idx && dst_a && dst_b, "tcg_permute2_f32: null pointer");
   int64_t blocks = (n / 4 + 255) / 256 + 1;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  permute2_f32<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(src_a, src_b, idx, dst_a, dst_b, n);
+  ::tcg::launch_pdl(permute2_f32, (unsigned)blocks, 256, 0, as_stream(stream), src_a, src_b, idx, dst_a, dst_b, n);
   TCG_LAUNCHED("permute2_f32");
   return TCG_OK;
 }
@@ -262,7 +275,7 @@ extern "C" int tcg_permute_f32(const float* src, const uint32_t* idx, float* dst
   TCG_REQUIRE(src && idx && dst, "tcg_permute_f32: null pointer");
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  permute_f32<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(src, idx, dst, n);
+  ::tcg::launch_pdl(permute_f32, (unsigned)blocks, 256, 0, as_stream(stream), src, idx, dst, n);
   TCG_LAUNCHED("permute_f32");
   return TCG_OK;
 }
@@ -271,6 +284,7 @@ namespace tcg {
 namespace {
 __global__ void scatter_f32(const float* __restrict__ src, const uint32_t* __restrict__ idx,
                             float* __restrict__ dst, int64_t n) {
+  TCG_PDL_ENTRY();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     dst[idx[i]] = src[i];
@@ -285,7 +299,7 @@ extern "C" int tcg_scatter_f32(const float* src, const uint32_t* idx, float* dst
   TCG_REQUIRE(src && idx && dst, "tcg_scatter_f32: null pointer");
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  tcg::scatter_f32<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(src, idx, dst, n);
+  ::tcg::launch_pdl(tcg::scatter_f32, (unsigned)blocks, 256, 0, as_stream(stream), src, idx, dst, n);
   TCG_LAUNCHED("scatter_f32");
   return TCG_OK;
 }

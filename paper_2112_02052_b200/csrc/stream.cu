@@ -184,6 +184,7 @@ __device__ __forceinline__ int warp_lower_bound(const int32_t* __restrict__ a, i
 
 template <int NT, bool DUAL, bool BIG, bool MASK, bool PAIR = false>
 __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG, PAIR>::WPC * 32, 1) spmm_stream(const Args a) {
+  TCG_PDL_ENTRY();
   using C = Cfg<NT, DUAL, BIG, PAIR>;
   constexpr int NB = C::NB, NI = C::NI, SLOT = C::SLOT, MB = C::MB, KB = C::KB;
   static_assert(!PAIR || (NT >= 2 && (!DUAL || NT == 4) && MB % 2 == 0), "pair steps: 16/32-wide");
@@ -1211,6 +1212,7 @@ __device__ __forceinline__ uint32_t agnn_off(int r, int c) {
 // read back by a separate GEMM.
 template <int KIND, bool PAIR = false, bool MASK = false, bool NEXT = false>
 __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const AgnnArgs a) {
+  TCG_PDL_ENTRY();
   using C = AgnnCfg<KIND>;
   constexpr bool BWD = KIND == 1;   // 0: forward, 1: backward A-side, 2: SDDMM only
   constexpr int NB = C::NB, NI = C::NI;
@@ -1655,7 +1657,7 @@ int launch_agnn(AgnnArgs& a, cudaStream_t s) {
   if (per_sm < 1) per_sm = 1;
   const int64_t ctas = (int64_t)num_sms() * per_sm;
   a.nwarps = (int)(ctas * C::WPC);
-  kern<<<(unsigned)ctas, C::WPC * 32, SMEM, s>>>(a);
+  ::tcg::launch_pdl(kern, (unsigned)ctas, C::WPC * 32, SMEM, s, a);
   TCG_LAUNCHED(KIND == 1 ? "agnn_stream_bwd" : KIND == 0 ? "agnn_stream_fwd" : "sddmm_stream");
   return TCG_OK;
 }
@@ -1688,6 +1690,7 @@ struct WideCfg {
 
 template <bool MASK>
 __global__ void __launch_bounds__(WideCfg::WPC * 32, 2) sddmm_wide(const AgnnArgs a) {
+  TCG_PDL_ENTRY();
   using C = WideCfg;
   constexpr int NB = C::NB, NI = C::NI;
   constexpr uint32_t RS = kWideRB * 128;
@@ -1866,7 +1869,7 @@ int launch_wide(AgnnArgs& a, cudaStream_t s) {
   if (per_sm < 1) per_sm = 1;
   const int64_t ctas = (int64_t)num_sms() * per_sm;
   a.nwarps = (int)(ctas * C::WPC);
-  kern<<<(unsigned)ctas, C::WPC * 32, C::SMEM, s>>>(a);
+  ::tcg::launch_pdl(kern, (unsigned)ctas, C::WPC * 32, C::SMEM, s, a);
   TCG_LAUNCHED("sddmm_wide");
   return TCG_OK;
 }
@@ -1939,7 +1942,7 @@ int launch_t(Args& a, int nchunks, cudaStream_t s) {
   (void)tb;
   a.nwarps = (int)(ctas * C::WPC);
   dim3 grid((unsigned)ctas, (unsigned)nchunks);
-  kern<<<grid, C::WPC * 32, C::SMEM, s>>>(a);
+  ::tcg::launch_pdl(kern, grid, C::WPC * 32, C::SMEM, s, a);
   TCG_LAUNCHED("spmm_stream");
   return TCG_OK;
 }
