@@ -54,8 +54,9 @@ for _ in range(5):
     run()
 torch.cuda.synchronize()
 eng = os.environ.get("TCG_SPMM_ENGINE", "default") + os.environ.get("TCG_WS_CFG", "")
-if os.environ.get("TCG_SPMM_PF"):
-    eng += "+pf" + os.environ["TCG_SPMM_PF"] + "/" + os.environ.get("TCG_SPMM_PFD", "16")
+for k in sorted(os.environ):
+    if k.startswith("TCG_") and k not in ("TCG_SPMM_ENGINE", "TCG_WS_CFG"):
+        eng += f"+{k[4:].lower()}={os.environ[k]}"
 refp = f"gpurun_out/ws_ref_{name}_{D}.pt"
 if eng == "default":
     torch.save(out.cpu(), refp)
