@@ -26,7 +26,8 @@ def hub(n, seed):
 
 
 graphs = [tcg.synth.gen_uniform(333, 4, 1), tcg.synth.gen_uniform(1001, 9, 2), hub(1200, 3),
-          tcg.synth.gen_powerlaw(900, 6, 4)]
+          tcg.synth.gen_powerlaw(900, 6, 4),
+          tcg.synth.gen_uniform(1500, 30, 5)]  # products-like windows (~480 edges): sddmm_wide, BIG SpMM
 worst = 0.0
 for g in graphs:
     n = g.num_nodes
@@ -47,6 +48,9 @@ for g in graphs:
         z = torch.randn(n, d, device="cuda")
         y, p = agnn_forward_device(t, z)
         agnn_backward_device(t, z, torch.randn_like(z), p, y_fwd=y)
+        from paper_2112_02052_b200 import _lib
+        sddmm_device(t, z, epilogue=_lib.EPI_SOFTMAX)
+        sddmm_device(t, z, torch.randn_like(z), epilogue=_lib.EPI_SOFTMAX_BWD, aux=p)
     z = torch.randn(n, 32, device="cuda")
     net = layers.AGNN(32, 32, 5, layers=2).cuda()
     lab = torch.randint(0, 5, (n,), device="cuda")
