@@ -7,8 +7,8 @@ sys.path.insert(0, ".")
 import torch
 from paper_2112_02052_b200 import dense
 
-n, c = 169343, 40
-for kin in (16, 32):
+shapes = [(169343, 40, 16), (169343, 40, 32), (2449029, 47, 16)]
+for n, c, kin in shapes:
     gen = torch.Generator(device="cuda").manual_seed(kin)
     x = torch.randn(n, kin, device="cuda", generator=gen)
     w = torch.randn(kin, c, device="cuda", generator=gen) / kin ** 0.5
@@ -26,4 +26,4 @@ for kin in (16, 32):
             fn()
         e1.record()
         torch.cuda.synchronize()
-        print(f"kin {kin} {name}: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us/call (incl. final_loss / sum_slabs)")
+        print(f"n {n} c {c} kin {kin} {name}: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us/call (incl. final_loss / sum_slabs)")
