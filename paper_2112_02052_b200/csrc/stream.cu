@@ -1675,9 +1675,13 @@ int launch_agnn(AgnnArgs& a, cudaStream_t s) {
 // agnn_stream<2> with kWideE-entry buffers. One block per step.
 constexpr int kWideE = 1024;
 constexpr int kWideRB = 16;
+// W16: 8 blocks of 512 B in flight per warp (the ring's bytes, not its depth,
+// bound the gather: 4 x 512 B measured 1.50 ms at products, 8 x 512 B below)
+template <bool W16 = false>
 struct WideCfg {
-  static constexpr int NB = 4, NI = 8;
-  static constexpr int RING = NB * 1024;
+  static constexpr int NB = W16 ? 8 : 4, NI = 2 * NB;
+  static_assert(NI <= TCG_STREAM_PAD, "id ring reads past the stream padding");
+  static constexpr int RING = NB * (W16 ? 512 : 1024);
   static constexpr int IDX = NI * 32;
   static constexpr int MAP = kWideRB * 128 * 2;  // u16 per fragment slot: local edge + 1
   static constexpr int ESC = kWideE * 4;
@@ -1688,11 +1692,16 @@ struct WideCfg {
   static constexpr int SMEM = WPC * WARP;
 };
 
-template <bool MASK>
-__global__ void __launch_bounds__(WideCfg::WPC * 32, 2) sddmm_wide(const AgnnArgs a) {
+// W16 (D <= 16): 64-B staged rows, one 16-B copy per lane per block (row L/4,
+// chunk L%4; row r at (r & 3) * 128 + (r >> 2) * 64 so the SDDMM's row pairs
+// r / r + 4 read different bank halves) and two mma per block instead of four:
+// mma j takes features 4t + 2j (k = t) and 4t + 2j + 1 (k = t + 4).
+template <bool MASK, bool W16 = false>
+__global__ void __launch_bounds__(WideCfg<W16>::WPC * 32, 2) sddmm_wide(const AgnnArgs a) {
   TCG_PDL_ENTRY();
-  using C = WideCfg;
+  using C = WideCfg<W16>;
   constexpr int NB = C::NB, NI = C::NI;
+  constexpr uint32_t SLOT = W16 ? 512 : 1024;
   constexpr uint32_t RS = kWideRB * 128;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1728,9 +1737,24 @@ __global__ void __launch_bounds__(WideCfg::WPC * 32, 2) sddmm_wide(const AgnnArg
     if (lane < 2) cp_async<16>(iring + (s & (NI - 1)) * 32 + lane * 16, csw + 8 * (int64_t)s + 4 * lane);
   };
   const int xvb = MASK ? (4 * g < a.dv ? 16 : 0) : 16;
+  // W16: lane L copies chunk L%4 of staged row L/4 (the block's column k = L/4,
+  // at position 2 (k & 3) + (k >> 2) of the pair-interleaved ids)
+  const int qr = lane >> 2, qc = lane & 3;
+  const uint32_t q_id = 4u * (uint32_t)(2 * (qr & 3) + (qr >> 2));
+  const uint32_t q_dst = (uint32_t)((qr & 3) * 128 + (qr >> 2) * 64 + qc * 16);
+  const int q_vb = MASK ? (4 * qc < a.dv ? 16 : 0) : 16;
+  const char* q_x = reinterpret_cast<const char*>(a.z) + 16 * qc;
   auto issue_x = [&](int s) {
+    const uint32_t sb = ring + (s & (NB - 1)) * SLOT;
+    if constexpr (W16) {
+      const uint32_t id = *reinterpret_cast<const uint32_t*>(iring_p + (s & (NI - 1)) * 32 + q_id);
+      if constexpr (MASK)
+        cp_async_n<16>(sb + q_dst, q_vb ? (const void*)(q_x + (uint64_t)id * xrow) : (const void*)a.z, q_vb);
+      else
+        cp_async<16>(sb + q_dst, q_x + (uint64_t)id * xrow);
+      return;
+    }
     const uint2 id = *reinterpret_cast<const uint2*>(iring_p + (s & (NI - 1)) * 32 + 8 * t);
-    const uint32_t sb = ring + (s & (NB - 1)) * 1024;
     if constexpr (MASK) {
       const void* z0 = a.z;
       cp_async_n<16>(sb + so0, xvb ? (const void*)(xb + (uint64_t)id.x * xrow) : z0, xvb);
@@ -1740,6 +1764,8 @@ __global__ void __launch_bounds__(WideCfg::WPC * 32, 2) sddmm_wide(const AgnnArg
       cp_async<16>(sb + so1, xb + (uint64_t)id.y * xrow);
     }
   };
+  // W16: this lane's SDDMM B chunk (staged row pr, chunk t)
+  const uint32_t sdw = (uint32_t)((pr & 3) * 128 + (pr >> 2) * 64 + t * 16);
   for (int s = 0; s < NB; ++s) issue_idx(s);
   cp_commit();
   cp_wait<0>();
@@ -1760,9 +1786,9 @@ __global__ void __launch_bounds__(WideCfg::WPC * 32, 2) sddmm_wide(const AgnnArg
   for (int w = ws; w < we; ++w) {
     const int nbw = cb1 - cb0;
     const int ne = (int)(e1 - e0);
-    // own rows (SDDMM A operand): rows g, g+8; features 4t.. and 4(t+4)..
+    // own rows (SDDMM A operand): rows g, g+8; features 4t.. and 4(t+4).. (W16: 4t.. only)
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
+    for (int h = 0; h < (W16 ? 2 : 4); ++h) {
       const int64_t r = (int64_t)w * 16 + g + 8 * (h & 1);
       const int f = 4 * (t + 4 * (h >> 1));
       const bool ok = r < a.n && (!MASK || f < a.dv);
@@ -1776,12 +1802,25 @@ __global__ void __launch_bounds__(WideCfg::WPC * 32, 2) sddmm_wide(const AgnnArg
     const int re = live ? (int)(__ldg(a.ptr + rg + 1) - e0) : 0;
     __syncwarp();
     for (int j = rb + sub; j < re; j += 2) erow[j] = (unsigned char)r;
+    // the window's fragment slots, staged once (independent coalesced loads) in the
+    // score buffer: edge j's slot is read by its round's map rebuild before the
+    // round's blocks write edge j's score over it
+    uint32_t* efs = reinterpret_cast<uint32_t*>(esc);
+#pragma unroll 4
+    for (int j = lane; j < ne; j += 32) efs[j] = __ldg(a.efrag + e0 + j);
+    __syncwarp();
     int rc = rb + sub;  // this lane's cursor into its row's edges
     uint32_t ao[4][4];
+    if constexpr (W16) {
+      // mma j: a0 (g, k=t) = feature 4t+2j, a1 row g+8, a2 (g, k=t+4) = 4t+2j+1, a3 row g+8
+      ao[0][0] = tf32_rn(own[0].x), ao[1][0] = tf32_rn(own[1].x), ao[2][0] = tf32_rn(own[0].y), ao[3][0] = tf32_rn(own[1].y);
+      ao[0][1] = tf32_rn(own[0].z), ao[1][1] = tf32_rn(own[1].z), ao[2][1] = tf32_rn(own[0].w), ao[3][1] = tf32_rn(own[1].w);
+    } else {
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      ao[h][0] = tf32_rn(own[h].x), ao[h][1] = tf32_rn(own[h].y);
-      ao[h][2] = tf32_rn(own[h].z), ao[h][3] = tf32_rn(own[h].w);
+      for (int h = 0; h < 4; ++h) {
+        ao[h][0] = tf32_rn(own[h].x), ao[h][1] = tf32_rn(own[h].y);
+        ao[h][2] = tf32_rn(own[h].z), ao[h][3] = tf32_rn(own[h].w);
+      }
     }
     for (int lb = 0; lb < nbw; ++lb, ++s) {
       if (lb % kWideRB == 0) {  // slot map of blocks [lb, lb + kWideRB)
@@ -1792,7 +1831,7 @@ __global__ void __launch_bounds__(WideCfg::WPC * 32, 2) sddmm_wide(const AgnnArg
         __syncwarp();
         const uint32_t lo = (uint32_t)lb * 128;
         while (rc < re) {
-          const uint32_t f = __ldg(a.efrag + e0 + rc) - lo;
+          const uint32_t f = efs[rc] - lo;
           if (f >= RS) break;  // this row's next edges belong to a later round
           map[f] = (uint16_t)(rc + 1);
           rc += 2;
@@ -1801,13 +1840,20 @@ __global__ void __launch_bounds__(WideCfg::WPC * 32, 2) sddmm_wide(const AgnnArg
       }
       cp_wait<NB - 1>();
       __syncwarp();
-      const uint32_t sb = ring + (s & (NB - 1)) * 1024;
+      const uint32_t sb = ring + (s & (NB - 1)) * SLOT;
       float sc[4] = {0.f, 0.f, 0.f, 0.f};
-      float b0[4], b1[4];
-      lds_slice<4>(b0, sb + sd0);
-      lds_slice<4>(b1, sb + sd1);
+      if constexpr (W16) {
+        float b[4];
+        lds_slice<4>(b, sb + sdw);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) mma_tf32_rb(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], b0[j], b1[j]);
+        for (int j = 0; j < 2; ++j) mma_tf32_rb(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], b[2 * j], b[2 * j + 1]);
+      } else {
+        float b0[4], b1[4];
+        lds_slice<4>(b0, sb + sd0);
+        lds_slice<4>(b1, sb + sd1);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mma_tf32_rb(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], b0[j], b1[j]);
+      }
       const float v[4] = {sc[0], sc[2], sc[1], sc[3]};
       const uint2 mw = reinterpret_cast<const uint2*>(map32)[(lb % kWideRB) * 32 + lane];
 #pragma unroll
@@ -1852,10 +1898,10 @@ __global__ void __launch_bounds__(WideCfg::WPC * 32, 2) sddmm_wide(const AgnnArg
   cp_wait<0>();
 }
 
-template <bool MASK>
+template <bool MASK, bool W16 = false>
 int launch_wide(AgnnArgs& a, cudaStream_t s) {
-  using C = WideCfg;
-  auto kern = sddmm_wide<MASK>;
+  using C = WideCfg<W16>;
+  auto kern = sddmm_wide<MASK, W16>;
   static int configured = -1;
   int dev = 0;
   TCG_CUDA(cudaGetDevice(&dev), "sddmm_wide device");
@@ -2147,7 +2193,11 @@ int stream_sddmm(const tcg_tiling* t, int dim, const float* xa, int64_t lda, con
   const bool mk = dim < 32;
   static const bool pair_off = std::getenv("TCG_NO_PAIRS") != nullptr;
   static const bool wide_all = std::getenv("TCG_SDDMM_WIDE") != nullptr;  // test hook: every window
-  if (wide || wide_all) return mk ? stream::launch_wide<true>(a, s) : stream::launch_wide<false>(a, s);
+  static const bool w16_off = std::getenv("TCG_SDDMM_W16_OFF") != nullptr;  // A/B: D <= 16 in the 32-wide layout
+  if (wide || wide_all) {
+    if (dim <= 16 && !w16_off) return dim < 16 ? stream::launch_wide<true, true>(a, s) : stream::launch_wide<false, true>(a, s);
+    return mk ? stream::launch_wide<true>(a, s) : stream::launch_wide<false>(a, s);
+  }
   if (t->pair_offsets && t->pair_stream && !pair_off) {
     a.boff = t->pair_offsets, a.cs = t->pair_stream;
     return mk ? stream::launch_agnn<2, true, true>(a, s) : stream::launch_agnn<2, true>(a, s);
