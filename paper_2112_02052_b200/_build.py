@@ -23,7 +23,7 @@ LIB = PKG / "libtcg_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
-         "-Xptxas", "-O3"]
+         "-Xptxas", "-O3"] + os.environ.get("TCG_NVCC_EXTRA", "").split()
 
 
 def _sources():
