@@ -35,6 +35,13 @@ extern "C" {
 
 #define TCG_PREC_F32 0  /* exact f32: CSR-order fold, bitwise = reference f32 */
 #define TCG_PREC_TF32 1 /* tensor cores: RNE-to-tf32 operands, f32 accumulate */
+/* flag bits (round 2): OR-ed into tcg_spmm's precision, tcg_dense's relu and the
+ * flags of the *_ex AGNN entry points. The operand is already on the tf32 grid
+ * (RN-rounded by its producer), so the kernels skip its rounding; the results are
+ * those of the unflagged call on the same values. */
+#define TCG_PREC_X2_TF32 0x10 /* tcg_spmm, tf32: x2 pre-rounded */
+#define TCG_DENSE_OUT_TF32 0x2 /* tcg_dense: round the stored output RN to tf32 */
+#define TCG_AGNN_Z_TF32 0x1    /* tcg_agnn_*_ex: z pre-rounded */
 
 /* SDDMM epilogues (fused per row window; rows never straddle windows). */
 #define TCG_EPI_NONE 0        /* out[e] = <xa[row e], xb[col e]>                 */
@@ -288,6 +295,16 @@ int tcg_agnn_backward_fused(const tcg_tiling* t, const float* z, int64_t ldz, co
                             const float* p, float* ds, float* ds_t, const uint32_t* inv_perm,
                             float* dz, int64_t lddz, int64_t dz_row0, int64_t win_begin,
                             int64_t win_end, void* stream);
+/* tcg_agnn_forward / tcg_agnn_backward_fused with flags (TCG_AGNN_Z_TF32: z is
+ * already on the tf32 grid, e.g. written by tcg_dense with TCG_DENSE_OUT_TF32). */
+int tcg_agnn_forward_ex(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim, float* p,
+                        float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
+                        int32_t flags, void* stream);
+int tcg_agnn_backward_fused_ex(const tcg_tiling* t, const float* z, int64_t ldz, const float* gy,
+                               int64_t ldg, const float* y_fwd, int64_t ld_yfwd, int64_t dim,
+                               const float* p, float* ds, float* ds_t, const uint32_t* inv_perm,
+                               float* dz, int64_t lddz, int64_t dz_row0, int64_t win_begin,
+                               int64_t win_end, int32_t flags, void* stream);
 /* tcg_agnn_forward followed by P in A^T edge order (p_t[inv_perm[e]] = p[e];
  * inv_perm from tcg_invert_perm of the transpose's perm), for the backward's
  * A^T SpMM. tcg_agnn_backward_fused does the same for dS when ds_t is given.

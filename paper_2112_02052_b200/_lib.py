@@ -18,6 +18,9 @@ ACT_NONE, ACT_RELU = 0, 1
 TCG_E_UNSUPPORTED = -4
 PREC_F32 = 0
 PREC_TF32 = 1
+PREC_X2_TF32 = 0x10  # TCG_PREC_X2_TF32: x2 already on the tf32 grid
+DENSE_OUT_TF32 = 0x2  # TCG_DENSE_OUT_TF32
+AGNN_Z_TF32 = 0x1  # TCG_AGNN_Z_TF32
 EPI_NONE = 0
 EPI_SOFTMAX = 1
 EPI_SOFTMAX_BWD = 2
@@ -95,6 +98,11 @@ SIGNATURES = {
                                     _P, _I64, _I64, _I64, _I64, _P]),
     "tcg_agnn_backward_fused": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _P, _I64, _P, _I64,
                                           _I64, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
+    "tcg_agnn_forward_ex": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _I64, _P, _P, _I64, _I64,
+                                      _I64, _I64, _I32, _P]),
+    "tcg_agnn_backward_fused_ex": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _P, _I64, _P, _I64,
+                                             _I64, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64,
+                                             _I32, _P]),
     "tcg_agnn_forward_t": (C.c_int, [C.POINTER(TcgTiling), _P, _I64, _I64, _P, _P, _P, _P, _I64,
                                      _I64, _I64, _I64, _P]),
     "tcg_scatter_f32": (C.c_int, [_P, _P, _P, _I64, _P]),

@@ -121,6 +121,15 @@ __device__ __forceinline__ void mma_tf32_rb(float (&d)[4], uint32_t a0, uint32_t
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "f"(b0), "f"(b1));
 }
 
+// B operands already on the tf32 grid (RN-rounded by their producer): the mma
+// reads the raw bits, which equals mma_tf32_rb on the same values
+template <bool PRE>
+__device__ __forceinline__ void mma_tf32_b(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                           float b0, float b1) {
+  if constexpr (PRE) mma_tf32(d, a0, a1, a2, a3, __float_as_uint(b0), __float_as_uint(b1));
+  else mma_tf32_rb(d, a0, a1, a2, a3, b0, b1);
+}
+
 template <typename T>
 __device__ __forceinline__ T ldg_stream(const T* p) {
   return __ldg(p);

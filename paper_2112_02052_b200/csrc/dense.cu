@@ -534,13 +534,21 @@ extern "C" int tcg_dense(const float* x, int64_t ldx, int64_t n, int64_t ci, con
                          const float* mask, int64_t ldm, float* y, int64_t ldy, void* stream) {
   TCG_REQUIRE(n >= 0 && ci >= 1 && co >= 1, "tcg_dense: bad shape");
   TCG_REQUIRE(ldx >= ci && ldy >= co && (mask == nullptr || ldm >= ci), "tcg_dense: bad ld");
+  TCG_REQUIRE((relu & ~(1 | TCG_DENSE_OUT_TF32)) == 0, "tcg_dense: unknown relu flags 0x%x", relu);
   if (n == 0) return TCG_OK;
   TCG_REQUIRE(x && m && y, "tcg_dense: null pointer");
   cudaStream_t s = as_stream(stream);
   {
-    // 32 x 32: mma.sync 3xTF32, ldmatrix-fed (csrc/dense_mma.cu)
+    // 32 x 32: mma.sync 3xTF32, ldmatrix-fed (csrc/dense_mma.cu); the only kernel
+    // that rounds its output in the epilogue (TCG_DENSE_OUT_TF32)
     const int rc = dense_mma32(x, ldx, n, (int)ci, m, (int)co, m_transposed != 0, bias, relu, mask, y, ldy, s);
     if (rc != 1) return rc;
+  }
+  if (relu & TCG_DENSE_OUT_TF32) {  // other shapes: the plain product, then one rounding pass
+    int rc = tcg_dense(x, ldx, n, ci, m, co, m_transposed, bias, relu & 1, mask, ldm, y, ldy, stream);
+    if (rc != TCG_OK) return rc;
+    TCG_REQUIRE(ldy == co, "tcg_dense: TCG_DENSE_OUT_TF32 needs dense output rows (ldy == co) off the 32 x 32 path");
+    return tcg_quantize_tf32(y, y, n * co, stream);
   }
   {
     // the wide input layers (33..128 -> 16 / 32) on mma.sync 3xTF32 (csrc/dense_mma.cu

@@ -139,9 +139,13 @@ __device__ __forceinline__ void store_tile(const float (&acc)[4][4], float* __re
 #pragma unroll
       for (int q = 0; q < 8; ++q) o[q] += __ldg(bias + 8 * t + q);
     }
-    if (relu) {
+    if (relu & 1) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) o[q] = fmaxf(o[q], 0.f);
+    }
+    if (relu & TCG_DENSE_OUT_TF32) {  // stored on the tf32 grid (RN) for tf32 consumers
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] = __uint_as_float(tf32_rn(o[q]));
     }
     float4* yr = reinterpret_cast<float4*>(y + r * ldy + 8 * t);
     yr[0] = make_float4(o[0], o[1], o[2], o[3]);

@@ -212,6 +212,13 @@ static bool row0_ok(const tcg_tiling* t, int64_t win_begin, int64_t win_end, int
 extern "C" int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim,
                                 float* p, float* y, int64_t ldy, int64_t y_row0,
                                 int64_t win_begin, int64_t win_end, void* stream) {
+  return tcg_agnn_forward_ex(t, z, ldz, dim, p, y, ldy, y_row0, win_begin, win_end, 0, stream);
+}
+
+extern "C" int tcg_agnn_forward_ex(const tcg_tiling* t, const float* z, int64_t ldz, int64_t dim,
+                                   float* p, float* y, int64_t ldy, int64_t y_row0,
+                                   int64_t win_begin, int64_t win_end, int32_t flags, void* stream) {
+  TCG_REQUIRE((flags & ~TCG_AGNN_Z_TF32) == 0, "tcg_agnn_forward_ex: unknown flags 0x%x", flags);
   TCG_REQUIRE(t != nullptr && dim >= 1 && ldz >= dim && ldy >= dim,
               "tcg_agnn_forward: bad arguments");
   TCG_REQUIRE(t->blk_h == 16 && t->blk_w == 8,
@@ -225,7 +232,8 @@ extern "C" int tcg_agnn_forward(const tcg_tiling* t, const float* z, int64_t ldz
   if (!no_stream && dim <= 32 && dim % 4 == 0 && t->num_edges > 0 && win_begin < win_end && z && p &&
       y) {
     const int rc = stream_agnn(t, false, (int)dim, z, ldz, z, ldz, nullptr, 0, nullptr, p, y, ldy, y_row0,
-                               win_begin, win_end, as_stream(stream));
+                               win_begin, win_end, as_stream(stream), nullptr, nullptr, 0,
+                               (flags & TCG_AGNN_Z_TF32) != 0);
     if (rc != TCG_E_UNSUPPORTED) return rc;
   }
   if (t->num_edges == 0 || dim > 64 || !fits_fused(t, nt) || wide_two_step(t, dim)) {
@@ -283,6 +291,17 @@ extern "C" int tcg_agnn_backward_fused(const tcg_tiling* t, const float* z, int6
                                        float* ds_t, const uint32_t* inv_perm,
                                        float* dz, int64_t lddz, int64_t dz_row0,
                                        int64_t win_begin, int64_t win_end, void* stream) {
+  return tcg_agnn_backward_fused_ex(t, z, ldz, gy, ldg, y_fwd, ld_yfwd, dim, p, ds, ds_t, inv_perm, dz, lddz,
+                                    dz_row0, win_begin, win_end, 0, stream);
+}
+
+extern "C" int tcg_agnn_backward_fused_ex(const tcg_tiling* t, const float* z, int64_t ldz,
+                                          const float* gy, int64_t ldg, const float* y_fwd,
+                                          int64_t ld_yfwd, int64_t dim, const float* p, float* ds,
+                                          float* ds_t, const uint32_t* inv_perm,
+                                          float* dz, int64_t lddz, int64_t dz_row0,
+                                          int64_t win_begin, int64_t win_end, int32_t flags, void* stream) {
+  TCG_REQUIRE((flags & ~TCG_AGNN_Z_TF32) == 0, "tcg_agnn_backward_fused_ex: unknown flags 0x%x", flags);
   TCG_REQUIRE(t != nullptr && dim >= 1 && ldz >= dim && ldg >= dim && lddz >= dim &&
                   ld_yfwd >= dim,
               "tcg_agnn_backward_fused: bad arguments");
@@ -298,7 +317,8 @@ extern "C" int tcg_agnn_backward_fused(const tcg_tiling* t, const float* z, int6
   if (!no_stream && dim <= 32 && dim % 4 == 0 && t->num_edges > 0 && win_begin < win_end) {
     TCG_REQUIRE(z && gy && y_fwd && p && ds && dz, "tcg_agnn_backward_fused: null pointer");
     const int rc = stream_agnn(t, true, (int)dim, z, ldz, gy, ldg, y_fwd, ld_yfwd, p, ds, dz, lddz, dz_row0,
-                               win_begin, win_end, as_stream(stream));
+                               win_begin, win_end, as_stream(stream), nullptr, nullptr, 0,
+                               (flags & TCG_AGNN_Z_TF32) != 0);
     if (rc != TCG_E_UNSUPPORTED) {
       if (rc != TCG_OK || !ds_t || !inv_perm) return rc;
       return tcg_scatter_f32(ds, inv_perm, ds_t, t->num_edges, stream);

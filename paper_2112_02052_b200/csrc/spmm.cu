@@ -175,8 +175,13 @@ static int spmm_run(const tcg_tiling* t, const float* x, int64_t ldx, int64_t di
   TCG_REQUIRE(0 <= win_begin && win_begin <= win_end && win_end <= t->num_windows,
               "tcg_spmm: window range [%lld, %lld) outside [0, %lld)", (long long)win_begin,
               (long long)win_end, (long long)t->num_windows);
+  // TCG_PREC_X2_TF32 (tf32 only): x2 is already on the tf32 grid, its B-operand
+  // rounding is skipped (same result)
+  const int x2_tf32 = (precision & TCG_PREC_X2_TF32) != 0;
+  precision &= ~TCG_PREC_X2_TF32;
   TCG_REQUIRE(precision == TCG_PREC_F32 || precision == TCG_PREC_TF32,
               "tcg_spmm: unknown precision %d", precision);
+  TCG_REQUIRE(!x2_tf32 || precision == TCG_PREC_TF32, "tcg_spmm: TCG_PREC_X2_TF32 needs TCG_PREC_TF32");
   if (win_begin == win_end || t->num_nodes == 0) return TCG_OK;
   TCG_REQUIRE(x && y && t->node_ptr, "tcg_spmm: null pointer");
   cudaStream_t s = as_stream(stream);
@@ -260,6 +265,7 @@ static int spmm_run(const tcg_tiling* t, const float* x, int64_t ldx, int64_t di
   q.w = weights, q.widx = weight_idx, q.w2 = weights2, q.widx2 = weight_idx2;
   q.bias = bias, q.y = y, q.ldy = ldy, q.y_row0 = y_row0, q.accumulate = accumulate;
   q.relu = relu;
+  q.x2_tf32 = x2 ? x2_tf32 : 0;
   static const bool no_stream = std::getenv("TCG_NO_STREAM") != nullptr;
   if (!no_stream) {
     const int rc = stream_spmm(t, q, s);

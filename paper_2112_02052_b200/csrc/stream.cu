@@ -182,7 +182,7 @@ __device__ __forceinline__ int warp_lower_bound(const int32_t* __restrict__ a, i
   return lo + __popc(__ballot_sync(0xffffffffu, pr));
 }
 
-template <int NT, bool DUAL, bool BIG, bool MASK, bool PAIR = false>
+template <int NT, bool DUAL, bool BIG, bool MASK, bool PAIR = false, bool X2R = false>
 __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG, PAIR>::WPC * 32, 1) spmm_stream(const Args a) {
   TCG_PDL_ENTRY();
   using C = Cfg<NT, DUAL, BIG, PAIR>;
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(Cfg<NT, DUAL, BIG, PAIR>::WPC * 32, 1) spmm_st
             lds_slice<NT>(x1, xs + xo + kb * SLOT * C::OPS + SLOT + d1);
             const uint4 af = lds_frag(fa + kb * 512 + MB * 512);
 #pragma unroll
-            for (int j = 0; j < NT; ++j) mma_tf32_rb(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
+            for (int j = 0; j < NT; ++j) mma_tf32_b<X2R>(acc[j], af.x, af.y, af.z, af.w, x0[j], x1[j]);
           }
         }
         // refill: X of block s + NB into this slot, ids of block s + 2NB. The
@@ -1210,7 +1210,8 @@ __device__ __forceinline__ uint32_t agnn_off(int r, int c) {
 // Zn = Y Wn (3xTF32 mma.sync; Y staged through the window's slot-map area, free
 // at the window end; Wn as tf32 hi / lo after the warps' areas), so Y is not
 // read back by a separate GEMM.
-template <int KIND, bool PAIR = false, bool MASK = false, bool NEXT = false>
+// ZR: the gathered operand z is already on the tf32 grid (no B-operand cvt)
+template <int KIND, bool PAIR = false, bool MASK = false, bool NEXT = false, bool ZR = false>
 __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const AgnnArgs a) {
   TCG_PDL_ENTRY();
   using C = AgnnCfg<KIND>;
@@ -1401,7 +1402,7 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
         lds_slice<4>(b0, sb + sd0);
         lds_slice<4>(b1, sb + sd1);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) mma_tf32_rb(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], b0[j], b1[j]);
+        for (int j = 0; j < 4; ++j) mma_tf32_b<ZR>(sc, ao[0][j], ao[1][j], ao[2][j], ao[3][j], b0[j], b1[j]);
         // C (g, 2t) <-> A (g, t); C (g, 2t+1) <-> A (g, t+4): A slots are
         // (0: (g,t), 1: (g+8,t), 2: (g,t+4), 3: (g+8,t+4)); C regs are
         // (0: (g,2t), 1: (g,2t+1), 2: (g+8,2t), 3: (g+8,2t+1))
@@ -1492,7 +1493,7 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
           const uint32_t a0 = tf32_rn(av[kb][0]), a1 = tf32_rn(av[kb][1]), a2 = tf32_rn(av[kb][2]),
                          a3 = tf32_rn(av[kb][3]);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) mma_tf32_rb(acc[j], a0, a1, a2, a3, x0[j], x1[j]);
+          for (int j = 0; j < 4; ++j) mma_tf32_b<ZR>(acc[j], a0, a1, a2, a3, x0[j], x1[j]);
         }
       }
       __syncwarp();
@@ -1638,10 +1639,10 @@ __global__ void __launch_bounds__(AgnnCfg<KIND>::WPC * 32, 2) agnn_stream(const 
   cp_wait<0>();
 }
 
-template <int KIND, bool PAIR = false, bool MASK = false, bool NEXT = false>
+template <int KIND, bool PAIR = false, bool MASK = false, bool NEXT = false, bool ZR = false>
 int launch_agnn(AgnnArgs& a, cudaStream_t s) {
   using C = AgnnCfg<KIND>;
-  auto kern = agnn_stream<KIND, PAIR, MASK, NEXT>;
+  auto kern = agnn_stream<KIND, PAIR, MASK, NEXT, ZR>;
   constexpr int SMEM = C::SMEM + (NEXT ? 2 * 1024 * 4 : 0);
   static int configured = -1;
   int dev = 0;
@@ -1966,10 +1967,10 @@ __global__ void stream_pad_kernel(const int32_t* __restrict__ boff, int64_t W, u
   for (int q = threadIdx.x; q < 8 * TCG_STREAM_PAD; q += blockDim.x) cs[8 * tb + q] = fill;
 }
 
-template <int NT, bool DUAL, bool BIG, bool MASK, bool PAIR = false>
+template <int NT, bool DUAL, bool BIG, bool MASK, bool PAIR = false, bool X2R = false>
 int launch_t(Args& a, int nchunks, cudaStream_t s) {
   using C = Cfg<NT, DUAL, BIG, PAIR>;
-  auto kern = spmm_stream<NT, DUAL, BIG, MASK, PAIR>;
+  auto kern = spmm_stream<NT, DUAL, BIG, MASK, PAIR, X2R>;
   static int configured = -1;
   int dev = 0;
   TCG_CUDA(cudaGetDevice(&dev), "spmm_stream device");
@@ -2066,6 +2067,7 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
       stream::Args ap = a;
       ap.boff = t->pair_offsets;
       ap.cs = t->pair_stream;
+      if (dual && q.x2_tf32) return stream::launch_t<4, true, false, false, true, true>(ap, nchunks, s);
       return dual ? stream::launch_t<4, true, false, false, true>(ap, nchunks, s)
                   : stream::launch_t<4, false, false, false, true>(ap, nchunks, s);
     }
@@ -2126,7 +2128,7 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
 int stream_agnn(const tcg_tiling* t, bool bwd, int dim, const float* z, int64_t ldz, const float* za,
                 int64_t lda, const float* yf, int64_t ldyf, const float* pin, float* eout,
                 float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
-                cudaStream_t s, const float* wn, float* zn, int64_t ldzn) {
+                cudaStream_t s, const float* wn, float* zn, int64_t ldzn, bool z_tf32) {
   if (dim < 4 || dim > 32 || dim % 4) return TCG_E_UNSUPPORTED;
   if (!t->block_offsets || !t->col_stream || !t->edge_frag) return TCG_E_UNSUPPORTED;
   if (t->max_window_edges <= 0 || t->max_window_edges > stream::kMaxE ||
@@ -2156,8 +2158,10 @@ int stream_agnn(const tcg_tiling* t, bool bwd, int dim, const float* z, int64_t 
   // 59.5 -> 63.5 us before) and keeps one block per step
   if (!bwd && t->pair_offsets && t->pair_stream && !pair_off) {
     a.boff = t->pair_offsets, a.cs = t->pair_stream;
+    if (z_tf32 && !mk) return stream::launch_agnn<0, true, false, false, true>(a, s);
     return mk ? stream::launch_agnn<0, true, true>(a, s) : stream::launch_agnn<0, true>(a, s);
   }
+  if (bwd && z_tf32 && !mk) return stream::launch_agnn<1, false, false, false, true>(a, s);
   if (bwd) return mk ? stream::launch_agnn<1, false, true>(a, s) : stream::launch_agnn<1>(a, s);
   return mk ? stream::launch_agnn<0, false, true>(a, s) : stream::launch_agnn<0>(a, s);
 }

@@ -56,6 +56,7 @@ struct Params {
   int64_t y_row0;
   int accumulate;
   int relu;  // ReLU on the stored output (stream engine epilogue only)
+  int x2_tf32;  // dual form: x2 already on the tf32 grid (stream engine: no B-operand cvt)
   // SDDMM A operand (window rows) and edge outputs
   const float* xa;
   int64_t lda;
@@ -88,6 +89,7 @@ bool stream_sddmm_wide(const tcg_tiling* t);
 int stream_agnn(const tcg_tiling* t, bool bwd, int dim, const float* z, int64_t ldz, const float* za,
                 int64_t lda, const float* yf, int64_t ldyf, const float* pin, float* eout,
                 float* y, int64_t ldy, int64_t y_row0, int64_t win_begin, int64_t win_end,
-                cudaStream_t s, const float* wn = nullptr, float* zn = nullptr, int64_t ldzn = 0);
+                cudaStream_t s, const float* wn = nullptr, float* zn = nullptr, int64_t ldzn = 0,
+                bool z_tf32 = false);
 
 }  // namespace tcg

@@ -60,16 +60,18 @@ def rows16(x):
     return out
 
 
-def dense(x, w, bias=None, relu=False, mask=None, transposed=False, out=None):
+def dense(x, w, bias=None, relu=False, mask=None, transposed=False, out=None, out_tf32=False):
     """y = act((x .* [mask>0]) M + bias), M = w ([ci x co]) or w^T when
-    `transposed` (w then [co x ci])."""
+    `transposed` (w then [co x ci]); out_tf32 stores y RN-rounded to tf32
+    (TCG_DENSE_OUT_TF32), for operands whose every consumer rounds them anyway."""
     lib = _lib.load()
     n, ci = x.shape
     co = w.shape[0] if transposed else w.shape[1]
     if out is None:
         out = rows_empty(n, co, x.device)
     _lib.check(lib.tcg_dense(x.data_ptr(), x.stride(0), n, ci, w.data_ptr(), co, int(transposed),
-                             _p(bias), int(relu), _p(mask), mask.stride(0) if mask is not None else 0,
+                             _p(bias), int(relu) | (_lib.DENSE_OUT_TF32 if out_tf32 else 0), _p(mask),
+                             mask.stride(0) if mask is not None else 0,
                              out.data_ptr(), out.stride(0), _stream()), "tcg_dense")
     return out
 
@@ -180,9 +182,11 @@ def softmax_xent_backward(logits, labels, grad_scale=None):
 
 class DenseFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, w, b, relu: bool):
+    def forward(ctx, x, w, b, relu: bool, out_tf32: bool = False):
+        # out_tf32: y stored on the tf32 grid (its consumers all round it: the
+        # AGNN aggregation's Z); the backward treats the rounding as identity
         x = rows16(x) if x.shape[1] > 128 and w.shape[1] in (16, 32) else rows_ok(x)
-        y = dense(x, w.contiguous(), bias=b, relu=relu)
+        y = dense(x, w.contiguous(), bias=b, relu=relu, out_tf32=out_tf32)
         ctx.relu = relu
         ctx.has_b = b is not None
         ctx.save_for_backward(x, w, y if relu else None)
@@ -194,13 +198,13 @@ class DenseFn(torch.autograd.Function):
         g = rows_ok(g)
         if not ctx.relu and not ctx.has_b and ctx.needs_input_grad[0]:
             dx, dw = dense_backward(x, g, w.contiguous())
-            return dx, dw, None, None
+            return dx, dw, None, None, None
         mask = y if ctx.relu else None
         dx = None
         if ctx.needs_input_grad[0]:
             dx = dense(g, w.contiguous(), mask=mask, transposed=True)
         dw, db = gemm_tn(x, g, mask=mask, colsum=ctx.has_b)
-        return dx, dw, db, None
+        return dx, dw, db, None, None
 
 
 class SoftmaxXentFn(torch.autograd.Function):

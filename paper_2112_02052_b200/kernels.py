@@ -235,9 +235,10 @@ def _sddmm_counters(t: TiledGraph, d: int) -> Counters:
 
 def spmm_device(t: TiledGraph, x, weights=None, *, mode="tf32", out=None, bias=None,
                 accumulate=False, weight_idx=None, x2=None, weights2=None, weight_idx2=None,
-                win_range=None, y_row0=None, relu=False):
+                win_range=None, y_row0=None, relu=False, x2_tf32=False):
     """Raw SpMM launch: Y = A_w X (+ A_w2 X2) (+ bias), rows of `win_range`;
-    relu=True (single operand) stores relu(Y) (tcg_spmm_act)."""
+    relu=True (single operand) stores relu(Y) (tcg_spmm_act); x2_tf32: x2 is
+    already on the tf32 grid (TCG_PREC_X2_TF32, tf32 mode)."""
     import torch
 
     lib = _lib.load()
@@ -261,7 +262,8 @@ def spmm_device(t: TiledGraph, x, weights=None, *, mode="tf32", out=None, bias=N
         C.byref(t.abi()), x.data_ptr(), x.stride(0), d, _ptr(weights), _ptr(weight_idx),
         _ptr(x2), x2.stride(0) if x2 is not None else 0, _ptr(weights2), _ptr(weight_idx2),
         _ptr(bias), out.data_ptr(), out.stride(0), y_row0, wb, we,
-        _lib.PREC_TF32 if mode == "tf32" else _lib.PREC_F32, int(bool(accumulate)), _stream()),
+        (_lib.PREC_TF32 | (_lib.PREC_X2_TF32 if x2_tf32 and x2 is not None else 0)) if mode == "tf32"
+        else _lib.PREC_F32, int(bool(accumulate)), _stream()),
         "tcg_spmm")
     return out
 
@@ -318,9 +320,10 @@ def permute_device(src, idx, out=None):
 
 
 def agnn_forward_device(t: TiledGraph, z, *, p=None, out=None, win_range=None, y_row0=0,
-                        p_t=None, inv_perm=None):
+                        p_t=None, inv_perm=None, z_tf32=False):
     """Fused TF32 AGNN aggregation (tcg_agnn_forward): returns (Y, P). With
-    `p_t` / `inv_perm` P is also written in A^T edge order (tcg_agnn_forward_t)."""
+    `p_t` / `inv_perm` P is also written in A^T edge order (tcg_agnn_forward_t);
+    z_tf32: z is already on the tf32 grid (tcg_agnn_forward_ex, TCG_AGNN_Z_TF32)."""
     import torch
 
     lib = _lib.load()
@@ -335,6 +338,11 @@ def agnn_forward_device(t: TiledGraph, z, *, p=None, out=None, win_range=None, y
                                           p.data_ptr(), p_t.data_ptr(), inv_perm.data_ptr(),
                                           out.data_ptr(), out.stride(0), y_row0, wb, we,
                                           _stream()), "tcg_agnn_forward_t")
+        return out, p
+    if z_tf32:
+        _lib.check(lib.tcg_agnn_forward_ex(C.byref(t.abi()), z.data_ptr(), z.stride(0), z.shape[1],
+                                           p.data_ptr(), out.data_ptr(), out.stride(0), y_row0, wb, we,
+                                           _lib.AGNN_Z_TF32, _stream()), "tcg_agnn_forward_ex")
         return out, p
     _lib.check(lib.tcg_agnn_forward(C.byref(t.abi()), z.data_ptr(), z.stride(0), z.shape[1],
                                     p.data_ptr(), out.data_ptr(), out.stride(0), y_row0, wb, we,
@@ -367,7 +375,7 @@ def agnn_forward_next_device(t: TiledGraph, z, w_next, *, p=None, out=None, z_ne
 
 
 def agnn_backward_device(t: TiledGraph, z, gy, p, *, ds=None, out=None, win_range=None,
-                         y_row0=0, y_fwd=None, ds_t=None, inv_perm=None):
+                         y_row0=0, y_fwd=None, ds_t=None, inv_perm=None, z_tf32=False):
     """A-side half of the AGNN backward (tcg_agnn_backward): returns (dZ_A, dS)
     with dS = P (dP - rowsum(P dP)), dP = <G_i, Z_j>, dZ_A = A_dS Z. With the
     forward output `y_fwd` the one-pass form (tcg_agnn_backward_fused,
@@ -382,12 +390,13 @@ def agnn_backward_device(t: TiledGraph, z, gy, p, *, ds=None, out=None, win_rang
         out = torch.empty((t.num_nodes, z.shape[1]), dtype=torch.float32, device=z.device)
         y_row0 = 0
     if y_fwd is not None:
-        _lib.check(lib.tcg_agnn_backward_fused(
+        _lib.check(lib.tcg_agnn_backward_fused_ex(
             C.byref(t.abi()), z.data_ptr(), z.stride(0), gy.data_ptr(), gy.stride(0),
             y_fwd.data_ptr(), y_fwd.stride(0), z.shape[1], p.data_ptr(), ds.data_ptr(),
             ds_t.data_ptr() if ds_t is not None else None,
             inv_perm.data_ptr() if ds_t is not None else None,
-            out.data_ptr(), out.stride(0), y_row0, wb, we, _stream()), "tcg_agnn_backward_fused")
+            out.data_ptr(), out.stride(0), y_row0, wb, we, _lib.AGNN_Z_TF32 if z_tf32 else 0,
+            _stream()), "tcg_agnn_backward_fused_ex")
         return out, ds
     _lib.check(lib.tcg_agnn_backward(C.byref(t.abi()), z.data_ptr(), z.stride(0), gy.data_ptr(),
                                      gy.stride(0), z.shape[1], p.data_ptr(), ds.data_ptr(),

@@ -172,6 +172,9 @@ _PERMUTE_WEIGHTS = os.environ.get("TCG_GATHER_WEIGHTS") is None
 # was measured slower (1.22 vs 1.15 ms / epoch) and is not offered.
 _FUSED_PT = os.environ.get("TCG_FUSED_PT") is not None
 
+# AGNNConv: Z = X W stored on the tf32 grid for the tensor-core aggregation (TCG_Z_TF32=0: off)
+_Z_TF32 = os.environ.get("TCG_Z_TF32", "1") != "0"
+
 # AGNN model: the next layer's dense step in the AGNN forward epilogue (opt-in, see AGNN._trunk)
 _AGNN_NEXT = os.environ.get("TCG_AGNN_NEXT") == "1"
 
@@ -186,10 +189,12 @@ def _inv_perm(t: TiledGraph):
 
 
 class AgnnAggregate(torch.autograd.Function):
-    """Y = spmm(A, P; Z), P = rowsoftmax(sddmm(Z, Z))."""
+    """Y = spmm(A, P; Z), P = rowsoftmax(sddmm(Z, Z)). z_tf32: Z is already on
+    the tf32 grid (AGNNConv's dense step stores it rounded), so the tensor-core
+    kernels skip its operand rounding -- same values, 16 fewer cvt per block."""
 
     @staticmethod
-    def forward(ctx, z, t: TiledGraph, mode: str):
+    def forward(ctx, z, t: TiledGraph, mode: str, z_tf32: bool = False):
         z = z.contiguous()
         m = t.num_edges
         p = torch.empty(max(m, 1), dtype=torch.float32, device=z.device)
@@ -200,22 +205,22 @@ class AgnnAggregate(torch.autograd.Function):
             p_t = torch.empty(m, dtype=torch.float32, device=z.device)
             agnn_forward_device(t, z, p=p, out=out, p_t=p_t, inv_perm=_inv_perm(t))
         elif mode == "tf32":
-            agnn_forward_device(t, z, p=p, out=out)
+            agnn_forward_device(t, z, p=p, out=out, z_tf32=z_tf32)
         else:
             if m:
                 sddmm_device(t, z, mode=mode, epilogue=_lib.EPI_SOFTMAX, out=p)
             spmm_device(t, z, p if m else None, mode=mode, out=out)
         ctx.save_for_backward(z, p, out if mode == "tf32" else None, p_t)
-        ctx.t, ctx.mode = t, mode
+        ctx.t, ctx.mode, ctx.z_tf32 = t, mode, z_tf32
         return out
 
     @staticmethod
     def backward(ctx, g):
         z, p, y_fwd, p_t = ctx.saved_tensors
-        return _agnn_backward(ctx.t, ctx.mode, z, p, y_fwd, p_t, g), None, None
+        return _agnn_backward(ctx.t, ctx.mode, z, p, y_fwd, p_t, g, ctx.z_tf32), None, None, None
 
 
-def _agnn_backward(t: TiledGraph, mode: str, z, p, y_fwd, p_t, g):
+def _agnn_backward(t: TiledGraph, mode: str, z, p, y_fwd, p_t, g, z_tf32=False):
     """dZ of Y = spmm(A, P; Z) for the incoming gradient g: the A-side
     (dS = P (dP - rowsum), A_dS Z) and one dual SpMM on A^T (A^T_P G + A^T_dS Z)."""
     g = g.contiguous()
@@ -229,20 +234,22 @@ def _agnn_backward(t: TiledGraph, mode: str, z, p, y_fwd, p_t, g):
     if mode == "tf32":
         # dS and A_dS Z from one gather of Z's neighbour rows (dS also in A^T order)
         agnn_backward_device(t, z, g, p, ds=ds, out=out, y_fwd=y_fwd, ds_t=ds_t,
-                             inv_perm=_inv_perm(t) if ds_t is not None else None)
+                             inv_perm=_inv_perm(t) if ds_t is not None else None, z_tf32=z_tf32)
     else:
         sddmm_device(t, g, z, mode=mode, epilogue=_lib.EPI_SOFTMAX_BWD, aux=p, out=ds)
         spmm_device(t, z, ds, mode=mode, out=out)
     tt = t.transpose()
     # one dual SpMM on A^T: A^T_P G + A^T_dS Z
     if p_t is not None:
-        spmm_device(tt.tiled, g, p_t, x2=z, weights2=ds_t, mode=mode, out=out, accumulate=True)
+        spmm_device(tt.tiled, g, p_t, x2=z, weights2=ds_t, mode=mode, out=out, accumulate=True,
+                    x2_tf32=z_tf32)
     elif mode == "tf32" and not _PERMUTE_WEIGHTS:
         spmm_device(tt.tiled, g, p, weight_idx=tt.perm, x2=z, weights2=ds, weight_idx2=tt.perm,
-                    mode=mode, out=out, accumulate=True)
+                    mode=mode, out=out, accumulate=True, x2_tf32=z_tf32)
     else:
         pt, dst = permute2_device(p, ds, tt.perm)
-        spmm_device(tt.tiled, g, pt, x2=z, weights2=dst, mode=mode, out=out, accumulate=True)
+        spmm_device(tt.tiled, g, pt, x2=z, weights2=dst, mode=mode, out=out, accumulate=True,
+                    x2_tf32=z_tf32)
     return out
 
 
@@ -407,10 +414,12 @@ class AGNNConv(nn.Module):
         self.mode = mode
 
     def forward(self, x, t: TiledGraph, shard: Shard | None = None, key=None):
-        z = DenseFn.apply(x, self.weight, None, False)
         if shard is not None:  # x: this rank's rows
-            return AgnnAggShard.apply(z, shard, key, self.mode)
-        return AgnnAggregate.apply(z, t, self.mode)
+            return AgnnAggShard.apply(DenseFn.apply(x, self.weight, None, False), shard, key, self.mode)
+        # Z on the tf32 grid: every consumer (the fused forward, the A-side backward,
+        # the dual A^T SpMM) rounds it to tf32 anyway, so the results are unchanged
+        rz = self.mode == "tf32" and _Z_TF32
+        return AgnnAggregate.apply(DenseFn.apply(x, self.weight, None, False, rz), t, self.mode, rz)
 
 
 class GCN(nn.Module):

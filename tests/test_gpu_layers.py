@@ -138,7 +138,8 @@ def test_agnn_aggregate_next(env, kind):
             torch.cuda.synchronize()
         if fused and kind == "uniform":
             names = [e.name for e in prof.events()]
-            assert any("agnn_stream<0, true, false, true>" in nm or "agnn_stream<0, 1, 0, 1>" in nm
+            # agnn_stream<KIND=0, PAIR, MASK=false, NEXT=true, ZR>
+            assert any("agnn_stream<0, true, false, true" in nm or "agnn_stream<0, 1, 0, 1" in nm
                        for nm in names), names
         zn.backward(gz)
         res.append((zn.detach(), zt.grad, wt.grad))
@@ -212,3 +213,35 @@ def test_models_train_and_graph_capture(env):
         assert torch.equal(cap, eager)
         for p, q in zip(m2.parameters(), grads):
             assert torch.equal(p.grad, q)
+
+
+def test_agnn_z_tf32_bitwise():
+    """AGNNConv stores Z = X W on the tf32 grid (TCG_DENSE_OUT_TF32) and the
+    fused forward / A-side backward / dual A^T SpMM skip its operand rounding
+    (TCG_AGNN_Z_TF32, TCG_PREC_X2_TF32): the loss and every gradient are
+    bitwise those of the unflagged path, which rounds Z inside the kernels."""
+    import torch
+
+    import paper_2112_02052_b200 as tcg
+    from paper_2112_02052_b200 import layers
+
+    g = tcg.synth.gen_uniform(4000, 7, seed=11)
+    t = tcg.translate(g, tcg.BlockConfig(), device="cuda")
+    t.transpose()
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(g.num_nodes, 48, device="cuda", generator=gen)
+    lab = torch.randint(0, 9, (g.num_nodes,), device="cuda", generator=gen)
+    res = {}
+    saved = layers._Z_TF32
+    try:
+        for flag in (False, True):
+            layers._Z_TF32 = flag
+            net = layers.AGNN(48, 32, 9, layers=3).cuda()
+            loss = net.loss(x, t, lab)
+            loss.backward()
+            res[flag] = (loss.detach().clone(), [p.grad.clone() for p in net.parameters()])
+    finally:
+        layers._Z_TF32 = saved
+    assert torch.equal(res[False][0], res[True][0])
+    for a, b in zip(res[False][1], res[True][1]):
+        assert torch.equal(a, b)
