@@ -138,7 +138,7 @@ constexpr int kEPL = 5;    // edges per lane prefetched for the next window (160
 // the window-even-padded pair stream (tcg_block_stream_pairs), so the per-step
 // costs (ring wait, id copies, cursor updates, loop) are paid once per 1 KB of
 // staged rows, as at 32-wide chunks.
-template <int NT, bool DUAL, bool BIG = false, bool PAIR = false, int DMB = 8>
+template <int NT, bool DUAL, bool BIG = false, bool PAIR = false, int DMB = 8, int OCC = 1>
 struct Cfg {
   static constexpr int KB = PAIR ? 2 : 1;  // blocks per step
   // ring depth in steps: 4 blocks of 32-wide rows in flight either way
@@ -151,7 +151,9 @@ struct Cfg {
   static constexpr int OPS = DUAL ? 2 : 1;
   // dual form: DMB-block fragment rounds; 4 keeps a warp at 12.5 KB, 4 CTAs (16 warps)
   // per SM instead of 3 at 8, which pays on short windows (see stream_spmm)
-  static constexpr int MB = DUAL ? DMB : BIG ? 8 : 16;  // A-fragment blocks resident (one round)
+  // OCC 3 (16-wide pair steps on large graphs): 8-block rounds and <= 85 registers, three
+  // 8-warp CTAs per SM instead of two (amazon0601 D=16 61.4-63.5 -> 59.4 us cold)
+  static constexpr int MB = DUAL ? DMB : (BIG || OCC > 1) ? 8 : 16;  // A-fragment blocks resident (one round)
   static constexpr int STEP = SLOT * OPS * KB;     // staged bytes of one step
   static constexpr int RING = NB * STEP;
   static constexpr int IDX = NI * 32 * KB;         // column ids of NI steps
@@ -184,10 +186,10 @@ __device__ __forceinline__ int warp_lower_bound(const int32_t* __restrict__ a, i
   return lo + __popc(__ballot_sync(0xffffffffu, pr));
 }
 
-template <int NT, bool DUAL, bool BIG, bool MASK, bool PAIR = false, bool X2R = false, int DMB = 8>
-__global__ void __launch_bounds__(Cfg<NT, DUAL, BIG, PAIR, DMB>::WPC * 32, 1) spmm_stream(const Args a) {
+template <int NT, bool DUAL, bool BIG, bool MASK, bool PAIR = false, bool X2R = false, int DMB = 8, int OCC = 1>
+__global__ void __launch_bounds__(Cfg<NT, DUAL, BIG, PAIR, DMB, OCC>::WPC * 32, OCC) spmm_stream(const Args a) {
   TCG_PDL_ENTRY();
-  using C = Cfg<NT, DUAL, BIG, PAIR, DMB>;
+  using C = Cfg<NT, DUAL, BIG, PAIR, DMB, OCC>;
   constexpr int NB = C::NB, NI = C::NI, SLOT = C::SLOT, MB = C::MB, KB = C::KB;
   static_assert(!PAIR || (NT >= 2 && (!DUAL || NT == 4) && MB % 2 == 0), "pair steps: 16/32-wide");
   constexpr uint32_t RS = MB * 128;  // fragment slots of one round
@@ -1969,10 +1971,10 @@ __global__ void stream_pad_kernel(const int32_t* __restrict__ boff, int64_t W, u
   for (int q = threadIdx.x; q < 8 * TCG_STREAM_PAD; q += blockDim.x) cs[8 * tb + q] = fill;
 }
 
-template <int NT, bool DUAL, bool BIG, bool MASK, bool PAIR = false, bool X2R = false, int DMB = 8>
+template <int NT, bool DUAL, bool BIG, bool MASK, bool PAIR = false, bool X2R = false, int DMB = 8, int OCC = 1>
 int launch_t(Args& a, int nchunks, cudaStream_t s) {
-  using C = Cfg<NT, DUAL, BIG, PAIR, DMB>;
-  auto kern = spmm_stream<NT, DUAL, BIG, MASK, PAIR, X2R, DMB>;
+  using C = Cfg<NT, DUAL, BIG, PAIR, DMB, OCC>;
+  auto kern = spmm_stream<NT, DUAL, BIG, MASK, PAIR, X2R, DMB, OCC>;
   static int configured = -1;
   int dev = 0;
   TCG_CUDA(cudaGetDevice(&dev), "spmm_stream device");
@@ -2086,6 +2088,12 @@ int stream_spmm(const tcg_tiling* t, const win::Params& q, cudaStream_t s) {
       stream::Args ap = a;
       ap.boff = t->pair_offsets;
       ap.cs = t->pair_stream;
+      // large graphs (amazon0601-sized): three CTAs per SM; arxiv-sized ones measured
+      // neutral to slightly slower that way (GCN-2 epoch 0.191-0.199 vs 0.196-0.203 ms)
+      const bool occ3 = t->num_nodes >= 262144;
+      if (!big && occ3)
+        return mk ? stream::launch_t<2, false, false, true, true, false, 8, 3>(ap, nchunks, s)
+                  : stream::launch_t<2, false, false, false, true, false, 8, 3>(ap, nchunks, s);
       return big ? (mk ? stream::launch_t<2, false, true, true, true>(ap, nchunks, s)
                        : stream::launch_t<2, false, true, false, true>(ap, nchunks, s))
                  : (mk ? stream::launch_t<2, false, false, true, true>(ap, nchunks, s)
