@@ -288,7 +288,7 @@ class AgnnAggShard(torch.autograd.Function):
     A^T_P G + A^T_dS Z."""
 
     @staticmethod
-    def forward(ctx, z_local, sh: Shard, key, mode: str):
+    def forward(ctx, z_local, sh: Shard, key, mode: str, z_tf32: bool = False):
         d = z_local.shape[1]
         zbuf, zf, zmine = sh.rows_buffer(("z", key), d)
         zmine.copy_(z_local)
@@ -297,11 +297,11 @@ class AgnnAggShard(torch.autograd.Function):
         ebuf, pv, dsv = sh.edge_buffer(key)
         wr = sh.plan.my_windows
         if mode == "tf32":
-            agnn_forward_device(sh.t, zf, p=pv, out=yf, win_range=wr, y_row0=0)
+            agnn_forward_device(sh.t, zf, p=pv, out=yf, win_range=wr, y_row0=0, z_tf32=z_tf32)
         else:
             sddmm_device(sh.t, zf, mode=mode, epilogue=_lib.EPI_SOFTMAX, out=pv, win_range=wr)
             spmm_device(sh.t, zf, pv, mode=mode, out=yf, win_range=wr, y_row0=0)
-        ctx.sh, ctx.key, ctx.mode = sh, key, mode
+        ctx.sh, ctx.key, ctx.mode, ctx.z_tf32 = sh, key, mode, z_tf32
         return ymine.clone()
 
     @staticmethod
@@ -329,7 +329,7 @@ class AgnnAggShard(torch.autograd.Function):
         out = rows_empty(r1 - r0, d, g.device)
         if mode == "tf32":
             agnn_backward_device(sh.t, zf, gf, pv, ds=dsv, out=out, win_range=wr, y_row0=r0,
-                                 y_fwd=yf)
+                                 y_fwd=yf, z_tf32=ctx.z_tf32)
         else:
             sddmm_device(sh.t, gf, zf, mode=mode, epilogue=_lib.EPI_SOFTMAX_BWD, aux=pv, out=dsv,
                          win_range=wr)
@@ -345,8 +345,8 @@ class AgnnAggShard(torch.autograd.Function):
                 sh.perm_pad.data_ptr() + 4 * kb, pt.data_ptr() + 4 * kb, dst.data_ptr() + 4 * kb,
                 ke - kb, _lib.current_stream()), "tcg_permute2_f32")
         spmm_device(sh.tt, gf, pt, x2=zf, weights2=dst, mode=mode, out=out, accumulate=True,
-                    win_range=wr, y_row0=r0)
-        return out, None, None, None
+                    win_range=wr, y_row0=r0, x2_tf32=ctx.z_tf32)
+        return out, None, None, None, None
 
 
 def _glorot(fan_in, fan_out, gen=None):
@@ -414,12 +414,13 @@ class AGNNConv(nn.Module):
         self.mode = mode
 
     def forward(self, x, t: TiledGraph, shard: Shard | None = None, key=None):
-        if shard is not None:  # x: this rank's rows
-            return AgnnAggShard.apply(DenseFn.apply(x, self.weight, None, False), shard, key, self.mode)
         # Z on the tf32 grid: every consumer (the fused forward, the A-side backward,
         # the dual A^T SpMM) rounds it to tf32 anyway, so the results are unchanged
         rz = self.mode == "tf32" and _Z_TF32
-        return AgnnAggregate.apply(DenseFn.apply(x, self.weight, None, False, rz), t, self.mode, rz)
+        z = DenseFn.apply(x, self.weight, None, False, rz)
+        if shard is not None:  # x: this rank's rows
+            return AgnnAggShard.apply(z, shard, key, self.mode, rz)
+        return AgnnAggregate.apply(z, t, self.mode, rz)
 
 
 class GCN(nn.Module):
