@@ -413,11 +413,13 @@ def test_ws_gather_engine_opt_in(tmp_path):
     assert float(r.stdout.strip().splitlines()[-1]) <= TF32_REL_L2
 
 
-@pytest.mark.parametrize("dim", [8, 16, 32])
+@pytest.mark.parametrize("dim", [4, 8, 12, 16, 20, 32])
 def test_stream_sddmm_wide_windows(env, oracle, dim):
     """Products-like windows (~480 edges, up to ~900 with the hub rows): the
     wide SDDMM (u16 slot map rebuilt per 16-block round) with each epilogue,
-    against the oracle; the launch is sddmm_wide, not the window engine."""
+    against the oracle; the launch is sddmm_wide, not the window engine. D <= 16
+    runs the 16-wide staged layout (masked below 16), 16 < D < 32 the 32-wide one
+    masked."""
     tcg, kernels, _, torch = env
     from paper_2112_02052_b200 import _lib
 
