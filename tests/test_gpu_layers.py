@@ -245,3 +245,32 @@ def test_agnn_z_tf32_bitwise():
     assert torch.equal(res[False][0], res[True][0])
     for a, b in zip(res[False][1], res[True][1]):
         assert torch.equal(a, b)
+
+
+def test_operand_tf32_flags():
+    """TCG_DENSE_OUT_TF32 stores tcg_dense's output RN-rounded to tf32 (the
+    32 x 32 kernel in its epilogue, other shapes by a rounding pass), and
+    TCG_PREC_X2_TF32 on a dual SpMM of a pre-rounded x2 equals the unflagged
+    call bitwise."""
+    import torch
+
+    import paper_2112_02052_b200 as tcg
+    from paper_2112_02052_b200 import dense, kernels, tiles
+
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    for n, ci, co in ((5000, 32, 32), (4500, 128, 16), (700, 20, 12)):
+        x = torch.randn(n, ci, device="cuda", generator=gen)
+        w = torch.randn(ci, co, device="cuda", generator=gen)
+        y = dense.dense(dense.rows_ok(x), w)
+        yr = dense.dense(dense.rows_ok(x), w, out_tf32=True)
+        assert torch.equal(yr, tiles.quantize_tf32(y)), (n, ci, co)
+    g = tcg.synth.gen_uniform(3000, 7, seed=4)
+    t = tcg.translate(g, tcg.BlockConfig(), device="cuda")
+    a = torch.randn(g.num_nodes, 32, device="cuda", generator=gen)
+    b = dense.dense(dense.rows_ok(torch.randn(g.num_nodes, 32, device="cuda", generator=gen)),
+                    torch.randn(32, 32, device="cuda", generator=gen), out_tf32=True)
+    w1 = torch.rand(g.num_edges, device="cuda", generator=gen)
+    w2 = torch.rand(g.num_edges, device="cuda", generator=gen)
+    y0 = kernels.spmm_device(t, a, w1, x2=b, weights2=w2)
+    y1 = kernels.spmm_device(t, a, w1, x2=b, weights2=w2, x2_tf32=True)
+    assert torch.equal(y0, y1)
